@@ -1,0 +1,149 @@
+"""ctypes wrapper around oracle/genred_oracle.c -- TEST INFRASTRUCTURE ONLY.
+
+The C file holds all of the oracle's arithmetic (fp64, Neumaier sums, plain double loops; see
+its header for the paper passage each function follows).  This module only marshals arguments:
+it widens the (usually fp32) inputs to fp64 exactly and passes pointers.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+import threading
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_SRC = os.path.join(_HERE, "genred_oracle.c")
+_LIB = os.path.join(_HERE, "liboracle.so")
+_lock = threading.Lock()
+_lib = None
+
+
+def lib_path() -> str:
+    return _LIB
+
+
+def build(force: bool = False) -> str:
+    """Compile the oracle (gcc -O2 -fopenmp, no fast-math).  Building the checker is not using it."""
+    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+        tmp = _LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", "-O2", "-std=c11", "-fopenmp", "-fPIC", "-shared",
+                               "-fno-fast-math", "-o", tmp, _SRC, "-lm"])
+        os.replace(tmp, _LIB)
+    return _LIB
+
+
+def _load():
+    global _lib
+    with _lock:
+        if _lib is None:
+            build()
+            lib = ctypes.CDLL(_LIB)
+            P = ctypes.c_void_p
+            I64, I32, F64 = ctypes.c_int64, ctypes.c_int, ctypes.c_double
+            lib.oracle_num_threads.restype = I32
+            lib.oracle_gauss_sum.argtypes = [I64, I64, I32, I32, F64, P, P, P, P, I64, P, P]
+            lib.oracle_gauss_gradx.argtypes = [I64, I64, I32, I32, F64, P, P, P, P, P, I64, P, P]
+            lib.oracle_lse.argtypes = [I64, I64, I32, F64, P, P, P, P, I64, P, P]
+            lib.oracle_argkmin.argtypes = [I64, I64, I32, I32, P, P, P, I64, P, P]
+            lib.oracle_sqdist_sum.argtypes = [I64, I64, I32, I32, P, P, P, P, I64, P, P]
+            for f in ("oracle_gauss_sum", "oracle_gauss_gradx", "oracle_lse", "oracle_argkmin",
+                      "oracle_sqdist_sum"):
+                getattr(lib, f).restype = None
+            _lib = lib
+    return _lib
+
+
+def num_threads() -> int:
+    return int(_load().oracle_num_threads())
+
+
+def _f64(a, ncols=None):
+    if a is None:
+        return None
+    a = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    if ncols is not None:
+        a = a.reshape(-1, ncols)
+    return a
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data
+
+
+def _rows(rows):
+    if rows is None:
+        return None, 0
+    r = np.ascontiguousarray(np.asarray(rows, dtype=np.int64))
+    return r, int(r.shape[0])
+
+
+def gauss_sum(x, y, b=None, sigma=1.0, rows=None):
+    """O1.  Returns (a [R,E], denom [R,E]) in fp64."""
+    x = _f64(x); y = _f64(y)
+    M, D = x.shape; N = y.shape[0]
+    b = _f64(b)
+    E = 1 if b is None else (b.shape[1] if b.ndim == 2 else 1)
+    r, nr = _rows(rows)
+    R = nr if r is not None else M
+    out = np.empty((R, E)); den = np.empty((R, E))
+    _load().oracle_gauss_sum(M, N, D, E, float(sigma), _ptr(x), _ptr(y), _ptr(b), _ptr(r), nr,
+                             _ptr(out), _ptr(den))
+    return out, den
+
+
+def gauss_gradx(x, y, b=None, g=None, sigma=1.0, rows=None):
+    """O2.  Returns (G [R,D], denom [R,D]) in fp64."""
+    x = _f64(x); y = _f64(y)
+    M, D = x.shape; N = y.shape[0]
+    b = _f64(b); g = _f64(g)
+    E = 1
+    if b is not None:
+        E = b.shape[1] if b.ndim == 2 else 1
+    elif g is not None:
+        E = g.shape[1] if g.ndim == 2 else 1
+    r, nr = _rows(rows)
+    R = nr if r is not None else M
+    out = np.empty((R, D)); den = np.empty((R, D))
+    _load().oracle_gauss_gradx(M, N, D, E, float(sigma), _ptr(x), _ptr(y), _ptr(b), _ptr(g),
+                               _ptr(r), nr, _ptr(out), _ptr(den))
+    return out, den
+
+
+def lse(x, y, h=None, eps=1.0, rows=None):
+    """O3.  Returns (a [R], m [R]) in fp64; m_i = max_j F_ij."""
+    x = _f64(x); y = _f64(y)
+    M, D = x.shape; N = y.shape[0]
+    h = None if h is None else _f64(h).reshape(-1)
+    r, nr = _rows(rows)
+    R = nr if r is not None else M
+    out = np.empty(R); mm = np.empty(R)
+    _load().oracle_lse(M, N, D, float(eps), _ptr(x), _ptr(y), _ptr(h), _ptr(r), nr,
+                       _ptr(out), _ptr(mm))
+    return out, mm
+
+
+def argkmin(x, y, K, rows=None):
+    """O4.  Returns (d [R,K] fp64 squared distances, j [R,K] int64), ascending in (d, j)."""
+    x = _f64(x); y = _f64(y)
+    M, D = x.shape; N = y.shape[0]
+    r, nr = _rows(rows)
+    R = nr if r is not None else M
+    dist = np.empty((R, K)); idx = np.empty((R, K), dtype=np.int64)
+    _load().oracle_argkmin(M, N, D, int(K), _ptr(x), _ptr(y), _ptr(r), nr, _ptr(dist), _ptr(idx))
+    return dist, idx
+
+
+def sqdist_sum(x, y, b=None, rows=None):
+    """O5.  Returns (a [R,E], denom [R,E])."""
+    x = _f64(x); y = _f64(y)
+    M, D = x.shape; N = y.shape[0]
+    b = _f64(b)
+    E = 1 if b is None else (b.shape[1] if b.ndim == 2 else 1)
+    r, nr = _rows(rows)
+    R = nr if r is not None else M
+    out = np.empty((R, E)); den = np.empty((R, E))
+    _load().oracle_sqdist_sum(M, N, D, E, _ptr(x), _ptr(y), _ptr(b), _ptr(r), nr,
+                              _ptr(out), _ptr(den))
+    return out, den
