@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""bench.py -- pair-evaluations/s of the Genred hot path on B200 (BASELINE.json ``metric``).
+
+Default workload (N=1): configuration C5 of BASELINE.json, the one the metric is quoted on:
+Gaussian Genred Sum a_i = sum_j exp(-|x_i - y_j|^2/sigma^2) b_j, M = N = 1e7, D = 3, E = 1,
+sigma = 0.5, x, y ~ U[0,1)^3, b ~ U[0,1) (synthetic, seeded).
+
+A step = one genred_eval (pack j-records -> pair-loop kernel -> fixed-order merge) over the whole
+problem.  With --gpus N (torchrun, one process per GPU, NCCL) the i-range is sharded: each step
+broadcasts y and b from rank 0 and every rank reduces its M/N rows (strong scaling of the fixed
+1e14-pair problem; no reduction collective is needed, north star (d)).
+
+Timing: W warm-up steps; then K steps bracketed by barrier + cuda synchronize, CUDA events on
+the launching stream, max over ranks.  Inputs (280 MB) exceed the 126 MB L2, so no flush.
+Extra keys: roofline (dominant kernel, live CUDA-event timing through genred_profile),
+cpu_baseline (the fp64 oracle on a bounded row sample, rank 0 at N=1), e2e (host buffers through
+the C ABI's host mode, H2D + D2H inside the timed region), clocks (NVML sampled during the timed
+region), gpu_launches (libgenred kernels launched in the timed region, all ranks).
+
+``--impl reference``: there is no reference implementation (PAPER.md only); the reference arm
+is the fp64 oracle (oracle/) timed on this host's cores on a bounded row sample of the same
+workload -- a deliberately slow baseline, not a target.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+import synth  # noqa: E402
+
+METRIC = "pair-evals/sec (M·N/s) Gaussian Genred Sum D=3 at 1/2/4/8 B200; % FP32/MUFU peak"
+UNIT = "pairs/s"
+SMS = 148
+MUFU_PER_CLK_SM = 16          # MUFU.EX2 lanes per clock per SM (sm_100)
+FP32_PER_CLK_SM = 128         # FP32 lanes per clock per SM (FFMA/FADD/FMUL; FFMA2 counts 2)
+
+
+def measured_peaks() -> dict:
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            return json.load(f)
+    return {}
+
+
+def workload(cid: int) -> dict:
+    """Per-config step definition: formula, algorithmic FP32 lane-ops and exps per pair (D=3)."""
+    c = synth.config(cid)
+    if cid in (1, 5):
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=7, mufu=1, out_dtype="float32")
+    if cid == 2:   # Sum + gradient in one fused pass: 7 + (w=e*b) + 3 grad FMA + sum add = 12
+        return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=12, mufu=1,
+                    out_dtype="float32")
+    if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
+        return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
+    raise SystemExit(f"config {cid} is not benchmarked yet")
+
+
+def alu_peak_pairs(fp32: int, mufu: int, mhz: float) -> float:
+    """Pairs/s ceiling of the FP32 + MUFU pipes for an algorithmic mix."""
+    per_clk = min(MUFU_PER_CLK_SM / mufu, FP32_PER_CLK_SM / fp32)
+    return per_clk * SMS * mhz * 1e6
+
+
+class ClockSampler:
+    """NVML SM-clock / throttle-reason sampler running during the timed region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+               0x8: "hw_slowdown", 0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown",
+               0x80: "hw_power_brake_slowdown", 0x100: "display_clock_setting"}
+
+    def __init__(self, device: int, period: float = 0.2):
+        self.device, self.period = device, period
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        self._t = None
+
+    def start(self):
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            h = pynvml.nvmlDeviceGetHandleByIndex(self.device)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            return self
+
+        def run():
+            while not self._stop.is_set():
+                try:
+                    self.samples.append(pynvml.nvmlDeviceGetClockInfo(h, pynvml.NVML_CLOCK_SM))
+                    r = pynvml.nvmlDeviceGetCurrentClocksEventReasons(h)
+                    for bit, name in self.REASONS.items():
+                        if r & bit and bit != 0x1:
+                            self.reasons.add(name)
+                except Exception:
+                    pass
+                self._stop.wait(self.period)
+
+        self._t = threading.Thread(target=run, daemon=True)
+        self._t.start()
+        return self
+
+    def stop(self) -> dict:
+        self._stop.set()
+        if self._t:
+            self._t.join()
+        med = statistics.median(self.samples) if self.samples else None
+        return {"sm_mhz": med, "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def ncu_traffic(cid: int):
+    """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
+    p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    return d.get(f"C{cid}")
+
+
+def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
+    """The fp64 oracle as it stands, on a bounded row sample of the same workload."""
+    import oracle
+    c = w["cfg"]
+    t0 = time.perf_counter()
+    if w["reduction"] == "lse":
+        o, _ = oracle.lse(x, y, None, eps=c.scale, rows=rows)
+        den = None
+    elif w["formula"] == "gauss_sum_gradx":
+        o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+        oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
+    else:
+        o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+    dt = time.perf_counter() - t0
+    res = {"value": len(rows) * c.N / dt, "unit": UNIT, "cores": oracle.num_threads(),
+           "kind": "oracle", "seconds": round(dt, 3),
+           "sample": f"{len(rows)} seeded rows x all N={c.N} (fp64, OpenMP, Neumaier)"}
+    if gpu_rows is not None:
+        if den is not None:
+            err = np.abs(np.asarray(gpu_rows, np.float64).reshape(o.shape) - o) / np.maximum(den, 1e-30)
+            res["max_r4_err_vs_gpu"] = float(err.max())
+        else:
+            res["max_abs_err_vs_gpu"] = float(np.abs(np.asarray(gpu_rows, np.float64).reshape(o.shape) - o).max())
+    return res
+
+
+def make_inputs(w: dict, dist_kind: str):
+    c = w["cfg"]
+    sd = synth.seeds(c.cid)
+    xk = dist_kind if w["reduction"] != "lse" else c.x_dist
+    yk = dist_kind if w["reduction"] != "lse" else c.y_dist
+    x = synth.points(xk, c.M, sd["x"], c.D)
+    y = synth.points(yk, c.N, sd["y"], c.D)
+    b = synth.signal(c.N, sd["b"], c.E) if w["reduction"] == "sum" else None
+    return x, y, b
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    import oracle
+    w = workload(args.config)
+    c = w["cfg"]
+    x, y, b = make_inputs(w, args.dist)
+    rows_per_step = max(1, int(args.ref_pairs // c.N))
+    rng = np.random.default_rng(12345)
+
+    def step():
+        rows = np.sort(rng.choice(c.M, size=rows_per_step, replace=False))
+        if w["reduction"] == "lse":
+            oracle.lse(x, y, None, eps=c.scale, rows=rows)
+        elif w["formula"] == "gauss_sum_gradx":
+            oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+            oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
+        else:
+            oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = time.perf_counter() - t0
+    pairs = rows_per_step * c.N * args.steps
+    value = pairs / dt
+    cores = oracle.num_threads()
+    sample = f"{rows_per_step} seeded rows x all N={c.N} per step (fp64 oracle, OpenMP)"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": c.name, "M": c.M, "N": c.N, "D": c.D, "E": c.E, "scale": c.scale,
+                   "dist": args.dist, "parallelism": "host cores (rank 0 only)"},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--dist", default="U3", choices=["U3", "GMM3"])
+    ap.add_argument("--cpu-rows", type=int, default=1024, help="oracle sample rows (cpu_baseline)")
+    ap.add_argument("--ref-pairs", type=float, default=1e9, help="oracle pairs per reference step")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu", action="store_true")
+    args = ap.parse_args()
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import torch.distributed as dist
+    from paper_2004_11127_b200 import genred
+
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = workload(args.config)
+    c = w["cfg"]
+    M, N = c.M, c.N
+    lo, hi = M * rank // world, M * (rank + 1) // world
+    x, y, b = make_inputs(w, args.dist)
+    xl = np.ascontiguousarray(x[lo:hi])
+    dev = torch.device("cuda", local)
+    xd = torch.from_numpy(xl).to(dev)
+    yd = torch.from_numpy(y).to(dev) if rank == 0 else torch.empty(y.shape, dtype=torch.float32, device=dev)
+    bd = None
+    if b is not None:
+        bd = torch.from_numpy(b).to(dev) if rank == 0 else torch.empty(b.shape, dtype=torch.float32, device=dev)
+    Ml = hi - lo
+    out_shape = (Ml,) if w["reduction"] == "lse" else (Ml, c.E)
+    out = torch.empty(out_shape, dtype=getattr(torch, w["out_dtype"]), device=dev)
+    out_grad = torch.empty((Ml, c.D), dtype=torch.float32, device=dev) \
+        if w["formula"] == "gauss_sum_gradx" else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        if world > 1:                                   # X1: y (and b) broadcast once per step
+            dist.broadcast(yd, src=0)
+            if bd is not None:
+                dist.broadcast(bd, src=0)
+        genred.eval(w["formula"], w["reduction"], xd, yd, bd, None, scale=c.scale, out=out,
+                    out_dtype=w["out_dtype"], out_grad=out_grad, stream=stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sum_over_ranks(v: float) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    # ---------------- device-resident timed region ----------------
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    plan = genred.last_plan(local)
+    sampler = ClockSampler(local).start()
+    genred.profile(True, local)
+    l0 = genred.launch_count(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    launches = genred.launch_count(local) - l0
+    kms = genred.profile_read(local)
+    genred.profile(False, local)
+    barrier()
+    ms_total = max_over_ranks(ev0.elapsed_time(ev1))
+    launches = int(sum_over_ranks(launches))
+    ms_step = ms_total / args.steps
+    value = M * N * args.steps / (ms_total * 1e-3)
+
+    # dominant kernel roofline (this rank's launches; the slowest rank bounds the job)
+    kmean = statistics.mean(kms) if kms else float("nan")
+    kmean = max_over_ranks(kmean)
+    peaks = measured_peaks()
+    mhz_max = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
+    peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
+    achieved = Ml * N / (kmean * 1e-3)
+    traffic = ncu_traffic(args.config)
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
+                "frac": achieved / peak, "traffic": traffic,
+                "kernel": f"{w['formula']}/{w['reduction']} pair loop", "kernel_ms": kmean,
+                "share_of_step": kmean / ms_step if world == 1 else None,
+                "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
+                              f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                "pairs_per_launch": Ml * N}
+
+    # ---------------- end-to-end: host buffers through the C ABI (H2D + D2H inside) ----------------
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(xl).pin_memory()
+        yh = torch.from_numpy(y).pin_memory()
+        bh = torch.from_numpy(b).pin_memory() if b is not None else None
+        oh = torch.empty(out_shape, dtype=getattr(torch, w["out_dtype"])).pin_memory()
+        gh = torch.empty((Ml, c.D), dtype=torch.float32).pin_memory() if out_grad is not None else None
+        a = genred.Args()
+        a.abi_version = genred.ABI_VERSION
+        a.formula, a.reduction = genred.FORMULAS[w["formula"]], genred.REDUCTIONS[w["reduction"]]
+        a.memory = genred.MEM_HOST
+        a.M, a.N, a.D, a.E, a.K, a.scale = Ml, N, c.D, c.E, 1, c.scale
+        a.x, a.y = xh.data_ptr(), yh.data_ptr()
+        a.b = bh.data_ptr() if bh is not None else None
+        a.out = oh.data_ptr()
+        a.out_dtype = genred.F64 if w["out_dtype"] == "float64" else genred.F32
+        a.out_grad = gh.data_ptr() if gh is not None else None
+        genred.eval_args(a, stream=stream)                      # warm the staging buffers
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            genred.eval_args(a, stream=stream)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        e2e_ms = max_over_ranks(e0.elapsed_time(e1))
+        h2d = xh.numel() * 4 + yh.numel() * 4 + (bh.numel() * 4 if bh is not None else 0)
+        d2h = oh.numel() * oh.element_size() + (gh.numel() * 4 if gh is not None else 0)
+        e2e = {"value": M * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
+               "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
+               "ms_per_step": e2e_ms / args.steps, "api": "genred_eval(memory=GENRED_MEM_HOST)"}
+
+    # ---------------- fp64 oracle on the host cores (rank 0, N=1 only) ----------------
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu:
+        rows = np.sort(np.random.default_rng(777).choice(M, size=min(args.cpu_rows, M), replace=False))
+        cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=out.cpu().numpy()[rows])
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": c.name, "M": M, "N": N, "D": c.D, "E": c.E, "scale": c.scale,
+                       "dist": args.dist if w["reduction"] != "lse" else f"x {c.x_dist}, y {c.y_dist}",
+                       "b": "U[0,1)" if b is not None else None,
+                       "parallelism": f"ishard{world}" if world > 1 else "single",
+                       "l2": "inputs larger than L2 (280 MB vs 126 MB); no flush" if c.cid == 5 else
+                             "inputs re-read from HBM/L2 each step; no flush",
+                       "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"],
+                       "ctas": plan["ctas"]},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches,
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,167 @@
+/*
+ * genred.h -- C ABI of libgenred, the B200 (sm_100a) Genred hot path.
+ *
+ * The paper's problem statement (Sec. 2, Eq. 1): given parameters p, i-variables
+ * x_i (i = 1..M), j-variables y_j (j = 1..N), a formula F and a reduction, evaluate
+ *
+ *        a_i = Reduction_{j=1..N} F(p, x_i, y_j)          "with a linear memory footprint".
+ *
+ * libgenred evaluates Eq. (1) for a FIXED formula set (the Gaussian kernel
+ * product Scal<Exp<Minus<SqDist<X,Y>>>,B>; its gradient; the squared
+ * distance) and the reductions Sum, log-sum-exp and ArgKMin.  Nothing of
+ * size M*N is ever allocated: library scratch is O((M+N)*(D+E)).
+ *
+ * Conventions (every entry point):
+ *   - Data pointers are fp32 row-major contiguous unless stated; by default they are DEVICE
+ *     pointers (GENRED_MEM_DEVICE).  With GENRED_MEM_HOST, x/y/b/g/out/out_idx/lse_state are
+ *     HOST pointers: the call stages them through context-owned device buffers (H2D, compute,
+ *     D2H on `stream`) and returns only after the results are in host memory.
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *   - Ownership: the caller owns every pointer and the stream.  The library reads x, y, b, g and
+ *     writes only out, out_idx, out_grad and lse_state.  Device-mode calls are asynchronous:
+ *     they return after enqueue and the buffers must stay live until the stream passes.
+ *   - Errors: return codes only (no abort, no C++ exception crosses the ABI).  Validation is
+ *     synchronous and happens before any launch; on error nothing is written.  The message of
+ *     the last failure on a context is returned by genred_last_error().  Asynchronous device
+ *     faults surface at the caller's next synchronisation.
+ *   - NaN / Inf inputs propagate under IEEE semantics and are not checked.
+ *   - A context is used by one host thread at a time; distinct contexts are independent.
+ */
+#ifndef GENRED_H
+#define GENRED_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GENRED_ABI_VERSION 1
+
+typedef struct genred_ctx genred_ctx;
+
+typedef enum {
+    GENRED_OK = 0,
+    GENRED_E_INVALID = 1,      /* bad argument value / null pointer / misalignment */
+    GENRED_E_UNSUPPORTED = 2,  /* (formula, reduction, D, E, K) not in the supported set */
+    GENRED_E_SHAPE = 3,        /* negative sizes, D/E/K out of range */
+    GENRED_E_NOMEM = 4,        /* scratch allocation failed */
+    GENRED_E_CUDA = 5          /* a CUDA runtime call or launch failed (message has the reason) */
+} genred_status;
+
+/* Formulas F (readings R1, R2, R5, R10 in DESIGN.md):
+ *   GAUSS           F_ij = exp(-|x_i - y_j|^2 / sigma^2) * b_j                 (E outputs)
+ *   GAUSS_GRADX     F_ij = d/dx_i of the above, contracted with the cotangent g_i:
+ *                   (-2/sigma^2) (x_i - y_j) exp(-|x_i-y_j|^2/sigma^2) <b_j, g_i>  (D outputs)
+ *   GAUSS_SUM_GRADX both of the above in one pass (out: M x E sum, out_grad: M x D gradient)
+ *   SQDIST          F_ij = |x_i - y_j|^2; under LSE: F_ij = -|x_i - y_j|^2 / eps + h_j,
+ *                   with h = b (N values, E = 1; NULL means h = 0).                          */
+typedef enum {
+    GENRED_GAUSS = 0,
+    GENRED_GAUSS_GRADX = 1,
+    GENRED_SQDIST = 2,
+    GENRED_GAUSS_SUM_GRADX = 3
+} genred_formula;
+
+/* Reductions:
+ *   SUM      a_i = sum_j F_ij
+ *   LSE      a_i = log sum_j exp(F_ij)   (natural log; max-shifted, streaming)
+ *   ARGKMIN  the K smallest (F_ij, j) in lexicographic order (ties -> lowest j), ascending.   */
+typedef enum { GENRED_SUM = 0, GENRED_LSE = 1, GENRED_ARGKMIN = 2 } genred_reduction;
+
+typedef enum { GENRED_F32 = 0, GENRED_F64 = 1 } genred_dtype;
+
+typedef enum { GENRED_MEM_DEVICE = 0, GENRED_MEM_HOST = 1 } genred_memory;
+
+/* Supported (formula, reduction) pairs and shapes:
+ *   (GAUSS, SUM), (GAUSS_GRADX, SUM), (GAUSS_SUM_GRADX, SUM): 1 <= D <= 8, 1 <= E <= 4
+ *   (SQDIST, SUM): 1 <= D <= 8, 1 <= E <= 4 (closed-form test combination)
+ *   (SQDIST, LSE): 1 <= D <= 8, E == 1
+ *   (SQDIST, ARGKMIN): 1 <= K <= 32 with 1 <= D <= 16 (FP32 path), or D >= 32, D % 4 == 0
+ *                      (tensor-core path, x and y rows 16-byte aligned), E == 1
+ * Anything else -> GENRED_E_UNSUPPORTED.                                                        */
+typedef struct {
+    int32_t abi_version;     /* must equal GENRED_ABI_VERSION */
+    int32_t formula;         /* genred_formula */
+    int32_t reduction;       /* genred_reduction */
+    int32_t memory;          /* genred_memory: DEVICE (default 0) or HOST pointers */
+    int64_t M, N;            /* rows of x (i-variables) and of y (j-variables); >= 0 */
+    int32_t D, E, K;         /* point dimension, signal dimension, K of ArgKMin (else ignored) */
+    int32_t split_j;         /* 0 = automatic; >= 1 forces the number of j-splits (tests) */
+    double  scale;           /* sigma (GAUSS*) or eps (SQDIST+LSE); finite and > 0; ignored otherwise */
+    const float *x;          /* M x D */
+    const float *y;          /* N x D */
+    const float *b;          /* N x E signal (GAUSS*, SQDIST+SUM; NULL means b = 1 with E = 1),
+                                or h (N values) for SQDIST+LSE (NULL means h = 0)           */
+    const float *g;          /* M x E cotangent for *_GRADX (NULL means g = 1) */
+    void    *out;            /* SUM: M x E | GAUSS_GRADX: M x D | LSE: M | ARGKMIN: M x K
+                                squared distances (always fp32 for ARGKMIN)                   */
+    int32_t  out_dtype;      /* genred_dtype of `out` (SUM/GRADX/LSE); F64 recommended for LSE */
+    int32_t  pad0;
+    float   *out_grad;       /* GAUSS_SUM_GRADX only: M x D fp32 gradient */
+    int64_t *out_idx;        /* ARGKMIN: M x K, 0-based j (+ j_offset); pad -1 (d = +inf) if K > N */
+    double  *lse_state;      /* optional, LSE only: M x 2 (m_i in log2 units, s_i) so that
+                                a_i = ln2 * (m_i + log2 s_i); input of genred_combine_lse      */
+    int64_t  j_offset;       /* added to every reported index (j-sharded evaluation) */
+} genred_args;
+
+/* Library-level information. */
+int32_t     genred_abi_version(void);
+const char *genred_build_info(void);                 /* compile flags, target arch */
+
+/* Context: one per CUDA device; owns the scratch arena (packed j-records, split-j partials,
+ * host-mode staging buffers), grown geometrically, freed by genred_destroy. */
+genred_status genred_create(int32_t cuda_device, genred_ctx **out);
+void          genred_destroy(genred_ctx *ctx);
+const char   *genred_last_error(const genred_ctx *ctx);
+
+/* Host-only argument check (no GPU needed): returns the status genred_eval would return from
+ * validation, and writes a message into msg[0..msg_len) (may be NULL). */
+genred_status genred_validate(const genred_args *args, char *msg, size_t msg_len);
+
+/* Evaluate Eq. (1) for `args` on `stream` (see conventions above). */
+genred_status genred_eval(genred_ctx *ctx, const genred_args *args, void *stream);
+
+/* Merge G partial log-sum-exp states (G x M x 2 doubles, as written to lse_state) of one set of
+ * rows, e.g. from G j-shards: (m, s)_1 (+) (m, s)_2 = (m*, s_1 2^(m_1-m*) + s_2 2^(m_2-m*)),
+ * m* = max(m_1, m_2) (reduction_monoids merge).  Writes a_i (natural log) to
+ * `out` (M values, dtype) and, if state_out != NULL, the merged state (M x 2).  Device pointers. */
+genred_status genred_combine_lse(genred_ctx *ctx, int64_t M, int32_t G, const double *states,
+                                 void *out, int32_t out_dtype, double *state_out, void *stream);
+
+/* Merge G sorted K-lists per row (G x M x K distances and indices, each list ascending in (d, j))
+ * into the K smallest under (d, j) lexicographic order (ArgKMin merge).
+ * Device pointers. */
+genred_status genred_merge_topk(genred_ctx *ctx, int64_t M, int32_t K, int32_t G,
+                                const float *d, const int64_t *idx,
+                                float *d_out, int64_t *idx_out, void *stream);
+
+/* Introspection for tests and the benchmark. */
+typedef struct {
+    int32_t split_j;         /* j-splits used by the last genred_eval */
+    int32_t rows_per_cta;    /* i-rows owned by one CTA */
+    int32_t ctas;            /* CTAs launched by the main kernel */
+    int32_t tile_j;          /* j-records per shared-memory stage */
+    int32_t kernels;         /* kernels launched by the last call */
+    int32_t path;            /* 0 = FP32/MUFU small-D path, 1 = tcgen05 tensor path */
+    int64_t scratch_bytes;   /* device scratch currently held by the context */
+} genred_plan;
+genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan);
+
+/* Total kernels launched by this context since creation (evidence for the bench's
+ * gpu_launches claim). */
+int64_t genred_launch_count(const genred_ctx *ctx);
+
+/* Live timing of the dominant kernel for the benchmark's roofline: while enabled, every
+ * genred_eval records a pair of CUDA events (owned by the context) on its stream around its
+ * main pair-loop kernel, for up to 4096 launches.  genred_profile(ctx, 0) disables and clears.
+ * genred_profile_read waits for the recorded events and writes up to `max` durations (ms) in
+ * launch order; it returns the number written (or -1 on a CUDA error). */
+genred_status genred_profile(genred_ctx *ctx, int32_t enable);
+int32_t       genred_profile_read(genred_ctx *ctx, float *ms, int32_t max);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GENRED_H */

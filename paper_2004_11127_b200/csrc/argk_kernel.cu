@@ -1,0 +1,240 @@
+// argk_kernel.cu -- ArgKMin over squared distances on the FP32 pipe, small D (
+// k-nearest neighbours):
+//
+//     a_i = the K smallest (|x_i - y_j|^2, j) in lexicographic order (ties -> lowest j, R7)
+//
+// Same pipeline as sum_kernel.cu (bulk-copy ring of 512-record j-tiles, rows in registers).
+// Per j-pair: packed FADD2/FMUL2/FFMA2 distance, one FMNMX + FSETP against the current K-th
+// best; a hit (about K ln(N/K) times per row) runs an unrolled compare-swap insertion into the
+// register-resident sorted list.  Within one thread j arrives in ascending order, so strict '<'
+// realises the (d, j) order; split-j lists are merged lexicographically by topk_merge.
+#include <math.h>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace genred {
+
+template <int D>
+struct ArgkCfg {
+    static constexpr int RS = ((2 * D) + 3) / 4 * 4;
+    static constexpr int PAIRS = kTileJ / 2;
+    static constexpr int TILE_FLOATS = PAIRS * RS;
+    static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
+    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+};
+
+struct ArgkParams {
+    const float *x, *J;
+    int64_t M;
+    int K;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float *dist;
+    int64_t *idx;
+    int64_t j_offset;
+    float *pdist;
+    int32_t *pidx;
+};
+
+template <int KMAX>
+__device__ __forceinline__ void topk_insert(float (&dist)[KMAX], int32_t (&idx)[KMAX], int K,
+                                            float cd, int32_t cj, float &kth) {
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k) {
+        if (k < K) {
+            const bool sw = cd < dist[k];
+            const float td = dist[k];
+            const int32_t tj = idx[k];
+            dist[k] = sw ? cd : td;
+            idx[k] = sw ? cj : tj;
+            cd = sw ? td : cd;
+            cj = sw ? tj : cj;
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < KMAX; ++k)
+        if (k == K - 1) kth = dist[k];
+}
+
+template <int D, int KMAX, int R>
+__global__ void __launch_bounds__(kThreads, 1) argk_kernel(const ArgkParams p) {
+    using Cfg = ArgkCfg<D>;
+    constexpr int RS = Cfg::RS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
+    uint64_t *empty = full + kStages;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
+    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+    const int nt = (int)(t1 - t0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
+            for (int k = 0; k < nt; ++k) {
+                const int s = k % kStages;
+                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
+                         Cfg::STAGE_BYTES, &full[s]);
+            }
+        }
+        return;
+    }
+
+    const int ct = threadIdx.x;
+    const int K = p.K;
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    float xr[R][D];
+    float dist[R][KMAX];
+    int32_t idx[R][KMAX];
+    float kth[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        const bool ok = i < p.M;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xr[r][d] = ok ? __ldg(p.x + i * D + d) : 0.0f;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) { dist[r][k] = INFINITY; idx[r][k] = -1; }
+        kth[r] = INFINITY;
+    }
+
+    for (int k = 0; k < nt; ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full[s], (k / kStages) & 1);
+        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+        const int32_t jbase = (int32_t)((t0 + k) * kTileJ);
+#pragma unroll 2
+        for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
+            float f[RS];
+#pragma unroll
+            for (int u = 0; u < RS / 4; ++u) {
+                const float4 v = lds128(tile + pp * RS + 4 * u);
+                f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 dd = add2(dup2(xr[r][0]), make_float2(f[0], f[1]));
+                float2 q = mul2(dd, dd);
+#pragma unroll
+                for (int d = 1; d < D; ++d) {
+                    dd = add2(dup2(xr[r][d]), make_float2(f[2 * d], f[2 * d + 1]));
+                    q = fma2(dd, dd, q);
+                }
+                if (fminf(q.x, q.y) < kth[r]) {
+                    const int32_t j0 = jbase + 2 * pp;
+                    if (q.x < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.x, j0, kth[r]);
+                    if (q.y < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.y, j0 + 1, kth[r]);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= p.M) continue;
+#pragma unroll
+        for (int k = 0; k < KMAX; ++k) {
+            if (k >= K) break;
+            if (p.split > 1) {
+                const int64_t off = ((int64_t)sp * p.M + i) * K + k;
+                p.pdist[off] = dist[r][k];
+                p.pidx[off] = idx[r][k];
+            } else {
+                p.dist[i * K + k] = dist[r][k];
+                p.idx[i * K + k] = idx[r][k] < 0 ? -1 : (int64_t)idx[r][k] + p.j_offset;
+            }
+        }
+    }
+}
+
+template <int KMAX>
+constexpr int argk_rows() { return KMAX <= 4 ? 2 : 1; }
+
+template <int D, int KMAX>
+static cudaError_t run_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
+    using Cfg = ArgkCfg<D>;
+    constexpr int R = argk_rows<KMAX>();
+    auto kern = argk_kernel<D, KMAX, R>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    ArgkParams p;
+    p.x = a.x; p.J = a.J; p.M = a.M; p.K = a.K; p.split = a.split;
+    p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.dist = a.dist; p.idx = a.idx;
+    p.j_offset = a.j_offset; p.pdist = a.pdist; p.pidx = a.pidx;
+    const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
+    const int64_t grid = ((a.M + rows - 1) / rows) * a.split;
+    *ctas = (int)grid;
+    kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D, int KMAX>
+static int occ_argk() {
+    using Cfg = ArgkCfg<D>;
+    auto kern = argk_kernel<D, KMAX, argk_rows<KMAX>()>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+template <int D>
+static cudaError_t run_argk_k(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
+    if (a.K <= 1) return run_argk<D, 1>(a, st, ctas);
+    if (a.K <= 4) return run_argk<D, 4>(a, st, ctas);
+    if (a.K <= 16) return run_argk<D, 16>(a, st, ctas);
+    return run_argk<D, 32>(a, st, ctas);
+}
+template <int D>
+static int occ_argk_k(int K) {
+    if (K <= 1) return occ_argk<D, 1>();
+    if (K <= 4) return occ_argk<D, 4>();
+    if (K <= 16) return occ_argk<D, 16>();
+    return occ_argk<D, 32>();
+}
+
+int argk_rows_per_thread(int K) { return K <= 4 ? 2 : 1; }
+
+#define GENRED_ARGK_D(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
+
+cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
+#define GENRED_CASE(DD) if (a.D == DD) return run_argk_k<DD>(a, st, ctas);
+    GENRED_ARGK_D(GENRED_CASE)
+#undef GENRED_CASE
+    return cudaErrorInvalidValue;
+}
+
+int argk_occupancy(int D, int K, int R) {
+    (void)R;
+#define GENRED_CASE(DD) if (D == DD) return occ_argk_k<DD>(K);
+    GENRED_ARGK_D(GENRED_CASE)
+#undef GENRED_CASE
+    return 1;
+}
+
+}  // namespace genred

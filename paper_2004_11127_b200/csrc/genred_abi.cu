@@ -1,0 +1,571 @@
+// genred_abi.cu -- the C ABI of libgenred (include/genred.h): validation, parameter folding,
+// launch planning (rows per thread, j-splits), scratch arena, host-pointer staging, dispatch.
+//
+// Host runtime only: every step of the path itself runs in the kernels of this library
+// (pack -> pair loop -> fixed-order merge).  There is no CPU fallback: without a device,
+// genred_create fails with GENRED_E_CUDA.
+#include <math.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/genred.h"
+#include "internal.h"
+
+using namespace genred;
+
+struct genred_ctx {
+    int device = 0;
+    int num_sms = 148;
+    std::string err;
+    void *scratch = nullptr;
+    size_t scratch_cap = 0;
+    void *stage = nullptr;
+    size_t stage_cap = 0;
+    genred_plan plan{};
+    int64_t launches = 0;
+    std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
+    bool profiling = false;
+    std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
+    int nprof = 0;
+};
+
+namespace {
+
+constexpr double kLog2e = 1.4426950408889634074;
+constexpr int kMaxSplit = 64;
+
+genred_status fail(genred_ctx *ctx, genred_status st, const std::string &msg) {
+    if (ctx) ctx->err = msg;
+    return st;
+}
+
+bool aligned(const void *p, size_t a) { return (reinterpret_cast<uintptr_t>(p) % a) == 0; }
+
+genred_status validate(const genred_args *a, std::string &msg) {
+    if (!a) { msg = "args is NULL"; return GENRED_E_INVALID; }
+    if (a->abi_version != GENRED_ABI_VERSION) {
+        msg = "abi_version mismatch (expected " + std::to_string(GENRED_ABI_VERSION) + ")";
+        return GENRED_E_INVALID;
+    }
+    if (a->memory != GENRED_MEM_DEVICE && a->memory != GENRED_MEM_HOST) {
+        msg = "memory must be GENRED_MEM_DEVICE or GENRED_MEM_HOST"; return GENRED_E_INVALID;
+    }
+    if (a->M < 0 || a->N < 0) { msg = "M and N must be >= 0"; return GENRED_E_SHAPE; }
+    if (a->D < 1 || a->E < 1) { msg = "D and E must be >= 1"; return GENRED_E_SHAPE; }
+    if (a->split_j < 0) { msg = "split_j must be >= 0"; return GENRED_E_INVALID; }
+    const int f = a->formula, r = a->reduction;
+    const bool sum_pair = r == GENRED_SUM &&
+        (f == GENRED_GAUSS || f == GENRED_GAUSS_GRADX || f == GENRED_GAUSS_SUM_GRADX || f == GENRED_SQDIST);
+    const bool lse_pair = r == GENRED_LSE && f == GENRED_SQDIST;
+    const bool argk_pair = r == GENRED_ARGKMIN && f == GENRED_SQDIST;
+    if (!sum_pair && !lse_pair && !argk_pair) {
+        msg = "unsupported (formula, reduction) pair"; return GENRED_E_UNSUPPORTED;
+    }
+    if (sum_pair && (a->D > 8 || a->E > 4)) {
+        msg = "Sum formulas support 1 <= D <= 8 and 1 <= E <= 4"; return GENRED_E_UNSUPPORTED;
+    }
+    if (lse_pair && (a->D > 8 || a->E != 1)) {
+        msg = "log-sum-exp supports 1 <= D <= 8 and E == 1 (scalar formula)"; return GENRED_E_UNSUPPORTED;
+    }
+    if (argk_pair) {
+        if (a->K < 1) { msg = "K must be >= 1"; return GENRED_E_SHAPE; }
+        if (a->K > 32) { msg = "ArgKMin supports K <= 32"; return GENRED_E_UNSUPPORTED; }
+        if (a->E != 1) { msg = "ArgKMin is scalar-formula only (E == 1)"; return GENRED_E_UNSUPPORTED; }
+        if (a->D > 16) { msg = "ArgKMin supports D <= 16 on the FP32 path"; return GENRED_E_UNSUPPORTED; }
+        if (a->N > (int64_t)INT32_MAX - kTileJ) { msg = "ArgKMin requires N < 2^31"; return GENRED_E_SHAPE; }
+        if (a->out_dtype != GENRED_F32) { msg = "ArgKMin distances are fp32 (out_dtype F32)"; return GENRED_E_INVALID; }
+    }
+    if ((f == GENRED_GAUSS || f == GENRED_GAUSS_GRADX || f == GENRED_GAUSS_SUM_GRADX || lse_pair) &&
+        !(isfinite(a->scale) && a->scale > 0.0)) {
+        msg = "scale (sigma or eps) must be finite and > 0"; return GENRED_E_INVALID;
+    }
+    if (a->out_dtype != GENRED_F32 && a->out_dtype != GENRED_F64) {
+        msg = "out_dtype must be GENRED_F32 or GENRED_F64"; return GENRED_E_INVALID;
+    }
+    if (a->M > 0) {
+        if (!a->out) { msg = "out is NULL"; return GENRED_E_INVALID; }
+        if (a->N > 0 && !a->x) { msg = "x is NULL"; return GENRED_E_INVALID; }
+        if (argk_pair && !a->out_idx) { msg = "out_idx is NULL"; return GENRED_E_INVALID; }
+        if (f == GENRED_GAUSS_SUM_GRADX && !a->out_grad) { msg = "out_grad is NULL"; return GENRED_E_INVALID; }
+    }
+    if (a->N > 0 && a->M > 0 && !a->y) { msg = "y is NULL"; return GENRED_E_INVALID; }
+    const void *fp[] = {a->x, a->y, a->b, a->g, a->out_grad};
+    for (const void *p : fp)
+        if (p && !aligned(p, 4)) { msg = "fp32 pointers must be 4-byte aligned"; return GENRED_E_INVALID; }
+    if (a->out && !aligned(a->out, a->out_dtype == GENRED_F64 ? 8 : 4)) {
+        msg = "out is misaligned for its dtype"; return GENRED_E_INVALID;
+    }
+    if ((a->out_idx && !aligned(a->out_idx, 8)) || (a->lse_state && !aligned(a->lse_state, 8))) {
+        msg = "out_idx / lse_state must be 8-byte aligned"; return GENRED_E_INVALID;
+    }
+    msg.clear();
+    return GENRED_OK;
+}
+
+int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
+    auto key = std::make_tuple(kind, a, b, c, R);
+    auto it = ctx->occ.find(key);
+    if (it != ctx->occ.end()) return it->second;
+    int n = 1;
+    if (kind == 0) n = sum_occupancy(a, b, c, R);
+    else if (kind == 1) n = lse_occupancy(a, R);
+    else n = argk_occupancy(a, b, R);
+    ctx->occ[key] = n;
+    return n;
+}
+
+// Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.
+int choose_split(int64_t itiles, int64_t ntiles, int64_t slots, double *eff_out) {
+    int best = 1;
+    double best_score = -1.0, best_eff = 0.0;
+    const int smax = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, ntiles / 4));
+    for (int S = 1; S <= smax; ++S) {
+        const int64_t tps = (ntiles + S - 1) / S;
+        const int64_t Seff = (ntiles + tps - 1) / tps;
+        if (Seff != S) continue;
+        const int64_t U = itiles * S;
+        const int64_t waves = (U + slots - 1) / slots;
+        const double eff = (double)U / (double)(waves * slots);
+        const double score = eff - 0.002 * S;
+        if (score > best_score + 1e-12) { best_score = score; best = S; best_eff = eff; }
+    }
+    if (eff_out) *eff_out = best_eff;
+    return best;
+}
+
+struct Plan {
+    int R = 1, split = 1;
+    int64_t itiles = 0, ntiles = 0, tiles_per_split = 0;
+};
+
+Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int occ_kind_a,
+               int occ_kind_b, int occ_kind_c) {
+    Plan pl;
+    pl.ntiles = (a->N + kTileJ - 1) / kTileJ;
+    int rcands[2] = {rmax, 1};
+    int ncand = rmax > 1 ? 2 : 1;
+    double best = -1.0;
+    for (int ci = 0; ci < ncand; ++ci) {
+        const int R = rcands[ci];
+        const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
+        const int64_t itiles = (a->M + rows - 1) / rows;
+        const int64_t slots = (int64_t)ctx->num_sms * occupancy(ctx, kind, occ_kind_a, occ_kind_b, occ_kind_c, R);
+        int S;
+        double eff;
+        if (a->split_j > 0) {
+            S = (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, pl.ntiles));
+            const int64_t U = itiles * S, waves = (U + slots - 1) / slots;
+            eff = (double)U / (double)(waves * slots);
+        } else {
+            S = choose_split(itiles, pl.ntiles, slots, &eff);
+        }
+        const double score = eff * (R == rmax ? 1.0 : 0.9);      // fewer rows/thread costs issue slots
+        if (score > best || (a->split_j > 0 && R == rmax)) {
+            best = score;
+            pl.R = R; pl.split = S; pl.itiles = itiles;
+            if (a->split_j > 0) break;                          // forced split: always rmax rows
+        }
+    }
+    pl.tiles_per_split = (pl.ntiles + pl.split - 1) / pl.split;
+    pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
+    return pl;
+}
+
+genred_status ensure(genred_ctx *ctx, void **buf, size_t *cap, size_t need) {
+    if (need <= *cap) return GENRED_OK;
+    size_t n = std::max(need, *cap + *cap / 2);
+    n = (n + 255) & ~size_t(255);
+    if (*buf) {
+        cudaFree(*buf);
+        *buf = nullptr;
+        *cap = 0;
+    }
+    if (cudaMalloc(buf, n) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, GENRED_E_NOMEM, "device scratch allocation of " + std::to_string(n) + " bytes failed");
+    }
+    *cap = n;
+    return GENRED_OK;
+}
+
+size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
+
+constexpr int kMaxProfiled = 4096;
+
+// Event pair around the main kernel (benchmark roofline timing); no-op unless profiling.
+cudaEvent_t prof_event(genred_ctx *ctx, bool start, cudaStream_t st) {
+    if (!ctx->profiling || ctx->nprof >= kMaxProfiled) return nullptr;
+    const size_t k = (size_t)ctx->nprof * 2 + (start ? 0 : 1);
+    while (ctx->ev.size() <= k) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+        ctx->ev.push_back(e);
+    }
+    cudaEventRecord(ctx->ev[k], st);
+    if (!start) ctx->nprof++;
+    return ctx->ev[k];
+}
+
+genred_status cuda_fail(genred_ctx *ctx, cudaError_t e, const char *where) {
+    cudaGetLastError();
+    return fail(ctx, GENRED_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
+}
+
+// Device-pointer evaluation (the path itself).
+genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st) {
+    const int f = a->formula, red = a->reduction;
+    const int64_t M = a->M, N = a->N;
+    const int D = a->D, E = a->E;
+    ctx->plan = genred_plan{};
+    ctx->plan.tile_j = kTileJ;
+    if (M == 0) return GENRED_OK;
+    const int out_f64 = a->out_dtype == GENRED_F64;
+    cudaError_t e;
+
+    if (N == 0) {                                               // neutral outputs (R11)
+        int kind, C = 0, K = 0;
+        if (red == GENRED_SUM) {
+            if (f == GENRED_GAUSS_SUM_GRADX) { kind = 1; C = E; K = D; }
+            else { kind = 0; C = (f == GENRED_GAUSS_GRADX) ? D : E; }
+        } else if (red == GENRED_LSE) kind = 2;
+        else { kind = 3; K = a->K; }
+        e = launch_fill(kind, M, C, K, a->out, out_f64, a->out_grad, a->out_idx, a->lse_state, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "fill kernel");
+        ctx->launches += 1;
+        ctx->plan.kernels = 1;
+        return GENRED_OK;
+    }
+
+    if (red == GENRED_SUM) {
+        const int mode = (f == GENRED_GAUSS) ? 0 : (f == GENRED_GAUSS_GRADX) ? 1
+                       : (f == GENRED_GAUSS_SUM_GRADX) ? 2 : 3;
+        const int rmax = sum_rows_per_thread_max(mode, D, E);
+        Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
+        const int RS = record_stride(D, E);
+        const int64_t npairs = pl.ntiles * (kTileJ / 2);
+        const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
+        const size_t jbytes = al256((size_t)npairs * RS * 4);
+        const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes);
+        if (s != GENRED_OK) return s;
+        float *J = (float *)ctx->scratch;
+        double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
+        // parameter folding in fp64, rounded once to fp32 (R15, R18)
+        float sc = 1.0f;
+        double scale_grad = 0.0;
+        if (mode != 3) {
+            const double sig = a->scale;
+            sc = (float)(sqrt(kLog2e) / sig);                   // 2^(-|s x - s y|^2) = e^(-|x-y|^2/sig^2)
+            scale_grad = -2.0 / (sig * sig * (double)sc);        // (x - y) = (x' - y') / s
+        }
+        e = launch_pack(mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS, a->y, a->b, N, D, E, sc, 0.f, npairs, J, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
+        SumLaunch L;
+        L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
+        L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
+        L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
+        L.out_grad = a->out_grad; L.part = part;
+        int ctas = 0;
+        prof_event(ctx, true, st);
+        e = launch_sum(L, st, &ctas);
+        prof_event(ctx, false, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
+        int kernels = 2;
+        if (pl.split > 1) {
+            const int cols_sum = (mode == 1) ? 0 : E;
+            e = launch_sum_finalize(part, pl.split, M, C, cols_sum, a->g, E, 1.0, scale_grad, mode,
+                                    a->out, out_f64, a->out_grad, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "sum finalize kernel");
+            kernels++;
+        }
+        ctx->launches += kernels;
+        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        return GENRED_OK;
+    }
+
+    if (red == GENRED_LSE) {
+        Plan pl = make_plan(ctx, a, 1, 4, D, 0, 0);
+        const int RS = record_stride(D, 1);
+        const int64_t npairs = pl.ntiles * (kTileJ / 2);
+        const size_t jbytes = al256((size_t)npairs * RS * 4);
+        const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * 2 * 8) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes);
+        if (s != GENRED_OK) return s;
+        float *J = (float *)ctx->scratch;
+        double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
+        e = launch_pack(PACK_LSE, a->y, a->b, N, D, 1, 1.0f, (float)kLog2e, npairs, J, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
+        LseLaunch L;
+        L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
+        L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+        L.negc = (float)(-kLog2e / a->scale);
+        L.h_zero = a->b == nullptr;
+        L.out = a->out; L.out_f64 = out_f64;
+        L.state = pl.split > 1 ? part : a->lse_state;
+        int ctas = 0;
+        prof_event(ctx, true, st);
+        e = launch_lse(L, st, &ctas);
+        prof_event(ctx, false, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "lse kernel");
+        int kernels = 2;
+        if (pl.split > 1) {
+            e = launch_lse_finalize(part, pl.split, M, a->out, out_f64, a->lse_state, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "lse finalize kernel");
+            kernels++;
+        }
+        ctx->launches += kernels;
+        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        return GENRED_OK;
+    }
+
+    // ArgKMin, small D, FP32 path
+    const int K = a->K;
+    const int R = argk_rows_per_thread(K);
+    Plan pl = make_plan(ctx, a, 2, R, D, K, 0);
+    const int RS = record_stride(D, 0);
+    const int64_t npairs = pl.ntiles * (kTileJ / 2);
+    const size_t jbytes = al256((size_t)npairs * RS * 4);
+    const size_t pdb = pl.split > 1 ? al256((size_t)pl.split * M * K * 4) : 0;
+    genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + 2 * pdb);
+    if (s != GENRED_OK) return s;
+    float *J = (float *)ctx->scratch;
+    float *pdist = pl.split > 1 ? (float *)((char *)ctx->scratch + jbytes) : nullptr;
+    int32_t *pidx = pl.split > 1 ? (int32_t *)((char *)ctx->scratch + jbytes + pdb) : nullptr;
+    e = launch_pack(PACK_ARGKMIN, a->y, nullptr, N, D, 0, 1.0f, 0.f, npairs, J, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
+    ArgkLaunch L;
+    L.D = D; L.K = K; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
+    L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+    L.dist = (float *)a->out; L.idx = a->out_idx; L.j_offset = a->j_offset;
+    L.pdist = pdist; L.pidx = pidx;
+    int ctas = 0;
+    prof_event(ctx, true, st);
+    e = launch_argk(L, st, &ctas);
+    prof_event(ctx, false, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "argkmin kernel");
+    int kernels = 2;
+    if (pl.split > 1) {
+        e = launch_topk_merge_i32(pdist, pidx, pl.split, M, K, (float *)a->out, a->out_idx,
+                                  a->j_offset, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "top-k merge kernel");
+        kernels++;
+    }
+    ctx->launches += kernels;
+    ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+    ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+    return GENRED_OK;
+}
+
+// Byte sizes of every operand, for host-pointer staging.
+struct Sizes {
+    size_t x, y, b, g, out, grad, idx, state;
+};
+Sizes operand_sizes(const genred_args *a) {
+    Sizes z{};
+    const size_t M = (size_t)a->M, N = (size_t)a->N;
+    z.x = M * a->D * 4;
+    z.y = N * a->D * 4;
+    const bool lse = a->reduction == GENRED_LSE, argk = a->reduction == GENRED_ARGKMIN;
+    z.b = a->b ? (lse ? N * 4 : N * a->E * 4) : 0;
+    z.g = a->g ? M * a->E * 4 : 0;
+    const size_t es = a->out_dtype == GENRED_F64 ? 8 : 4;
+    if (argk) z.out = M * a->K * 4;
+    else if (lse) z.out = M * es;
+    else if (a->formula == GENRED_GAUSS_GRADX) z.out = M * a->D * es;
+    else z.out = M * a->E * es;
+    z.grad = a->formula == GENRED_GAUSS_SUM_GRADX ? M * a->D * 4 : 0;
+    z.idx = argk ? M * a->K * 8 : 0;
+    z.state = (lse && a->lse_state) ? M * 16 : 0;
+    return z;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t genred_abi_version(void) { return GENRED_ABI_VERSION; }
+
+#define GENRED_STR2(x) #x
+#define GENRED_STR(x) GENRED_STR2(x)
+const char *genred_build_info(void) {
+    return "libgenred abi=" GENRED_STR(GENRED_ABI_VERSION) " target=sm_100a (compute_100a) nvcc "
+           GENRED_STR(__CUDACC_VER_MAJOR__) "." GENRED_STR(__CUDACC_VER_MINOR__);
+}
+
+genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
+    if (!out) return GENRED_E_INVALID;
+    *out = nullptr;
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess || n == 0) {
+        cudaGetLastError();
+        return GENRED_E_CUDA;
+    }
+    if (cuda_device < 0 || cuda_device >= n) return GENRED_E_INVALID;
+    genred_ctx *ctx = new (std::nothrow) genred_ctx();
+    if (!ctx) return GENRED_E_NOMEM;
+    ctx->device = cuda_device;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(cuda_device);
+    int major = 0, minor = 0;
+    cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
+    cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
+    cudaSetDevice(prev);
+    if (major != 10 || minor != 0) {
+        delete ctx;
+        return GENRED_E_UNSUPPORTED;                            // sm_100a code only
+    }
+    *out = ctx;
+    return GENRED_OK;
+}
+
+void genred_destroy(genred_ctx *ctx) {
+    if (!ctx) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(ctx->device);
+    if (ctx->scratch) cudaFree(ctx->scratch);
+    if (ctx->stage) cudaFree(ctx->stage);
+    for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
+    cudaSetDevice(prev);
+    delete ctx;
+}
+
+const char *genred_last_error(const genred_ctx *ctx) {
+    return ctx ? ctx->err.c_str() : "null context";
+}
+
+genred_status genred_validate(const genred_args *args, char *msg, size_t msg_len) {
+    std::string m;
+    genred_status s = validate(args, m);
+    if (msg && msg_len) {
+        strncpy(msg, m.c_str(), msg_len - 1);
+        msg[msg_len - 1] = 0;
+    }
+    return s;
+}
+
+genred_status genred_eval(genred_ctx *ctx, const genred_args *args, void *stream) {
+    if (!ctx) return GENRED_E_INVALID;
+    std::string m;
+    genred_status s = validate(args, m);
+    if (s != GENRED_OK) return fail(ctx, s, m);
+    ctx->err.clear();
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    cudaStream_t st = (cudaStream_t)stream;
+    if (args->memory == GENRED_MEM_DEVICE) {
+        s = eval_device(ctx, args, st);
+    } else {
+        // Host pointers: stage through context-owned device buffers, H2D -> eval -> D2H.
+        Sizes z = operand_sizes(args);
+        size_t off[8], tot = 0;
+        size_t sz[8] = {z.x, z.y, z.b, z.g, z.out, z.grad, z.idx, z.state};
+        for (int k = 0; k < 8; ++k) { off[k] = tot; tot += al256(sz[k]); }
+        s = ensure(ctx, &ctx->stage, &ctx->stage_cap, tot + 256);
+        if (s == GENRED_OK) {
+            char *base = (char *)ctx->stage;
+            genred_args d = *args;
+            d.memory = GENRED_MEM_DEVICE;
+            const void *src[4] = {args->x, args->y, args->b, args->g};
+            const void **dst[4] = {(const void **)&d.x, (const void **)&d.y, (const void **)&d.b,
+                                   (const void **)&d.g};
+            for (int k = 0; k < 4 && s == GENRED_OK; ++k) {
+                if (!src[k] || sz[k] == 0) continue;
+                *dst[k] = base + off[k];
+                cudaError_t e = cudaMemcpyAsync(base + off[k], src[k], sz[k], cudaMemcpyHostToDevice, st);
+                if (e != cudaSuccess) s = cuda_fail(ctx, e, "H2D copy");
+            }
+            d.out = args->out ? base + off[4] : nullptr;
+            d.out_grad = args->out_grad ? (float *)(base + off[5]) : nullptr;
+            d.out_idx = args->out_idx ? (int64_t *)(base + off[6]) : nullptr;
+            d.lse_state = args->lse_state ? (double *)(base + off[7]) : nullptr;
+            if (s == GENRED_OK) s = eval_device(ctx, &d, st);
+            void *hdst[4] = {args->out, args->out_grad, args->out_idx, args->lse_state};
+            const void *dsrc[4] = {d.out, d.out_grad, d.out_idx, d.lse_state};
+            size_t dsz[4] = {z.out, z.grad, z.idx, z.state};
+            for (int k = 0; k < 4 && s == GENRED_OK; ++k) {
+                if (!hdst[k] || dsz[k] == 0) continue;
+                cudaError_t e = cudaMemcpyAsync(hdst[k], dsrc[k], dsz[k], cudaMemcpyDeviceToHost, st);
+                if (e != cudaSuccess) s = cuda_fail(ctx, e, "D2H copy");
+            }
+            if (s == GENRED_OK) {
+                cudaError_t e = cudaStreamSynchronize(st);
+                if (e != cudaSuccess) s = cuda_fail(ctx, e, "stream synchronize");
+            }
+        }
+    }
+    if (prev != ctx->device) cudaSetDevice(prev);
+    return s;
+}
+
+genred_status genred_combine_lse(genred_ctx *ctx, int64_t M, int32_t G, const double *states,
+                                 void *out, int32_t out_dtype, double *state_out, void *stream) {
+    if (!ctx) return GENRED_E_INVALID;
+    if (M < 0 || G < 1) return fail(ctx, GENRED_E_SHAPE, "M >= 0 and G >= 1 required");
+    if (M > 0 && (!states || (!out && !state_out))) return fail(ctx, GENRED_E_INVALID, "null pointer");
+    if (out_dtype != GENRED_F32 && out_dtype != GENRED_F64) return fail(ctx, GENRED_E_INVALID, "bad out_dtype");
+    if (M == 0) return GENRED_OK;
+    cudaError_t e = launch_lse_finalize(states, G, M, out, out_dtype == GENRED_F64, state_out,
+                                        (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "combine_lse kernel");
+    ctx->launches += 1;
+    return GENRED_OK;
+}
+
+genred_status genred_merge_topk(genred_ctx *ctx, int64_t M, int32_t K, int32_t G, const float *d,
+                                const int64_t *idx, float *d_out, int64_t *idx_out, void *stream) {
+    if (!ctx) return GENRED_E_INVALID;
+    if (M < 0 || K < 1 || G < 1) return fail(ctx, GENRED_E_SHAPE, "M >= 0, K >= 1, G >= 1 required");
+    if (G > 64 || K > 1024) return fail(ctx, GENRED_E_UNSUPPORTED, "merge_topk supports G <= 64");
+    if (M > 0 && (!d || !idx || !d_out || !idx_out)) return fail(ctx, GENRED_E_INVALID, "null pointer");
+    if (M == 0) return GENRED_OK;
+    cudaError_t e = launch_topk_merge_i64(d, idx, G, M, K, d_out, idx_out, (cudaStream_t)stream);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "merge_topk kernel");
+    ctx->launches += 1;
+    return GENRED_OK;
+}
+
+genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
+    if (!ctx || !plan) return GENRED_E_INVALID;
+    *plan = ctx->plan;
+    return GENRED_OK;
+}
+
+int64_t genred_launch_count(const genred_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+genred_status genred_profile(genred_ctx *ctx, int32_t enable) {
+    if (!ctx) return GENRED_E_INVALID;
+    ctx->profiling = enable != 0;
+    ctx->nprof = 0;
+    return GENRED_OK;
+}
+
+int32_t genred_profile_read(genred_ctx *ctx, float *ms, int32_t max) {
+    if (!ctx || (!ms && max > 0)) return -1;
+    int n = std::min(ctx->nprof, (int)max);
+    for (int k = 0; k < n; ++k) {
+        if (cudaEventSynchronize(ctx->ev[2 * k + 1]) != cudaSuccess ||
+            cudaEventElapsedTime(&ms[k], ctx->ev[2 * k], ctx->ev[2 * k + 1]) != cudaSuccess) {
+            cudaGetLastError();
+            return -1;
+        }
+    }
+    return n;
+}
+
+}  // extern "C"

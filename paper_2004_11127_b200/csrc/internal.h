@@ -1,0 +1,84 @@
+// internal.h -- launch interfaces between the C-ABI layer (genred_abi.cu) and the kernel
+// translation units.  Not installed; not part of the ABI.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace genred {
+
+constexpr int kTileJ = 512;                 // j-records per shared-memory stage
+constexpr int kStages = 4;                  // depth of the bulk-copy ring
+constexpr int kConsumerWarps = 8;           // math warps per CTA
+constexpr int kThreads = (kConsumerWarps + 1) * 32;   // + 1 producer (bulk-copy) warp
+constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference of an empty LSE state
+
+// Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.
+inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
+
+enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE = 2, PACK_ARGKMIN = 3 };
+
+// Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
+// kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E.
+// Records past N (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf
+// (LSE, ArgKMin), which contribute nothing.
+cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
+                        float s, float hscale, int64_t npairs, float *J, cudaStream_t st);
+
+struct SumLaunch {
+    int mode;                 // 0 SUM, 1 GRADX, 2 SUM_GRADX, 3 SQDIST_SUM
+    int D, E, R;              // R = rows per consumer thread
+    const float *x, *J, *g;
+    int64_t M;
+    int split;                // number of j-splits (grid = itiles * split)
+    int64_t tiles_per_split, ntiles;
+    float s;                  // coordinate pre-scale (sqrt(log2e)/sigma, or 1 for SQDIST)
+    double scale_sum, scale_grad;
+    void *out; int out_f64;   // sum output (SUM / SUM_GRADX / SQDIST_SUM) or gradient (GRADX)
+    float *out_grad;          // SUM_GRADX gradient output
+    double *part;             // split > 1: split x M x C fp64 partials
+};
+cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
+int sum_occupancy(int mode, int D, int E, int R);
+int sum_rows_per_thread_max(int mode, int D, int E);
+
+struct LseLaunch {
+    int D, R;
+    const float *x, *J;
+    int64_t M;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float negc;               // -log2(e)/eps
+    int h_zero;               // h == 0 everywhere (skips a per-pair FADD)
+    void *out; int out_f64;   // split == 1: a_i
+    double *state;            // split == 1: optional M x 2 state; split > 1: split x M x 2 partials
+};
+cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
+int lse_occupancy(int D, int R);
+
+struct ArgkLaunch {
+    int D, K, R;
+    const float *x, *J;
+    int64_t M;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float *dist; int64_t *idx; int64_t j_offset;   // split == 1 outputs
+    float *pdist; int32_t *pidx;                   // split > 1: split x M x K partials
+};
+cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas);
+int argk_occupancy(int D, int K, int R);
+int argk_rows_per_thread(int K);
+
+// Deterministic (fixed-order) merges of split-j partials.
+cudaError_t launch_sum_finalize(const double *part, int split, int64_t M, int C, int cols_sum,
+                                const float *g, int E, double scale_sum, double scale_grad,
+                                int mode, void *out, int out_f64, float *out_grad, cudaStream_t st);
+cudaError_t launch_lse_finalize(const double *part, int split, int64_t M, void *out, int out_f64,
+                                double *state_out, cudaStream_t st);
+cudaError_t launch_topk_merge_i32(const float *pd, const int32_t *pi, int split, int64_t M, int K,
+                                  float *dist, int64_t *idx, int64_t j_offset, cudaStream_t st);
+cudaError_t launch_topk_merge_i64(const float *pd, const int64_t *pi, int G, int64_t M, int K,
+                                  float *dist, int64_t *idx, cudaStream_t st);
+cudaError_t launch_fill(int kind, int64_t M, int C, int K, void *out, int out_f64, float *out_grad,
+                        int64_t *idx, double *state, cudaStream_t st);
+
+}  // namespace genred

@@ -1,0 +1,285 @@
+// lse_kernel.cu -- streaming, max-shifted log-sum-exp reduction:
+//
+//     F_ij = -|x_i - y_j|^2 / eps + h_j ,     a_i = log sum_j exp(F_ij)          (Eq. 1)
+//
+// evaluated in the log2 domain: v_ij = log2(e) F_ij = negc |x_i - y_j|^2 + h'_j with
+// negc = -log2(e)/eps, h' = log2(e) h.  Each row keeps a reference m_i (log2 units) and
+// s_i = sum_j 2^(v_ij - m_i) (reading R6 in DESIGN.md):
+//   * RAW differences d = x - y (no pre-scaling of coordinates: the query shift of a pre-scaled
+//     x costs up to 1.35e-6 in a_i);
+//   * t = fma(negc, |d|^2, h' - m) then MUFU.EX2; two j's per packed FADD2/FFMA2;
+//   * lazy rescale: terms are summed per 16-j sub-chunk into a fresh fp32 pair; the sub-chunk's
+//     max t (FMNMX3) is checked once; if it exceeds TAU = 8 the sub-chunk is discarded, m is
+//     set to the sub-chunk's exact max v (never m + t), s is rescaled in fp64 and the sub-chunk
+//     is recomputed -- rare (a few times per row);
+//   * fp32 partials are promoted to fp64 every 128 j; the output is finalised in fp64:
+//     a_i = ln2 (m_i + log2 s_i).
+// Pipeline and tiling are those of sum_kernel.cu (bulk-copy ring of 512-record j-tiles).
+#include <math.h>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace genred {
+
+constexpr float kTau = 8.0f;          // lazy-rescale threshold, log2 units
+constexpr int kSub = 8;               // record pairs per sub-chunk (16 j)
+constexpr int kPromote = 8;           // sub-chunks per fp64 promotion (128 j)
+
+template <int D>
+struct LseCfg {
+    static constexpr int RS = ((2 * (D + 1)) + 3) / 4 * 4;
+    static constexpr int PAIRS = kTileJ / 2;
+    static constexpr int TILE_FLOATS = PAIRS * RS;
+    static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
+    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+};
+
+struct LseParams {
+    const float *x, *J;
+    int64_t M;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float negc;
+    void *out;
+    int out_f64;
+    double *state;
+};
+
+template <int D, int R, bool HZ>
+__global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
+    using Cfg = LseCfg<D>;
+    constexpr int RS = Cfg::RS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
+    uint64_t *empty = full + kStages;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
+    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+    const int nt = (int)(t1 - t0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {
+        if (lane == 0) {
+            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
+            for (int k = 0; k < nt; ++k) {
+                const int s = k % kStages;
+                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
+                         Cfg::STAGE_BYTES, &full[s]);
+            }
+        }
+        return;
+    }
+
+    const int ct = threadIdx.x;
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    const float negc = p.negc;
+    const float2 negc2 = dup2(negc);
+    float xr[R][D];
+    float m[R];
+    double s64[R];
+    float2 s32[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        const bool ok = i < p.M;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xr[r][d] = ok ? __ldg(p.x + i * D + d) : 0.0f;
+        m[r] = kLseSentinel;
+        s64[r] = 0.0;
+        s32[r] = make_float2(0.f, 0.f);
+    }
+
+    for (int k = 0; k < nt; ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full[s], (k / kStages) & 1);
+        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+        for (int sc = 0; sc < Cfg::PAIRS / kSub; ++sc) {
+            const float *base = tile + sc * kSub * RS;
+            float tm[R];
+            float2 cs[R];
+            float2 hm0[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                tm[r] = -INFINITY;
+                cs[r] = make_float2(0.f, 0.f);
+                hm0[r] = dup2(-m[r]);
+            }
+#pragma unroll
+            for (int q = 0; q < kSub; ++q) {
+                float f[RS];
+#pragma unroll
+                for (int u = 0; u < RS / 4; ++u) {
+                    const float4 v = lds128(base + q * RS + 4 * u);
+                    f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+                }
+                float2 ny[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
+                const float2 hp = make_float2(f[2 * D], f[2 * D + 1]);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 dd = add2(dup2(xr[r][0]), ny[0]);
+                    float2 q2 = mul2(dd, dd);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) {
+                        dd = add2(dup2(xr[r][d]), ny[d]);
+                        q2 = fma2(dd, dd, q2);
+                    }
+                    const float2 hm = HZ ? hm0[r] : add2(hp, hm0[r]);
+                    const float2 t = fma2(q2, negc2, hm);          // v - m, log2 units
+                    tm[r] = max3(tm[r], t.x, t.y);
+                    cs[r] = add2(cs[r], make_float2(ex2(t.x), ex2(t.y)));
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                if (tm[r] > kTau) {
+                    // ---- rare path: new reference = exact max of v over this sub-chunk ----
+                    float vmax = -INFINITY;
+                    for (int q = 0; q < kSub; ++q) {
+                        const float *rec = base + q * RS;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float q1 = 0.f;
+#pragma unroll
+                            for (int d = 0; d < D; ++d) {
+                                const float dd = xr[r][d] + rec[2 * d + h];
+                                q1 = fmaf(dd, dd, q1);
+                            }
+                            vmax = fmaxf(vmax, fmaf(q1, negc, HZ ? 0.0f : rec[2 * D + h]));
+                        }
+                    }
+                    const float mn = fmaxf(vmax, m[r]);
+                    s64[r] = (s64[r] + (double)s32[r].x + (double)s32[r].y) *
+                             exp2((double)m[r] - (double)mn);
+                    m[r] = mn;
+                    float c1 = 0.f;
+                    for (int q = 0; q < kSub; ++q) {
+                        const float *rec = base + q * RS;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float q1 = 0.f;
+#pragma unroll
+                            for (int d = 0; d < D; ++d) {
+                                const float dd = xr[r][d] + rec[2 * d + h];
+                                q1 = fmaf(dd, dd, q1);
+                            }
+                            const float hmv = HZ ? -mn : (rec[2 * D + h] + (-mn));
+                            c1 += ex2(fmaf(q1, negc, hmv));
+                        }
+                    }
+                    s32[r] = make_float2(c1, 0.f);
+                } else {
+                    s32[r] = add2(s32[r], cs[r]);
+                }
+            }
+            if ((sc + 1) % kPromote == 0) {
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    s64[r] += (double)s32[r].x + (double)s32[r].y;
+                    s32[r] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= p.M) continue;
+        const double stot = s64[r] + (double)s32[r].x + (double)s32[r].y;
+        if (p.split > 1) {
+            p.state[((int64_t)sp * p.M + i) * 2 + 0] = (double)m[r];
+            p.state[((int64_t)sp * p.M + i) * 2 + 1] = stot;
+            continue;
+        }
+        const double a = (stot > 0.0) ? 0.69314718055994530942 * ((double)m[r] + log2(stot)) : -INFINITY;
+        if (p.out) {
+            if (p.out_f64) ((double *)p.out)[i] = a;
+            else ((float *)p.out)[i] = (float)a;
+        }
+        if (p.state) {
+            p.state[2 * i + 0] = (double)m[r];
+            p.state[2 * i + 1] = stot;
+        }
+    }
+}
+
+template <int D, int R, bool HZ>
+static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    using Cfg = LseCfg<D>;
+    auto kern = lse_kernel<D, R, HZ>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    LseParams p;
+    p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.tiles_per_split = a.tiles_per_split;
+    p.ntiles = a.ntiles; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
+    const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
+    const int64_t grid = ((a.M + rows - 1) / rows) * a.split;
+    *ctas = (int)grid;
+    kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int D, int R>
+static int occ_lse() {
+    using Cfg = LseCfg<D>;
+    auto kern = lse_kernel<D, R, false>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+template <int D>
+static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    if (a.R == 1) return a.h_zero ? run_lse<D, 1, true>(a, st, ctas) : run_lse<D, 1, false>(a, st, ctas);
+    return a.h_zero ? run_lse<D, 4, true>(a, st, ctas) : run_lse<D, 4, false>(a, st, ctas);
+}
+
+cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    switch (a.D) {
+        case 1: return run_lse_r<1>(a, st, ctas);
+        case 2: return run_lse_r<2>(a, st, ctas);
+        case 3: return run_lse_r<3>(a, st, ctas);
+        case 4: return run_lse_r<4>(a, st, ctas);
+        case 5: return run_lse_r<5>(a, st, ctas);
+        case 6: return run_lse_r<6>(a, st, ctas);
+        case 7: return run_lse_r<7>(a, st, ctas);
+        case 8: return run_lse_r<8>(a, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+
+int lse_occupancy(int D, int R) {
+#define GENRED_OCC(DD) if (D == DD) return R == 1 ? occ_lse<DD, 1>() : occ_lse<DD, 4>();
+    GENRED_OCC(1) GENRED_OCC(2) GENRED_OCC(3) GENRED_OCC(4)
+    GENRED_OCC(5) GENRED_OCC(6) GENRED_OCC(7) GENRED_OCC(8)
+#undef GENRED_OCC
+    return 1;
+}
+
+}  // namespace genred

@@ -1,0 +1,367 @@
+// sum_kernel.cu -- Genred Sum reductions on the FP32 + MUFU pipes:
+//
+//   GAUSS       a_i   = sum_j exp(-|x_i - y_j|^2 / sigma^2) b_j           (Eq. 1)
+//   GAUSS_GRADX G_i   = sum_j (-2/sigma^2)(x_i - y_j) e_ij <b_j, g_i>
+//   SUM_GRADX   both in one pass (shares the distance and the exponential)
+//   SQDIST_SUM  a_i   = sum_j |x_i - y_j|^2 b_j                           (test combination)
+//
+// Design (B200-first; the paper's GPU Gems "tiled map-reduce", is prior art):
+//   * one CTA owns 256*R i-rows, kept in registers (R rows per math thread), and one j-range;
+//   * a producer warp streams j-tiles (512 records, pair-interleaved, pre-scaled by
+//     s = sqrt(log2 e)/sigma so that exp(-|x-y|^2/sigma^2) = 2^(-|x'-y'|^2)) from HBM/L2 into a
+//     4-stage shared-memory ring with cp.async.bulk (TMA engine) completing on mbarriers;
+//   * math warps read each record pair once per thread (broadcast LDS.128) and evaluate two j's
+//     at a time with packed FADD2/FMUL2/FFMA2 and two MUFU.EX2 (ex2.approx.ftz), so a pair costs
+//     3.5 issue slots of FP32 work + 1 MUFU for D=3 (the MUFU pipe, 16/clk/SM, is the bound);
+//   * per-tile fp32 partials are promoted to fp64 every 512 j (reading R18 in DESIGN.md);
+//   * j-splits (grid = i-tiles x splits) fill all 148 SMs; their fp64 partials are merged in a
+//     fixed order by sum_finalize (deterministic, no float atomics).
+#include <math.h>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace genred {
+
+template <int MODE, int D, int E>
+struct SumCfg {
+    static constexpr int RS = ((2 * (D + E)) + 3) / 4 * 4;       // floats per record pair
+    static constexpr int PAIRS = kTileJ / 2;
+    static constexpr int TILE_FLOATS = PAIRS * RS;
+    static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
+    static constexpr int NS = (MODE == 1) ? 0 : E;                // sum columns
+    static constexpr int NG = (MODE == 1 || MODE == 2) ? D : 0;   // gradient columns
+    static constexpr int C = NS + NG;
+    static constexpr bool GRAD = NG > 0;
+    static constexpr bool EXP = MODE != 3;
+    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+};
+
+struct SumParams {
+    const float *x, *J, *g;
+    int64_t M;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float s;
+    double scale_sum, scale_grad;
+    void *out;
+    int out_f64;
+    float *out_grad;
+    double *part;
+};
+
+template <int MODE, int D, int E, int R>
+__global__ void __launch_bounds__(kThreads, 2) sum_kernel(const SumParams p) {
+    using Cfg = SumCfg<MODE, D, E>;
+    constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *tiles = reinterpret_cast<float *>(smem_raw);
+    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
+    uint64_t *empty = full + kStages;
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
+    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+    const int nt = (int)(t1 - t0);
+
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < kStages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        fence_barrier_init();
+    }
+    __syncthreads();
+
+    if (warp == kConsumerWarps) {                     // ---- producer: bulk-copy j-tiles ----
+        if (lane == 0) {
+            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
+            for (int k = 0; k < nt; ++k) {
+                const int s = k % kStages;
+                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
+                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
+                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
+                         Cfg::STAGE_BYTES, &full[s]);
+            }
+        }
+        return;
+    }
+
+    // ---- math warps: R rows per thread, registers only --------------------------------------
+    const int ct = threadIdx.x;
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    float xr[R][D];
+    float gr[R][E];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        const bool ok = i < p.M;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xr[r][d] = ok ? p.s * __ldg(p.x + i * D + d) : 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            gr[r][e] = (Cfg::GRAD && E > 1 && ok && p.g) ? __ldg(p.g + i * E + e) : 1.0f;
+    }
+    float2 acc[R][NS > 0 ? NS : 1];
+    float2 accg[R][NG > 0 ? NG : 1];
+    double acc64[R][C];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc64[r][c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < (NS > 0 ? NS : 1); ++c) acc[r][c] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < (NG > 0 ? NG : 1); ++c) accg[r][c] = make_float2(0.f, 0.f);
+    }
+
+    for (int k = 0; k < nt; ++k) {
+        const int s = k % kStages;
+        mbar_wait(&full[s], (k / kStages) & 1);
+        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+#pragma unroll 2
+        for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
+            float f[RS];
+#pragma unroll
+            for (int q = 0; q < RS / 4; ++q) {
+                const float4 v = lds128(tile + pp * RS + 4 * q);
+                f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+            }
+            float2 ny[D], bv[E];
+#pragma unroll
+            for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
+#pragma unroll
+            for (int e = 0; e < E; ++e) bv[e] = make_float2(f[2 * D + 2 * e], f[2 * D + 2 * e + 1]);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 dd[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) dd[d] = add2(dup2(xr[r][d]), ny[d]);   // x' - y'
+                float2 q = mul2(dd[0], dd[0]);
+#pragma unroll
+                for (int d = 1; d < D; ++d) q = fma2(dd[d], dd[d], q);             // |x'-y'|^2
+                if constexpr (!Cfg::EXP) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[r][e] = fma2(q, bv[e], acc[r][e]);
+                } else {
+                    const float2 ex = make_float2(ex2(-q.x), ex2(-q.y));   // e^{-|x-y|^2/sigma^2}
+                    if constexpr (MODE == 0) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                    } else {
+                        float2 w;
+                        if constexpr (E == 1) {
+                            w = mul2(ex, bv[0]);                   // e_ij b_j (g_i applied later)
+                            if constexpr (MODE == 2) acc[r][0] = add2(acc[r][0], w);
+                        } else {
+                            float2 bg = mul2(bv[0], dup2(gr[r][0]));
+#pragma unroll
+                            for (int e = 1; e < E; ++e) bg = fma2(bv[e], dup2(gr[r][e]), bg);
+                            w = mul2(ex, bg);                      // e_ij <b_j, g_i>
+                            if constexpr (MODE == 2) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                            }
+                        }
+#pragma unroll
+                        for (int d = 0; d < D; ++d) accg[r][d] = fma2(w, dd[d], accg[r][d]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        // promote the tile's fp32 partials to fp64 (every 512 j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                acc64[r][c] += (double)acc[r][c].x + (double)acc[r][c].y;
+                acc[r][c] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                acc64[r][NS + c] += (double)accg[r][c].x + (double)accg[r][c].y;
+                accg[r][c] = make_float2(0.f, 0.f);
+            }
+        }
+    }
+
+    // ---- epilogue --------------------------------------------------------------------------
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= p.M) continue;
+        if (p.split > 1) {
+            double *dst = p.part + ((int64_t)sp * p.M + i) * C;
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst[c] = acc64[r][c];
+            continue;
+        }
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+            const double v = acc64[r][c] * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i * NS + c] = v;
+            else ((float *)p.out)[i * NS + c] = (float)v;
+        }
+        if constexpr (NG > 0) {
+            double gs = p.scale_grad;
+            if (E == 1 && p.g) gs *= (double)__ldg(p.g + i);
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                const double v = acc64[r][NS + c] * gs;
+                if (MODE == 2) p.out_grad[i * D + c] = (float)v;
+                else if (p.out_f64) ((double *)p.out)[i * D + c] = v;
+                else ((float *)p.out)[i * D + c] = (float)v;
+            }
+        }
+    }
+}
+
+// ---- host-side dispatch over (MODE, D, E, R) ------------------------------------------------
+template <int MODE, int D, int E, int R>
+static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
+    using Cfg = SumCfg<MODE, D, E>;
+    auto kern = sum_kernel<MODE, D, E, R>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    SumParams p;
+    p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;
+    p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.s = a.s;
+    p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
+    p.out_grad = a.out_grad; p.part = a.part;
+    const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
+    const int64_t itiles = (a.M + rows - 1) / rows;
+    const int64_t grid = itiles * a.split;
+    *ctas = (int)grid;
+    kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+template <int MODE, int D, int E, int R>
+static int occ_sum() {
+    using Cfg = SumCfg<MODE, D, E>;
+    auto kern = sum_kernel<MODE, D, E, R>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess)
+        return 1;
+    return n > 0 ? n : 1;
+}
+
+// Largest rows-per-thread that stays spill-free under __launch_bounds__(288, 2) (96 registers).
+template <int MODE, int D, int E>
+constexpr int sum_rmax() {
+    return (MODE == 0 || MODE == 3) ? ((D + E <= 6) ? 4 : 2) : ((D + E <= 4) ? 2 : 1);
+}
+template <int MODE, int D, int E>
+static cudaError_t run_sum_r(const SumLaunch &a, cudaStream_t st, int *ctas) {
+    constexpr int RM = sum_rmax<MODE, D, E>();
+    return a.R == 1 ? run_sum<MODE, D, E, 1>(a, st, ctas) : run_sum<MODE, D, E, RM>(a, st, ctas);
+}
+template <int MODE, int D, int E>
+static int occ_sum_r(int R) {
+    constexpr int RM = sum_rmax<MODE, D, E>();
+    return R == 1 ? occ_sum<MODE, D, E, 1>() : occ_sum<MODE, D, E, RM>();
+}
+
+template <int MODE, int D>
+static cudaError_t run_sum_e(const SumLaunch &a, cudaStream_t st, int *ctas) {
+    switch (a.E) {
+        case 1: return run_sum_r<MODE, D, 1>(a, st, ctas);
+        case 2: return run_sum_r<MODE, D, 2>(a, st, ctas);
+        case 3: return run_sum_r<MODE, D, 3>(a, st, ctas);
+        case 4: return run_sum_r<MODE, D, 4>(a, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+template <int MODE, int D>
+static int occ_sum_e(int E, int R) {
+    switch (E) {
+        case 1: return occ_sum_r<MODE, D, 1>(R);
+        case 2: return occ_sum_r<MODE, D, 2>(R);
+        case 3: return occ_sum_r<MODE, D, 3>(R);
+        case 4: return occ_sum_r<MODE, D, 4>(R);
+    }
+    return 1;
+}
+
+template <int MODE>
+static cudaError_t run_sum_d(const SumLaunch &a, cudaStream_t st, int *ctas) {
+    switch (a.D) {
+        case 1: return run_sum_e<MODE, 1>(a, st, ctas);
+        case 2: return run_sum_e<MODE, 2>(a, st, ctas);
+        case 3: return run_sum_e<MODE, 3>(a, st, ctas);
+        case 4: return run_sum_e<MODE, 4>(a, st, ctas);
+        case 5: return run_sum_e<MODE, 5>(a, st, ctas);
+        case 6: return run_sum_e<MODE, 6>(a, st, ctas);
+        case 7: return run_sum_e<MODE, 7>(a, st, ctas);
+        case 8: return run_sum_e<MODE, 8>(a, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+template <int MODE>
+static int occ_sum_d(int D, int E, int R) {
+    switch (D) {
+        case 1: return occ_sum_e<MODE, 1>(E, R);
+        case 2: return occ_sum_e<MODE, 2>(E, R);
+        case 3: return occ_sum_e<MODE, 3>(E, R);
+        case 4: return occ_sum_e<MODE, 4>(E, R);
+        case 5: return occ_sum_e<MODE, 5>(E, R);
+        case 6: return occ_sum_e<MODE, 6>(E, R);
+        case 7: return occ_sum_e<MODE, 7>(E, R);
+        case 8: return occ_sum_e<MODE, 8>(E, R);
+    }
+    return 1;
+}
+
+cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
+    switch (a.mode) {
+        case 0: return run_sum_d<0>(a, st, ctas);
+        case 1: return run_sum_d<1>(a, st, ctas);
+        case 2: return run_sum_d<2>(a, st, ctas);
+        case 3: return run_sum_d<3>(a, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+
+template <int MODE>
+static int rmax_d_e(int D, int E) {
+    int r = 1;
+#define GENRED_RM(DD, EE) if (D == DD && E == EE) r = sum_rmax<MODE, DD, EE>();
+#define GENRED_RM_E(DD) GENRED_RM(DD, 1) GENRED_RM(DD, 2) GENRED_RM(DD, 3) GENRED_RM(DD, 4)
+    GENRED_RM_E(1) GENRED_RM_E(2) GENRED_RM_E(3) GENRED_RM_E(4)
+    GENRED_RM_E(5) GENRED_RM_E(6) GENRED_RM_E(7) GENRED_RM_E(8)
+#undef GENRED_RM_E
+#undef GENRED_RM
+    return r;
+}
+
+int sum_rows_per_thread_max(int mode, int D, int E) {
+    switch (mode) {
+        case 0: return rmax_d_e<0>(D, E);
+        case 1: return rmax_d_e<1>(D, E);
+        case 2: return rmax_d_e<2>(D, E);
+        case 3: return rmax_d_e<3>(D, E);
+    }
+    return 1;
+}
+
+int sum_occupancy(int mode, int D, int E, int R) {
+    switch (mode) {
+        case 0: return occ_sum_d<0>(D, E, R);
+        case 1: return occ_sum_d<1>(D, E, R);
+        case 2: return occ_sum_d<2>(D, E, R);
+        case 3: return occ_sum_d<3>(D, E, R);
+    }
+    return 1;
+}
+
+}  // namespace genred

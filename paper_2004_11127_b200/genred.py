@@ -1,0 +1,299 @@
+"""Thin Python binding of libgenred (include/genred.h) -- argument marshalling only.
+
+Every step of the Genred path (Eq. 1) runs inside libgenred's sm_100a kernels;
+this module only checks tensor properties, fills the ``genred_args`` struct and calls the C ABI
+through ctypes.  PyTorch supplies device memory and the current CUDA stream.  There is no CPU
+fallback: if libgenred.so is missing or no B200 is visible, the calls raise.
+
+Names follow the C ABI: ``eval`` (genred_eval), ``combine_lse`` (genred_combine_lse),
+``merge_topk`` (genred_merge_topk), ``last_plan``, ``launch_count``.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+import threading
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ROOT = os.path.dirname(HERE)
+LIB_PATH = os.path.join(HERE, "libgenred.so")
+HEADER = os.path.join(ROOT, "include", "genred.h")
+
+ABI_VERSION = 1
+OK, E_INVALID, E_UNSUPPORTED, E_SHAPE, E_NOMEM, E_CUDA = range(6)
+STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_SHAPE", 4: "E_NOMEM", 5: "E_CUDA"}
+
+FORMULAS = {"gauss": 0, "gauss_gradx": 1, "sqdist": 2, "gauss_sum_gradx": 3}
+REDUCTIONS = {"sum": 0, "lse": 1, "argkmin": 2}
+F32, F64 = 0, 1
+MEM_DEVICE, MEM_HOST = 0, 1
+
+
+class GenredError(RuntimeError):
+    def __init__(self, status: int, msg: str):
+        super().__init__(f"genred {STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+class Args(ctypes.Structure):
+    """Mirror of ``genred_args`` (include/genred.h); field order and types must match."""
+    _fields_ = [
+        ("abi_version", ctypes.c_int32), ("formula", ctypes.c_int32),
+        ("reduction", ctypes.c_int32), ("memory", ctypes.c_int32),
+        ("M", ctypes.c_int64), ("N", ctypes.c_int64),
+        ("D", ctypes.c_int32), ("E", ctypes.c_int32), ("K", ctypes.c_int32),
+        ("split_j", ctypes.c_int32), ("scale", ctypes.c_double),
+        ("x", ctypes.c_void_p), ("y", ctypes.c_void_p), ("b", ctypes.c_void_p),
+        ("g", ctypes.c_void_p), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
+        ("pad0", ctypes.c_int32), ("out_grad", ctypes.c_void_p), ("out_idx", ctypes.c_void_p),
+        ("lse_state", ctypes.c_void_p), ("j_offset", ctypes.c_int64),
+    ]
+
+
+class Plan(ctypes.Structure):
+    _fields_ = [("split_j", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32),
+                ("ctas", ctypes.c_int32), ("tile_j", ctypes.c_int32), ("kernels", ctypes.c_int32),
+                ("path", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64)]
+
+
+_lib = None
+_lock = threading.Lock()
+_ctxs: dict = {}
+
+
+def header_functions() -> list:
+    """Names of every function declared in include/genred.h."""
+    txt = open(HEADER).read()
+    return sorted(set(re.findall(r"\b(genred_[a-z_]+)\s*\(", txt)))
+
+
+def load():
+    """Load libgenred.so (build it first with ``python -m paper_2004_11127_b200.build``)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"libgenred.so not built at {LIB_PATH}; run "
+                               "`python -m paper_2004_11127_b200.build` (no CPU fallback exists)")
+        lib = ctypes.CDLL(LIB_PATH)
+        P, I32, I64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64
+        lib.genred_abi_version.restype = I32
+        lib.genred_build_info.restype = ctypes.c_char_p
+        lib.genred_create.argtypes = [I32, ctypes.POINTER(P)]
+        lib.genred_create.restype = I32
+        lib.genred_destroy.argtypes = [P]
+        lib.genred_destroy.restype = None
+        lib.genred_last_error.argtypes = [P]
+        lib.genred_last_error.restype = ctypes.c_char_p
+        lib.genred_validate.argtypes = [ctypes.POINTER(Args), ctypes.c_char_p, ctypes.c_size_t]
+        lib.genred_validate.restype = I32
+        lib.genred_eval.argtypes = [P, ctypes.POINTER(Args), P]
+        lib.genred_eval.restype = I32
+        lib.genred_combine_lse.argtypes = [P, I64, I32, P, P, I32, P, P]
+        lib.genred_combine_lse.restype = I32
+        lib.genred_merge_topk.argtypes = [P, I64, I32, I32, P, P, P, P, P]
+        lib.genred_merge_topk.restype = I32
+        lib.genred_last_plan.argtypes = [P, ctypes.POINTER(Plan)]
+        lib.genred_last_plan.restype = I32
+        lib.genred_launch_count.argtypes = [P]
+        lib.genred_launch_count.restype = I64
+        lib.genred_profile.argtypes = [P, I32]
+        lib.genred_profile.restype = I32
+        lib.genred_profile_read.argtypes = [P, P, I32]
+        lib.genred_profile_read.restype = I32
+        if lib.genred_abi_version() != ABI_VERSION:
+            raise RuntimeError("libgenred ABI version mismatch")
+        _lib = lib
+        return lib
+
+
+def context(device: int | None = None):
+    """Per-device genred_ctx (created on first use)."""
+    import torch
+    lib = load()
+    if device is None:
+        device = torch.cuda.current_device()
+    with _lock:
+        if device not in _ctxs:
+            h = ctypes.c_void_p()
+            st = lib.genred_create(int(device), ctypes.byref(h))
+            if st != OK:
+                raise GenredError(st, f"genred_create(device={device}) failed (needs a B200, sm_100a)")
+            _ctxs[device] = h
+        return _ctxs[device]
+
+
+def validate(args: Args) -> tuple:
+    buf = ctypes.create_string_buffer(256)
+    st = load().genred_validate(ctypes.byref(args), buf, 256)
+    return st, buf.value.decode()
+
+
+def last_plan(device: int | None = None) -> dict:
+    p = Plan()
+    load().genred_last_plan(context(device), ctypes.byref(p))
+    return {k: getattr(p, k) for k, _ in Plan._fields_}
+
+
+def launch_count(device: int | None = None) -> int:
+    return int(load().genred_launch_count(context(device)))
+
+
+def profile(enable: bool, device: int | None = None) -> None:
+    """genred_profile: record CUDA events around every main kernel from now on (or stop)."""
+    load().genred_profile(context(device), 1 if enable else 0)
+
+
+def profile_read(device: int | None = None, max_n: int = 4096) -> list:
+    """genred_profile_read: durations (ms) of the main kernels recorded since profile(True)."""
+    buf = (ctypes.c_float * max_n)()
+    n = load().genred_profile_read(context(device), buf, max_n)
+    if n < 0:
+        raise GenredError(E_CUDA, "genred_profile_read failed")
+    return [float(buf[k]) for k in range(n)]
+
+
+def _ptr(t):
+    if t is None:
+        return None
+    if isinstance(t, np.ndarray):
+        return t.ctypes.data
+    return t.data_ptr()
+
+
+def _check(t, name, dtype_ok=("float32",)):
+    if t is None:
+        return
+    if isinstance(t, np.ndarray):
+        if not t.flags["C_CONTIGUOUS"] or str(t.dtype) not in dtype_ok:
+            raise ValueError(f"{name} must be a C-contiguous {dtype_ok} numpy array")
+        return
+    if not t.is_contiguous() or str(t.dtype).replace("torch.", "") not in dtype_ok:
+        raise ValueError(f"{name} must be a contiguous {dtype_ok} tensor")
+
+
+def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1.0, K: int = 1,
+         out=None, out_dtype: str = "float32", out_grad=None, out_idx=None, lse_state=None,
+         split_j: int = 0, j_offset: int = 0, stream=None):
+    """Evaluate a_i = Reduction_j F(x_i, y_j) (Eq. 1) through genred_eval.
+
+    x: (M, D), y: (N, D), b: (N, E) (or h: (N,) for LSE), g: (M, E); fp32, contiguous, all CUDA
+    tensors (device mode, asynchronous on ``stream`` / the current stream) or all numpy arrays
+    (host mode: staged H2D -> kernels -> D2H inside libgenred, synchronous).
+    Returns out (and out_grad / out_idx when applicable).
+    """
+    host = isinstance(x, np.ndarray)
+    M, D = int(x.shape[0]), int(x.shape[1])
+    N = int(y.shape[0])
+    f, r = FORMULAS[formula], REDUCTIONS[reduction]
+    E = 1
+    if b is not None and r != REDUCTIONS["lse"]:
+        E = int(b.shape[1]) if b.ndim == 2 else 1
+    elif g is not None:
+        E = int(g.shape[1]) if g.ndim == 2 else 1
+    for t, n in ((x, "x"), (y, "y"), (b, "b"), (g, "g")):
+        _check(t, n)
+    odt = F64 if out_dtype in ("float64", "f64") else F32
+    if out is None:
+        if r == REDUCTIONS["argkmin"]:
+            oshape, odtype = (M, K), "float32"
+        elif r == REDUCTIONS["lse"]:
+            oshape, odtype = (M,), out_dtype
+        elif f == FORMULAS["gauss_gradx"]:
+            oshape, odtype = (M, D), out_dtype
+        else:
+            oshape, odtype = (M, E), out_dtype
+        if host:
+            out = np.empty(oshape, dtype=odtype)
+        else:
+            import torch
+            out = torch.empty(oshape, dtype=getattr(torch, odtype), device=x.device)
+    if f == FORMULAS["gauss_sum_gradx"] and out_grad is None:
+        if host:
+            out_grad = np.empty((M, D), np.float32)
+        else:
+            import torch
+            out_grad = torch.empty((M, D), dtype=torch.float32, device=x.device)
+    if r == REDUCTIONS["argkmin"] and out_idx is None:
+        if host:
+            out_idx = np.empty((M, K), np.int64)
+        else:
+            import torch
+            out_idx = torch.empty((M, K), dtype=torch.int64, device=x.device)
+    a = Args()
+    a.abi_version = ABI_VERSION
+    a.formula, a.reduction = f, r
+    a.memory = MEM_HOST if host else MEM_DEVICE
+    a.M, a.N, a.D, a.E, a.K = M, N, D, E, int(K)
+    a.split_j = int(split_j)
+    a.scale = float(scale)
+    a.x, a.y, a.b, a.g = _ptr(x), _ptr(y), _ptr(b), _ptr(g)
+    a.out, a.out_dtype = _ptr(out), odt
+    a.out_grad, a.out_idx, a.lse_state = _ptr(out_grad), _ptr(out_idx), _ptr(lse_state)
+    a.j_offset = int(j_offset)
+    if host:
+        dev, sptr = None, None
+    else:
+        import torch
+        dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        sptr = ctypes.c_void_p(s.cuda_stream)
+    ctx = context(dev)
+    st = load().genred_eval(ctx, ctypes.byref(a), sptr)
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+    if r == REDUCTIONS["argkmin"]:
+        return out, out_idx
+    if f == FORMULAS["gauss_sum_gradx"]:
+        return out, out_grad
+    return out
+
+
+def eval_args(args: Args, stream=None, device: int | None = None) -> None:
+    """Call genred_eval on a prepared Args struct (used by the benchmark's timed loops)."""
+    import torch
+    ctx = context(device)
+    sptr = None
+    if args.memory == MEM_DEVICE:
+        s = stream if stream is not None else torch.cuda.current_stream()
+        sptr = ctypes.c_void_p(s.cuda_stream)
+    st = load().genred_eval(ctx, ctypes.byref(args), sptr)
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+
+
+def combine_lse(states, out=None, out_dtype: str = "float64", state_out=None, stream=None):
+    """genred_combine_lse: states (G, M, 2) fp64 CUDA tensor -> a (M,) natural-log LSE."""
+    import torch
+    G, M = int(states.shape[0]), int(states.shape[1])
+    if not states.is_contiguous() or states.dtype != torch.float64:
+        raise ValueError("states must be a contiguous float64 (G, M, 2) tensor")
+    if out is None:
+        out = torch.empty((M,), dtype=getattr(torch, out_dtype), device=states.device)
+    ctx = context(states.device.index)
+    s = stream if stream is not None else torch.cuda.current_stream(states.device)
+    st = load().genred_combine_lse(ctx, M, G, _ptr(states), _ptr(out),
+                                   F64 if out.dtype == torch.float64 else F32, _ptr(state_out),
+                                   ctypes.c_void_p(s.cuda_stream))
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+    return out
+
+
+def merge_topk(d, idx, stream=None):
+    """genred_merge_topk: (G, M, K) fp32 distances + int64 indices -> (M, K) merged lists."""
+    import torch
+    G, M, K = (int(v) for v in d.shape)
+    d_out = torch.empty((M, K), dtype=torch.float32, device=d.device)
+    i_out = torch.empty((M, K), dtype=torch.int64, device=d.device)
+    ctx = context(d.device.index)
+    s = stream if stream is not None else torch.cuda.current_stream(d.device)
+    st = load().genred_merge_topk(ctx, M, K, G, _ptr(d.contiguous()), _ptr(idx.contiguous()),
+                                  _ptr(d_out), _ptr(i_out), ctypes.c_void_p(s.cuda_stream))
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+    return d_out, i_out

@@ -1,0 +1,63 @@
+"""Parity metrics (DESIGN.md Sec. 3 readings R4, R6, R8) shared by the GPU tests and bench.py.
+
+Pure comparison logic: no method arithmetic.  The expected values always come from oracle/.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+SUM_TOL = 1e-5        # north star: max relative error <= 1e-5 for Sum and gradient (R4 metric)
+LSE_TOL = 1e-6        # north star: <= 1e-6 absolute on LSE (fp64 output, R6)
+GAP_TOL = 1e-6        # north star: index exactness required where the oracle's gap > 1e-6 (R8)
+
+
+def r4_error(gpu, orc, denom, floor: float = 1e-30) -> np.ndarray:
+    """err = |a - o| / S with S = sum_j |term_ij| per coordinate (R4); rows with S < floor
+    (complete fp32 underflow, R13) use an absolute floor."""
+    gpu = np.asarray(gpu, np.float64)
+    return np.abs(gpu - orc) / np.maximum(denom, floor)
+
+
+def assert_sum_parity(gpu, orc, denom, tol: float = SUM_TOL, what: str = ""):
+    err = r4_error(gpu, orc, denom)
+    worst = float(err.max()) if err.size else 0.0
+    assert np.all(np.isfinite(np.asarray(gpu, np.float64))), f"{what}: non-finite GPU output"
+    assert worst <= tol, f"{what}: max R4 error {worst:.3e} > {tol:.0e} at {np.unravel_index(err.argmax(), err.shape)}"
+    return worst
+
+
+def assert_lse_parity(gpu, orc, tol: float = LSE_TOL, what: str = ""):
+    gpu = np.asarray(gpu, np.float64)
+    both_inf = np.isneginf(gpu) & np.isneginf(orc)
+    err = np.where(both_inf, 0.0, np.abs(gpu - orc))
+    worst = float(err.max()) if err.size else 0.0
+    assert worst <= tol, f"{what}: max |LSE error| {worst:.3e} > {tol:.0e}"
+    return worst
+
+
+def argk_check(gpu_d, gpu_j, orc_d_k1, orc_j_k1, K: int, gap_tol: float = GAP_TOL,
+               dist_tol: float = 1e-6, what: str = ""):
+    """R8: orc_* hold the oracle's K+1 best (d, j).  Position k's index must match where the
+    relative gaps on both sides of it exceed gap_tol; elsewhere only the distance is checked.
+    Returns (#checked index positions, #distance-only positions)."""
+    gpu_d = np.asarray(gpu_d, np.float64)
+    od, oj = orc_d_k1[:, :K + 1], orc_j_k1[:, :K + 1]
+    M = od.shape[0]
+    n_idx = n_dist = 0
+    for i in range(M):
+        d = od[i]
+        for k in range(K):
+            if oj[i, k] < 0:                       # padding (K > N)
+                assert gpu_j[i, k] == -1 and np.isinf(gpu_d[i, k]), f"{what}: row {i} pad"
+                continue
+            lo = np.inf if k == 0 else (d[k] - d[k - 1]) / max(d[k], 1e-300)
+            hi = np.inf if (k + 1 >= d.shape[0] or not np.isfinite(d[k + 1])) else \
+                (d[k + 1] - d[k]) / max(d[k + 1], 1e-300)
+            if lo > gap_tol and hi > gap_tol:
+                assert gpu_j[i, k] == oj[i, k], f"{what}: row {i} pos {k}: j {gpu_j[i, k]} != {oj[i, k]}"
+                n_idx += 1
+            else:
+                n_dist += 1
+            assert abs(gpu_d[i, k] - d[k]) <= dist_tol * d[k] + 1e-30, \
+                f"{what}: row {i} pos {k}: d {gpu_d[i, k]} vs {d[k]}"
+    return n_idx, n_dist

@@ -1,0 +1,372 @@
+"""GPU parity: libgenred (through the C ABI) against the fp64 oracle, element by element.
+
+Sizes span several i-tiles (1024 rows per CTA), several j-tiles (512 records per stage) and
+ragged tails; full BASELINE.json sizes are checked on seeded row samples in the launch
+configuration bench.py times.  Tolerances (north star, readings R4/R6/R8 in DESIGN.md):
+Sum/gradient R4 error <= 1e-5, LSE <= 1e-6 absolute (fp64 output), ArgKMin indices exact where
+the oracle's gaps exceed 1e-6.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synth
+from tests.parity import assert_sum_parity, assert_lse_parity, argk_check
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def G():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    from paper_2004_11127_b200 import genred
+    genred.context(0)
+    return genred
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def host(t):
+    return t.detach().cpu().numpy()
+
+
+# ------------------------------------------------------------------------------------------------
+# Gaussian Sum / gradient / fused, small-D grid with ragged tails
+# ------------------------------------------------------------------------------------------------
+
+SHAPES = [(1, 1), (1, 7), (37, 1), (1000, 1000), (2500, 3333), (1025, 513), (3000, 600)]
+
+
+@pytest.mark.parametrize("M,N", SHAPES)
+@pytest.mark.parametrize("dist", ["U3", "GMM3"])
+def test_gauss_sum_c1_like(G, M, N, dist):
+    x = synth.points(dist, M, 1001); y = synth.points(dist, N, 2001)
+    b = synth.signal(N, 3001)
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5)
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+    assert_sum_parity(host(a), o, den, what=f"gauss_sum {dist} {M}x{N}")
+
+
+@pytest.mark.parametrize("D,E", [(1, 1), (2, 1), (3, 2), (4, 4), (5, 1), (8, 3), (7, 2)])
+def test_gauss_sum_dims(G, D, E):
+    M, N = 1500, 2100
+    rng = np.random.default_rng(D * 10 + E)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = rng.standard_normal((N, E)).astype(np.float32)
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.8)
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.8)
+    assert_sum_parity(host(a), o, den, what=f"gauss D={D} E={E}")
+
+
+@pytest.mark.parametrize("D,E", [(3, 1), (1, 1), (2, 2), (5, 3), (8, 1), (4, 4)])
+@pytest.mark.parametrize("with_g", [False, True])
+def test_gauss_gradx(G, D, E, with_g):
+    M, N = 1300, 1700
+    rng = np.random.default_rng(100 + D * 10 + E)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = rng.standard_normal((N, E)).astype(np.float32)
+    g = rng.standard_normal((M, E)).astype(np.float32) if with_g else None
+    out = G.eval("gauss_gradx", "sum", dev(x), dev(y), dev(b), None if g is None else dev(g), scale=0.5)
+    o, den = oracle.gauss_gradx(x, y, b, g, sigma=0.5)
+    assert_sum_parity(host(out), o, den, what=f"gradx D={D} E={E} g={with_g}")
+
+
+@pytest.mark.parametrize("D,E", [(3, 1), (2, 3), (6, 2)])
+def test_gauss_sum_gradx_fused(G, D, E):
+    M, N = 2049, 1500
+    rng = np.random.default_rng(7 + D + E)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = rng.random((N, E)).astype(np.float32)
+    g = rng.standard_normal((M, E)).astype(np.float32)
+    s, gr = G.eval("gauss_sum_gradx", "sum", dev(x), dev(y), dev(b), dev(g), scale=0.5)
+    os_, dens = oracle.gauss_sum(x, y, b, sigma=0.5)
+    og, deng = oracle.gauss_gradx(x, y, b, g, sigma=0.5)
+    assert_sum_parity(host(s), os_, dens, what="fused sum")
+    assert_sum_parity(host(gr), og, deng, what="fused grad")
+
+
+def test_sqdist_sum_closed_form_combo(G):
+    M, N = 1100, 2600
+    x = synth.uniform3(M, 5); y = synth.gmm3(N, 6); b = synth.signal(N, 7, E=2, signed=True)
+    a = G.eval("sqdist", "sum", dev(x), dev(y), dev(b))
+    o, den = oracle.sqdist_sum(x, y, b)
+    assert_sum_parity(host(a), o, den, what="sqdist sum")
+
+
+def test_single_point_bit_exact(G):
+    """P1: x = y gives exp(0) b = b exactly (d = 0 -> MUFU.EX2(-0) = 1)."""
+    x = np.array([[0.3, 0.7, 0.1]], np.float32); b = np.array([[1.75]], np.float32)
+    a = G.eval("gauss", "sum", dev(x), dev(x), dev(b), scale=0.5)
+    assert host(a)[0, 0] == np.float32(1.75)
+    gr = G.eval("gauss_gradx", "sum", dev(x), dev(x), dev(b), scale=0.5)
+    assert np.all(host(gr) == 0.0)
+
+
+def test_spec_worked_examples(G, golden):
+    for ex in golden["gauss_sum"]:
+        a = G.eval("gauss", "sum", dev(np.array(ex["x"], np.float32)), dev(np.array(ex["y"], np.float32)),
+                   dev(np.array(ex["b"], np.float32)), scale=ex["sigma"])
+        np.testing.assert_allclose(host(a), ex["expected"], rtol=1e-6, err_msg=ex["cite"])
+    for ex in golden["gauss_gradx"]:
+        a = G.eval("gauss_gradx", "sum", dev(np.array(ex["x"], np.float32)),
+                   dev(np.array(ex["y"], np.float32)), dev(np.array(ex["b"], np.float32)),
+                   dev(np.array(ex["g"], np.float32)), scale=ex["sigma"])
+        np.testing.assert_allclose(host(a), ex["expected"], rtol=1e-6, atol=1e-7, err_msg=ex["cite"])
+    for ex in golden["lse"]:
+        y = np.array(ex["y"], np.float32).reshape(-1, 3)
+        h = None if ex["h"] is None else dev(np.array(ex["h"], np.float32))
+        a = G.eval("sqdist", "lse", dev(np.array(ex["x"], np.float32)), dev(y), h, scale=ex["eps"],
+                   out_dtype="float64")
+        e = float(ex["expected"][0]) if not isinstance(ex["expected"][0], str) else -math.inf
+        if math.isinf(e):
+            assert host(a)[0] == -math.inf
+        else:
+            assert abs(host(a)[0] - e) <= 1e-6, ex["cite"]
+    for ex in golden["argkmin"]:
+        x = np.array(ex["x"], np.float32); y = np.array(ex["y"], np.float32).reshape(-1, x.shape[1])
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=ex["K"])
+        assert host(j).tolist() == ex["expected_idx"], ex["cite"]
+
+
+@pytest.mark.parametrize("split", [1, 2, 3, 7])
+def test_split_invariance_and_determinism(G, split):
+    """Tiling invariance across forced j-splits; bitwise determinism run to run."""
+    M, N = 3000, 9000
+    x = synth.gmm3(M, 11); y = synth.gmm3(N, 12); b = synth.signal(N, 13, signed=True)
+    a1 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
+    assert G.last_plan()["split_j"] == split
+    a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
+    assert torch.equal(a1, a2)
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+    assert_sum_parity(host(a1), o, den, what=f"split={split}")
+
+
+def test_host_mode_matches_device_mode(G):
+    M, N = 2000, 3000
+    x = synth.uniform3(M, 21); y = synth.uniform3(N, 22); b = synth.signal(N, 23)
+    ad = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5))
+    ah = G.eval("gauss", "sum", x, y, b, scale=0.5)
+    np.testing.assert_array_equal(ad, ah)
+    ld = host(G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64"))
+    lh = G.eval("sqdist", "lse", x, y, None, scale=0.05, out_dtype="float64")
+    np.testing.assert_array_equal(ld, lh)
+
+
+# ------------------------------------------------------------------------------------------------
+# Log-sum-exp
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("M,N", [(1, 1), (5, 17), (1000, 1000), (2500, 7001), (1030, 40000)])
+@pytest.mark.parametrize("hkind", ["zero", "random"])
+def test_lse(G, M, N, hkind):
+    x = synth.uniform3(M, 31); y = synth.gmm3(N, 32)
+    h = None if hkind == "zero" else (np.random.default_rng(33).standard_normal(N) * 3).astype(np.float32)
+    a = G.eval("sqdist", "lse", dev(x), dev(y), None if h is None else dev(h), scale=0.05,
+               out_dtype="float64")
+    o, _ = oracle.lse(x, y, h, eps=0.05)
+    assert_lse_parity(host(a), o, what=f"lse {M}x{N} h={hkind}")
+
+
+@pytest.mark.parametrize("D", [1, 2, 5, 8])
+def test_lse_dims(G, D):
+    rng = np.random.default_rng(D)
+    x = rng.random((900, D)).astype(np.float32); y = rng.random((2000, D)).astype(np.float32)
+    a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.1, out_dtype="float64")
+    o, _ = oracle.lse(x, y, None, eps=0.1)
+    assert_lse_parity(host(a), o, what=f"lse D={D}")
+
+
+def test_lse_stability_extremes(G):
+    """SPEC S:274 / S:300: huge spreads of F never overflow."""
+    x = np.zeros((3, 3), np.float32)
+    y = np.zeros((600, 3), np.float32)
+    h = np.zeros(600, np.float32); h[0] = 1e4; h[1] = -1e4; h[599] = 9999.0
+    a = host(G.eval("sqdist", "lse", dev(x), dev(y), dev(h), scale=1.0, out_dtype="float64"))
+    o, _ = oracle.lse(x, y, h, eps=1.0)
+    assert np.all(np.isfinite(a))
+    assert_lse_parity(a, o, tol=2e-3, what="extremes")   # fp32 h' = log2e*h carries ~1e-3 at |h|=1e4
+
+
+@pytest.mark.parametrize("split", [1, 2, 5])
+def test_lse_split_state_and_combine(G, split):
+    M, N = 1500, 12000
+    x = synth.uniform3(M, 41); y = synth.gmm3(N, 42)
+    st = torch.empty((M, 2), dtype=torch.float64, device="cuda")
+    a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64",
+               lse_state=st, split_j=split)
+    o, _ = oracle.lse(x, y, None, eps=0.05)
+    assert_lse_parity(host(a), o, what=f"lse split={split}")
+    s = host(st)
+    np.testing.assert_allclose(math.log(2) * (s[:, 0] + np.log2(s[:, 1])), host(a), rtol=0, atol=1e-12)
+
+
+def test_combine_lse_spec_example(G):
+    """(m=0, s=2) (+) (m=1, s=1) = (1, 1 + 2/e), natural-log units.  Our states are in
+    log2 units: m2 = m / ln 2 and s unchanged."""
+    l2 = 1 / math.log(2)
+    states = torch.tensor([[[0.0 * l2, 2.0]], [[1.0 * l2, 1.0]]], dtype=torch.float64, device="cuda")
+    so = torch.empty((1, 2), dtype=torch.float64, device="cuda")
+    a = G.combine_lse(states, state_out=so)
+    s = host(so)[0]
+    assert abs(s[0] - l2) < 1e-15 and abs(s[1] - (1 + 2 * math.exp(-1))) < 1e-15
+    assert abs(host(a)[0] - (1 + math.log(1 + 2 * math.exp(-1)))) < 1e-15
+
+
+def test_jshard_emulated_lse_sum_argk(G):
+    """j-sharded evaluation (north star (d)) emulated on one GPU: shards of y, partial states,
+    combine_lse / fp64 partial sums / merge_topk -> equals the oracle on the whole range."""
+    M, N, Gs = 800, 9001, 3
+    x = synth.uniform3(M, 51); y = synth.gmm3(N, 52); b = synth.signal(N, 53)
+    bounds = [N * r // Gs for r in range(Gs + 1)]
+    states, sums, ds, js = [], [], [], []
+    for r in range(Gs):
+        lo, hi = bounds[r], bounds[r + 1]
+        st = torch.empty((M, 2), dtype=torch.float64, device="cuda")
+        G.eval("sqdist", "lse", dev(x), dev(y[lo:hi]), None, scale=0.05, out_dtype="float64", lse_state=st)
+        states.append(st)
+        sums.append(G.eval("gauss", "sum", dev(x), dev(y[lo:hi]), dev(b[lo:hi]), scale=0.5, out_dtype="float64"))
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y[lo:hi]), K=5, j_offset=lo)
+        ds.append(d); js.append(j)
+    a = G.combine_lse(torch.stack(states))
+    o, _ = oracle.lse(x, y, None, eps=0.05)
+    assert_lse_parity(host(a), o, what="jshard lse")
+    s = host(torch.stack(sums).sum(0))
+    os_, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+    assert_sum_parity(s, os_, den, what="jshard sum")
+    dm, jm = G.merge_topk(torch.stack(ds), torch.stack(js))
+    od, oj = oracle.argkmin(x, y, 6)
+    argk_check(host(dm), host(jm), od, oj, 5, what="jshard argk")
+
+
+# ------------------------------------------------------------------------------------------------
+# ArgKMin (small D, FP32 path)
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("M,N,D,K", [(1000, 1000, 3, 1), (1000, 3001, 3, 10), (2100, 5000, 2, 4),
+                                     (700, 2000, 7, 16), (300, 1500, 16, 32), (50, 3, 3, 5),
+                                     (1, 1, 1, 1)])
+def test_argkmin_small_d(G, M, N, D, K):
+    rng = np.random.default_rng(M + N + D + K)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+    od, oj = oracle.argkmin(x, y, K + 1)
+    argk_check(host(d), host(j), od, oj, K, what=f"argk {M}x{N} D={D} K={K}")
+
+
+def test_argkmin_lattice_ties(G):
+    """P7 on the GPU: node, then the 6 unit neighbours in ascending j, then the d^2=2 ring."""
+    g = np.arange(5, dtype=np.float32)
+    grids = np.meshgrid(g, g, g, indexing="ij")
+    y = np.stack([q.reshape(-1) for q in grids], 1)
+    x = np.array([[2, 2, 2]], np.float32)
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=8)
+    assert host(j)[0].tolist() == [62, 37, 57, 61, 63, 67, 87, 32]
+    assert host(d)[0].tolist() == [0, 1, 1, 1, 1, 1, 1, 2]
+
+
+@pytest.mark.parametrize("split", [1, 3])
+def test_argkmin_duplicates_across_splits(G, split):
+    y = np.tile(np.array([[0.5, 0.5, 0.5]], np.float32), (4000, 1))
+    x = np.array([[0.5, 0.5, 0.5], [0.4, 0.5, 0.5]], np.float32)
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=6, split_j=split)
+    assert host(j).tolist() == [[0, 1, 2, 3, 4, 5]] * 2
+
+
+# ------------------------------------------------------------------------------------------------
+# Degenerate inputs and error paths
+# ------------------------------------------------------------------------------------------------
+
+def test_empty_axes(G):
+    x = dev(synth.uniform3(5, 1)); y0 = dev(np.zeros((0, 3), np.float32))
+    a = G.eval("gauss", "sum", x, y0, dev(np.zeros((0, 1), np.float32)), scale=0.5)
+    assert torch.all(a == 0)
+    l = G.eval("sqdist", "lse", x, y0, None, scale=0.05, out_dtype="float64")
+    assert torch.all(torch.isneginf(l))
+    d, j = G.eval("sqdist", "argkmin", x, y0, K=3)
+    assert torch.all(j == -1) and torch.all(torch.isinf(d))
+    x0 = dev(np.zeros((0, 3), np.float32))
+    a = G.eval("gauss", "sum", x0, dev(synth.uniform3(5, 2)), None, scale=0.5)
+    assert a.shape == (0, 1)
+
+
+def test_k_larger_than_n_pads(G):
+    x = dev(synth.uniform3(3, 1)); y = dev(synth.uniform3(2, 2))
+    d, j = G.eval("sqdist", "argkmin", x, y, K=4)
+    assert torch.all(j[:, 2:] == -1) and torch.all(torch.isinf(d[:, 2:]))
+    assert torch.all(j[:, :2] >= 0)
+
+
+def test_error_paths_write_nothing(G):
+    x = dev(synth.uniform3(10, 1)); y = dev(synth.uniform3(10, 2))
+    out = torch.full((10, 1), 123.0, device="cuda")
+    with pytest.raises(G.GenredError) as ei:
+        G.eval("gauss", "sum", x, y, None, scale=-1.0, out=out)
+    assert ei.value.status == G.E_INVALID
+    with pytest.raises(G.GenredError) as ei:
+        G.eval("gauss", "lse", x, y, None, scale=1.0, out=out)
+    assert ei.value.status == G.E_UNSUPPORTED
+    with pytest.raises(G.GenredError) as ei:
+        G.eval("sqdist", "argkmin", x, y, K=0)
+    assert ei.value.status == G.E_SHAPE
+    torch.cuda.synchronize()
+    assert torch.all(out == 123.0)
+
+
+def test_linear_memory_scratch(G):
+    """PAPER.md:96 (linear memory): scratch is O((M+N)(D+E)), never O(M N)."""
+    x = dev(synth.uniform3(20000, 1)); y = dev(synth.uniform3(20000, 2)); b = dev(synth.signal(20000, 3))
+    G.eval("gauss", "sum", x, y, b, scale=0.5, split_j=1)
+    sb = G.last_plan()["scratch_bytes"]
+    assert sb < 64 * (20000 + 20000) * 4 + (1 << 20)
+
+
+# ------------------------------------------------------------------------------------------------
+# Full BASELINE.json sizes, sampled rows, in bench.py's launch configuration (auto plan)
+# ------------------------------------------------------------------------------------------------
+
+def _rows(M, n, seed):
+    r = np.random.default_rng(seed).choice(M, size=n, replace=False)
+    return np.sort(np.concatenate([r, [0, M - 1]]))
+
+
+def test_config2_full_size_sampled(G):
+    c = synth.config(2); sd = synth.seeds(2)
+    x = synth.uniform3(c.M, sd["x"]); y = synth.uniform3(c.N, sd["y"]); b = synth.signal(c.N, sd["b"])
+    s, gr = G.eval("gauss_sum_gradx", "sum", dev(x), dev(y), dev(b), None, scale=c.scale)
+    rows = _rows(c.M, 512, 7)
+    os_, dens = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+    og, deng = oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
+    assert_sum_parity(host(s)[rows], os_, dens, what="C2 sum")
+    assert_sum_parity(host(gr)[rows], og, deng, what="C2 grad")
+    # separate-kernel path gives the same numbers up to rounding
+    s2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=c.scale)
+    assert_sum_parity(host(s2)[rows], os_, dens, what="C2 sum (separate)")
+
+
+def test_config3_full_size_sampled(G):
+    c = synth.config(3); sd = synth.seeds(3)
+    x = synth.uniform3(c.M, sd["x"]); y = synth.gmm3(c.N, sd["y"])
+    a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=c.scale, out_dtype="float64")
+    rows = _rows(c.M, 256, 8)
+    o, _ = oracle.lse(x, y, None, eps=c.scale, rows=rows)
+    assert_lse_parity(host(a)[rows], o, what="C3 lse")
+    # all rows: max_j F <= LSE <= max_j F + log N, with max_j F from the GPU's own ArgKMin K=1
+    d, _ = G.eval("sqdist", "argkmin", dev(x), dev(y), K=1)
+    fmax = -host(d)[:, 0].astype(np.float64) / c.scale
+    A = host(a)
+    assert np.all(A >= fmax - 1e-5) and np.all(A <= fmax + math.log(c.N) + 1e-5)
+
+
+def test_config5_full_size_sampled(G):
+    c = synth.config(5); sd = synth.seeds(5)
+    x = synth.uniform3(c.M, sd["x"]); y = synth.uniform3(c.N, sd["y"]); b = synth.signal(c.N, sd["b"])
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=c.scale)
+    rows = _rows(c.M, 64, 9)
+    o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+    assert_sum_parity(host(a)[rows], o, den, what="C5 sum")
