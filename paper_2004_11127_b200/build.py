@@ -35,7 +35,7 @@ def _deps_hash(src: str) -> str:
                             + [os.path.join(ROOT, "include", "genred.h")]):
         with open(f, "rb") as fh:
             h.update(fh.read())
-    h.update(" ".join(ARCH + FLAGS).encode())
+    h.update(" ".join(ARCH + [f for f in FLAGS if not f.startswith("-I")]).encode())
     return h.hexdigest()[:16]
 
 
@@ -58,7 +58,7 @@ def build(verbose: bool = False, jobs: int | None = None) -> str:
     jobs = jobs or min(len(srcs), os.cpu_count() or 4)
     with cf.ThreadPoolExecutor(jobs) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
-    stamp = hashlib.sha1("".join(objs).encode()).hexdigest()[:16]
+    stamp = hashlib.sha1("".join(os.path.basename(o) for o in objs).encode()).hexdigest()[:16]
     stamp_file = os.path.join(BUILD, "libgenred.stamp")
     if os.path.exists(LIB) and os.path.exists(stamp_file) and open(stamp_file).read() == stamp:
         return LIB

@@ -11,7 +11,7 @@
 namespace genred {
 
 __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *__restrict__ b,
-                            int64_t N, int D, int E, float s, float hscale, int64_t npairs, int RS,
+                            int64_t N, int D, int E, float s, double hscale, int64_t npairs, int RS,
                             float *__restrict__ J) {
     const float NEG_INF = -INFINITY;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
@@ -24,26 +24,36 @@ __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *
                 float v = valid ? y[j * D + d] : 0.0f;
                 float r;
                 if (kind == PACK_GAUSS || kind == PACK_SQDIST_SUM) r = valid ? -(s * v) : 0.0f;
-                else if (kind == PACK_LSE) r = valid ? -v : NEG_INF;   // padded y at +inf distance
-                else r = valid ? -v : NEG_INF;          // ARGKMIN: padded y at +inf distance
+                else r = valid ? -v : NEG_INF;          // LSE / ARGKMIN: padded y at +inf distance
                 rec[2 * d + h] = r;
             }
             if (kind == PACK_GAUSS || kind == PACK_SQDIST_SUM) {
                 for (int e = 0; e < E; ++e)
                     rec[2 * D + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
-            } else if (kind == PACK_LSE) {
-                rec[2 * D + h] = valid ? (b ? hscale * b[j] : 0.0f) : NEG_INF;
+            } else if (kind == PACK_LSE_H) {
+                // h' = log2(e) h as an fp32 hi + lo pair (fp64 product), so that
+                // (h'_hi - m) + h'_lo keeps |h| ~ 1e4 biases exact to fp32 rounding of t.
+                const double hv = valid ? hscale * (double)b[j] : 0.0;
+                const float hi = valid ? (float)hv : NEG_INF;
+                rec[2 * D + h] = hi;
+                rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
             }
         }
-        const int used = (kind == PACK_ARGKMIN) ? 2 * D : (kind == PACK_LSE ? 2 * D + 2 : 2 * (D + E));
+        const int used = (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) ? 2 * D
+                       : (kind == PACK_LSE_H ? 2 * D + 4 : 2 * (D + E));
         for (int k = used; k < RS; ++k) rec[k] = 0.0f;
     }
 }
 
+int pack_record_stride(int kind, int D, int E) {
+    if (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) return record_stride(D, 0);
+    if (kind == PACK_LSE_H) return record_stride(D, 2);
+    return record_stride(D, E);
+}
+
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E, float s,
-                        float hscale, int64_t npairs, float *J, cudaStream_t st) {
-    int RS = (kind == PACK_ARGKMIN) ? record_stride(D, 0)
-                                    : record_stride(D, kind == PACK_LSE ? 1 : E);
+                        double hscale, int64_t npairs, float *J, cudaStream_t st) {
+    const int RS = pack_record_stride(kind, D, E);
     int64_t blocks = (npairs + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;

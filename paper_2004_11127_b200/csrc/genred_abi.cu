@@ -264,7 +264,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             sc = (float)(sqrt(kLog2e) / sig);                   // 2^(-|s x - s y|^2) = e^(-|x-y|^2/sig^2)
             scale_grad = -2.0 / (sig * sig * (double)sc);        // (x - y) = (x' - y') / s
         }
-        e = launch_pack(mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS, a->y, a->b, N, D, E, sc, 0.f, npairs, J, st);
+        e = launch_pack(mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         SumLaunch L;
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
@@ -293,7 +293,8 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
 
     if (red == GENRED_LSE) {
         Plan pl = make_plan(ctx, a, 1, 4, D, 0, 0);
-        const int RS = record_stride(D, 1);
+        const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
+        const int RS = pack_record_stride(pk, D, 1);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * 2 * 8) : 0;
@@ -301,7 +302,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
-        e = launch_pack(PACK_LSE, a->y, a->b, N, D, 1, 1.0f, (float)kLog2e, npairs, J, st);
+        e = launch_pack(pk, a->y, a->b, N, D, 1, 1.0f, kLog2e, npairs, J, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         LseLaunch L;
         L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
@@ -332,7 +333,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     const int K = a->K;
     const int R = argk_rows_per_thread(K);
     Plan pl = make_plan(ctx, a, 2, R, D, K, 0);
-    const int RS = record_stride(D, 0);
+    const int RS = pack_record_stride(PACK_ARGKMIN, D, 0);
     const int64_t npairs = pl.ntiles * (kTileJ / 2);
     const size_t jbytes = al256((size_t)npairs * RS * 4);
     const size_t pdb = pl.split > 1 ? al256((size_t)pl.split * M * K * 4) : 0;
@@ -341,7 +342,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     float *J = (float *)ctx->scratch;
     float *pdist = pl.split > 1 ? (float *)((char *)ctx->scratch + jbytes) : nullptr;
     int32_t *pidx = pl.split > 1 ? (int32_t *)((char *)ctx->scratch + jbytes + pdb) : nullptr;
-    e = launch_pack(PACK_ARGKMIN, a->y, nullptr, N, D, 0, 1.0f, 0.f, npairs, J, st);
+    e = launch_pack(PACK_ARGKMIN, a->y, nullptr, N, D, 0, 1.0f, 0.0, npairs, J, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
     ArgkLaunch L;
     L.D = D; L.K = K; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;

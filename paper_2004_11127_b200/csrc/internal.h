@@ -15,14 +15,17 @@ constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference
 // Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
 
-enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE = 2, PACK_ARGKMIN = 3 };
+enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4 };
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
-// kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E.
-// Records past N (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf
-// (LSE, ArgKMin), which contribute nothing.
+// kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
+// (Sum kinds), nothing more (ArgKMin, LSE with h = 0), or (h'hi[2p], h'hi[2p+1], h'lo[2p],
+// h'lo[2p+1]) with h' = hscale * h split into fp32 hi + lo (LSE with h).  Records past N
+// (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf (LSE, ArgKMin),
+// which contribute nothing.
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
-                        float s, float hscale, int64_t npairs, float *J, cudaStream_t st);
+                        float s, double hscale, int64_t npairs, float *J, cudaStream_t st);
+int pack_record_stride(int kind, int D, int E);
 
 struct SumLaunch {
     int mode;                 // 0 SUM, 1 GRADX, 2 SUM_GRADX, 3 SQDIST_SUM

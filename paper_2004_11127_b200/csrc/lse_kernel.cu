@@ -26,9 +26,10 @@ constexpr float kTau = 8.0f;          // lazy-rescale threshold, log2 units
 constexpr int kSub = 8;               // record pairs per sub-chunk (16 j)
 constexpr int kPromote = 8;           // sub-chunks per fp64 promotion (128 j)
 
-template <int D>
+template <int D, bool HZ>
 struct LseCfg {
-    static constexpr int RS = ((2 * (D + 1)) + 3) / 4 * 4;
+    // records: 2D coordinates (-y), then for h != 0 the pair of fp32 h'hi and h'lo
+    static constexpr int RS = ((2 * D + (HZ ? 0 : 4)) + 3) / 4 * 4;
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
     static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
@@ -48,7 +49,7 @@ struct LseParams {
 
 template <int D, int R, bool HZ>
 __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
-    using Cfg = LseCfg<D>;
+    using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
     float *tiles = reinterpret_cast<float *>(smem_raw);
@@ -130,7 +131,11 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                 float2 ny[D];
 #pragma unroll
                 for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
-                const float2 hp = make_float2(f[2 * D], f[2 * D + 1]);
+                float2 hhi = make_float2(0.f, 0.f), hlo = make_float2(0.f, 0.f);
+                if constexpr (!HZ) {
+                    hhi = make_float2(f[2 * D], f[2 * D + 1]);
+                    hlo = make_float2(f[2 * D + 2], f[2 * D + 3]);
+                }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     float2 dd = add2(dup2(xr[r][0]), ny[0]);
@@ -140,7 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                         dd = add2(dup2(xr[r][d]), ny[d]);
                         q2 = fma2(dd, dd, q2);
                     }
-                    const float2 hm = HZ ? hm0[r] : add2(hp, hm0[r]);
+                    const float2 hm = HZ ? hm0[r] : add2(add2(hhi, hm0[r]), hlo);  // (h'-m) exact-ish
                     const float2 t = fma2(q2, negc2, hm);          // v - m, log2 units
                     tm[r] = max3(tm[r], t.x, t.y);
                     cs[r] = add2(cs[r], make_float2(ex2(t.x), ex2(t.y)));
@@ -161,7 +166,9 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                                 const float dd = xr[r][d] + rec[2 * d + h];
                                 q1 = fmaf(dd, dd, q1);
                             }
-                            vmax = fmaxf(vmax, fmaf(q1, negc, HZ ? 0.0f : rec[2 * D + h]));
+                            float hv = 0.0f;
+                            if constexpr (!HZ) hv = rec[2 * D + h];
+                            vmax = fmaxf(vmax, fmaf(q1, negc, hv));
                         }
                     }
                     const float mn = fmaxf(vmax, m[r]);
@@ -179,7 +186,8 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                                 const float dd = xr[r][d] + rec[2 * d + h];
                                 q1 = fmaf(dd, dd, q1);
                             }
-                            const float hmv = HZ ? -mn : (rec[2 * D + h] + (-mn));
+                            float hmv = -mn;
+                            if constexpr (!HZ) hmv = (rec[2 * D + h] + (-mn)) + rec[2 * D + 2 + h];
                             c1 += ex2(fmaf(q1, negc, hmv));
                         }
                     }
@@ -224,7 +232,7 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
 
 template <int D, int R, bool HZ>
 static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
-    using Cfg = LseCfg<D>;
+    using Cfg = LseCfg<D, HZ>;
     auto kern = lse_kernel<D, R, HZ>;
     static bool attr_done = false;
     if (!attr_done) {
@@ -245,7 +253,7 @@ static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
 
 template <int D, int R>
 static int occ_lse() {
-    using Cfg = LseCfg<D>;
+    using Cfg = LseCfg<D, false>;
     auto kern = lse_kernel<D, R, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     int n = 0;
