@@ -43,7 +43,8 @@ __device__ __forceinline__ void topk_insert(float (&dist)[KMAX], int32_t (&idx)[
 #pragma unroll
     for (int k = 0; k < KMAX; ++k) {
         if (k < K) {
-            const bool sw = cd < dist[k];
+            // (d, j) lexicographic: a displaced entry keeps precedence over later equal d's
+            const bool sw = cd < dist[k] || (cd == dist[k] && (uint32_t)cj < (uint32_t)idx[k]);
             const float td = dist[k];
             const int32_t tj = idx[k];
             dist[k] = sw ? cd : td;

@@ -140,7 +140,8 @@ def test_split_invariance_and_determinism(G, split):
     M, N = 3000, 9000
     x = synth.gmm3(M, 11); y = synth.gmm3(N, 12); b = synth.signal(N, 13, signed=True)
     a1 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
-    assert G.last_plan()["split_j"] == split
+    ntiles = -(-N // 512)
+    assert G.last_plan()["split_j"] == -(-ntiles // -(-ntiles // split))   # j-tiles per split rounded up
     a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
     assert torch.equal(a1, a2)
     o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
@@ -170,7 +171,7 @@ def test_lse(G, M, N, hkind):
     a = G.eval("sqdist", "lse", dev(x), dev(y), None if h is None else dev(h), scale=0.05,
                out_dtype="float64")
     o, _ = oracle.lse(x, y, h, eps=0.05)
-    assert_lse_parity(host(a), o, what=f"lse {M}x{N} h={hkind}")
+    assert_lse_parity(host(a), o, rel=True, what=f"lse {M}x{N} h={hkind}")
 
 
 @pytest.mark.parametrize("D", [1, 2, 5, 8])
