@@ -65,6 +65,9 @@ def workload(cid: int) -> dict:
                     out_dtype="float32")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
+    if cid == 4:   # k-NN, D=784: 3xTF32 tcgen05 contraction (tensor-bound)
+        return dict(cfg=c, formula="sqdist", reduction="argkmin", fp32=None, mufu=None,
+                    out_dtype="float32")
     raise SystemExit(f"config {cid} is not benchmarked yet")
 
 
@@ -136,6 +139,15 @@ def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
     import oracle
     c = w["cfg"]
     t0 = time.perf_counter()
+    if w["reduction"] == "argkmin":
+        od, oj = oracle.argkmin(x, y, c.K, rows=rows)
+        dt = time.perf_counter() - t0
+        res = {"value": len(rows) * c.N / dt, "unit": UNIT, "cores": oracle.num_threads(),
+               "kind": "oracle", "seconds": round(dt, 3),
+               "sample": f"{len(rows)} seeded rows x all N={c.N}, D={c.D} (fp64 direct differences)"}
+        if gpu_rows is not None:
+            res["index_match_frac_vs_gpu"] = float(np.mean(np.asarray(gpu_rows) == oj))
+        return res
     if w["reduction"] == "lse":
         o, _ = oracle.lse(x, y, None, eps=c.scale, rows=rows)
         den = None
@@ -162,6 +174,8 @@ def make_inputs(w: dict, dist_kind: str):
     sd = synth.seeds(c.cid)
     xk = dist_kind if w["reduction"] != "lse" else c.x_dist
     yk = dist_kind if w["reduction"] != "lse" else c.y_dist
+    if c.cid == 4:
+        xk = yk = "MNIST784"
     x = synth.points(xk, c.M, sd["x"], c.D)
     y = synth.points(yk, c.N, sd["y"], c.D)
     b = synth.signal(c.N, sd["b"], c.E) if w["reduction"] == "sum" else None
@@ -175,12 +189,15 @@ def run_reference(args, rank: int, world: int) -> None:
     w = workload(args.config)
     c = w["cfg"]
     x, y, b = make_inputs(w, args.dist)
-    rows_per_step = max(1, int(args.ref_pairs // c.N))
+    ref_pairs = args.ref_pairs or (1e9 if w["reduction"] != "argkmin" else 1e9 / c.D)
+    rows_per_step = max(1, int(ref_pairs // c.N))
     rng = np.random.default_rng(12345)
 
     def step():
         rows = np.sort(rng.choice(c.M, size=rows_per_step, replace=False))
-        if w["reduction"] == "lse":
+        if w["reduction"] == "argkmin":
+            oracle.argkmin(x, y, c.K, rows=rows)
+        elif w["reduction"] == "lse":
             oracle.lse(x, y, None, eps=c.scale, rows=rows)
         elif w["formula"] == "gauss_sum_gradx":
             oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
@@ -220,8 +237,8 @@ def main() -> None:
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--dist", default="U3", choices=["U3", "GMM3"])
-    ap.add_argument("--cpu-rows", type=int, default=1024, help="oracle sample rows (cpu_baseline)")
-    ap.add_argument("--ref-pairs", type=float, default=1e9, help="oracle pairs per reference step")
+    ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (cpu_baseline); 0 = auto")
+    ap.add_argument("--ref-pairs", type=float, default=0, help="oracle pairs per reference step (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
@@ -253,8 +270,10 @@ def main() -> None:
     if b is not None:
         bd = torch.from_numpy(b).to(dev) if rank == 0 else torch.empty(b.shape, dtype=torch.float32, device=dev)
     Ml = hi - lo
-    out_shape = (Ml,) if w["reduction"] == "lse" else (Ml, c.E)
+    argk = w["reduction"] == "argkmin"
+    out_shape = (Ml,) if w["reduction"] == "lse" else ((Ml, c.K) if argk else (Ml, c.E))
     out = torch.empty(out_shape, dtype=getattr(torch, w["out_dtype"]), device=dev)
+    out_idx = torch.empty((Ml, c.K), dtype=torch.int64, device=dev) if argk else None
     out_grad = torch.empty((Ml, c.D), dtype=torch.float32, device=dev) \
         if w["formula"] == "gauss_sum_gradx" else None
     stream = torch.cuda.current_stream(dev)
@@ -264,8 +283,9 @@ def main() -> None:
             dist.broadcast(yd, src=0)
             if bd is not None:
                 dist.broadcast(bd, src=0)
-        genred.eval(w["formula"], w["reduction"], xd, yd, bd, None, scale=c.scale, out=out,
-                    out_dtype=w["out_dtype"], out_grad=out_grad, stream=stream)
+        genred.eval(w["formula"], w["reduction"], xd, yd, bd, None, scale=c.scale, K=c.K, out=out,
+                    out_dtype=w["out_dtype"], out_grad=out_grad, out_idx=out_idx, j_offset=0,
+                    stream=stream)
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -316,16 +336,32 @@ def main() -> None:
     kmean = max_over_ranks(kmean)
     peaks = measured_peaks()
     mhz_max = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
-    peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
-    achieved = Ml * N / (kmean * 1e-3)
+    if argk:
+        plan["fallback_rows"] = genred.last_plan(local)["fallback_rows"]
     traffic = ncu_traffic(args.config)
-    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
-                "frac": achieved / peak, "traffic": traffic,
-                "kernel": f"{w['formula']}/{w['reduction']} pair loop", "kernel_ms": kmean,
-                "share_of_step": kmean / ms_step if world == 1 else None,
-                "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
-                              f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
-                "pairs_per_launch": Ml * N}
+    if argk:
+        # tensor-bound: 3xTF32 = three tf32 GEMMs of 2*M*N*D flops each, against the measured
+        # bf16 dense peak x the nominal tf32/bf16 ratio 1/2 (B200_PROFILING.md)
+        bf16 = float(peaks.get("bf16_tflops", 1590.0))
+        peak_t = bf16 * 0.5
+        flops = 3 * 2.0 * Ml * N * c.D
+        achieved_t = flops / (kmean * 1e-3) / 1e12
+        roofline = {"bound": "tensor", "achieved": achieved_t, "peak": peak_t, "unit": "TFLOP/s",
+                    "frac": achieved_t / peak_t, "traffic": traffic,
+                    "kernel": "knn_tc_kernel (tcgen05 kind::tf32, 3xTF32)", "kernel_ms": kmean,
+                    "share_of_step": kmean / ms_step if world == 1 else None,
+                    "peak_basis": f"bf16_tflops {bf16:.1f} (MEASURED_PEAKS.json, burst) x 0.5 (tf32/bf16 nominal)",
+                    "flops_per_launch": flops, "exact_fp32_equivalent_flops": 2.0 * Ml * N * c.D}
+    else:
+        peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
+        achieved = Ml * N / (kmean * 1e-3)
+        roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
+                    "frac": achieved / peak, "traffic": traffic,
+                    "kernel": f"{w['formula']}/{w['reduction']} pair loop", "kernel_ms": kmean,
+                    "share_of_step": kmean / ms_step if world == 1 else None,
+                    "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
+                                  f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                    "pairs_per_launch": Ml * N}
 
     # ---------------- end-to-end: host buffers through the C ABI (H2D + D2H inside) ----------------
     e2e = None
@@ -335,6 +371,7 @@ def main() -> None:
         bh = torch.from_numpy(b).pin_memory() if b is not None else None
         oh = torch.empty(out_shape, dtype=getattr(torch, w["out_dtype"])).pin_memory()
         gh = torch.empty((Ml, c.D), dtype=torch.float32).pin_memory() if out_grad is not None else None
+        ih = torch.empty((Ml, c.K), dtype=torch.int64).pin_memory() if argk else None
         a = genred.Args()
         a.abi_version = genred.ABI_VERSION
         a.formula, a.reduction = genred.FORMULAS[w["formula"]], genred.REDUCTIONS[w["reduction"]]
@@ -345,6 +382,8 @@ def main() -> None:
         a.out = oh.data_ptr()
         a.out_dtype = genred.F64 if w["out_dtype"] == "float64" else genred.F32
         a.out_grad = gh.data_ptr() if gh is not None else None
+        a.out_idx = ih.data_ptr() if ih is not None else None
+        a.K = c.K
         genred.eval_args(a, stream=stream)                      # warm the staging buffers
         barrier()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -356,7 +395,8 @@ def main() -> None:
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1))
         h2d = xh.numel() * 4 + yh.numel() * 4 + (bh.numel() * 4 if bh is not None else 0)
-        d2h = oh.numel() * oh.element_size() + (gh.numel() * 4 if gh is not None else 0)
+        d2h = oh.numel() * oh.element_size() + (gh.numel() * 4 if gh is not None else 0) + \
+            (ih.numel() * 8 if ih is not None else 0)
         e2e = {"value": M * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
                "h2d_bytes_per_step": int(sum_over_ranks(h2d)),
                "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
@@ -365,8 +405,10 @@ def main() -> None:
     # ---------------- fp64 oracle on the host cores (rank 0, N=1 only) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
-        rows = np.sort(np.random.default_rng(777).choice(M, size=min(args.cpu_rows, M), replace=False))
-        cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=out.cpu().numpy()[rows])
+        nrows = args.cpu_rows or max(16, min(M, int(1e10 // (N * (c.D if argk else 1)))))
+        rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
+        gpu_rows = (out_idx if argk else out).cpu().numpy()[rows]
+        cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=gpu_rows)
 
     if rank == 0:
         line = {
@@ -380,7 +422,8 @@ def main() -> None:
                        "l2": "inputs larger than L2 (280 MB vs 126 MB); no flush" if c.cid == 5 else
                              "inputs re-read from HBM/L2 each step; no flush",
                        "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"],
-                       "ctas": plan["ctas"]},
+                       "ctas": plan["ctas"], "K": c.K if argk else None,
+                       "fallback_rows": plan.get("fallback_rows")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }

@@ -78,8 +78,9 @@ typedef enum { GENRED_MEM_DEVICE = 0, GENRED_MEM_HOST = 1 } genred_memory;
  *   (GAUSS, SUM), (GAUSS_GRADX, SUM), (GAUSS_SUM_GRADX, SUM): 1 <= D <= 8, 1 <= E <= 4
  *   (SQDIST, SUM): 1 <= D <= 8, 1 <= E <= 4 (closed-form test combination)
  *   (SQDIST, LSE): 1 <= D <= 8, E == 1
- *   (SQDIST, ARGKMIN): 1 <= K <= 32 with 1 <= D <= 16 (FP32 path), or D >= 32, D % 4 == 0
- *                      (tensor-core path, x and y rows 16-byte aligned), E == 1
+ *   (SQDIST, ARGKMIN): E == 1 and either 1 <= D <= 16, 1 <= K <= 32 (FP32 path), or
+ *                      17 <= D <= 16384, 1 <= K <= 28 (tcgen05 3xTF32 screening + exact fp64
+ *                      re-rank of the K' best candidates, PAPER.md:97 k-NN)
  * Anything else -> GENRED_E_UNSUPPORTED.                                                        */
 typedef struct {
     int32_t abi_version;     /* must equal GENRED_ABI_VERSION */
@@ -146,6 +147,8 @@ typedef struct {
     int32_t kernels;         /* kernels launched by the last call */
     int32_t path;            /* 0 = FP32/MUFU small-D path, 1 = tcgen05 tensor path */
     int64_t scratch_bytes;   /* device scratch currently held by the context */
+    int64_t fallback_rows;   /* tensor path: rows whose 3xTF32 screening failed the margin
+                                certificate and were rescanned exactly (synchronises; else -1) */
 } genred_plan;
 genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan);
 

@@ -30,6 +30,7 @@ struct genred_ctx {
     genred_plan plan{};
     int64_t launches = 0;
     std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
+    int *fallback_dev = nullptr;                               // k-NN rows rescanned exactly
     bool profiling = false;
     std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
     int nprof = 0;
@@ -77,7 +78,8 @@ genred_status validate(const genred_args *a, std::string &msg) {
         if (a->K < 1) { msg = "K must be >= 1"; return GENRED_E_SHAPE; }
         if (a->K > 32) { msg = "ArgKMin supports K <= 32"; return GENRED_E_UNSUPPORTED; }
         if (a->E != 1) { msg = "ArgKMin is scalar-formula only (E == 1)"; return GENRED_E_UNSUPPORTED; }
-        if (a->D > 16) { msg = "ArgKMin supports D <= 16 on the FP32 path"; return GENRED_E_UNSUPPORTED; }
+        if (a->D > 16 && a->K > 28) { msg = "the tensor-core ArgKMin path (D > 16) supports K <= 28"; return GENRED_E_UNSUPPORTED; }
+        if (a->D > 16384) { msg = "ArgKMin supports D <= 16384"; return GENRED_E_UNSUPPORTED; }
         if (a->N > (int64_t)INT32_MAX - kTileJ) { msg = "ArgKMin requires N < 2^31"; return GENRED_E_SHAPE; }
         if (a->out_dtype != GENRED_F32) { msg = "ArgKMin distances are fp32 (out_dtype F32)"; return GENRED_E_INVALID; }
     }
@@ -199,7 +201,8 @@ size_t al256(size_t x) { return (x + 255) & ~size_t(255); }
 constexpr int kMaxProfiled = 4096;
 
 // Event pair around the main kernel (benchmark roofline timing); no-op unless profiling.
-cudaEvent_t prof_event(genred_ctx *ctx, bool start, cudaStream_t st) {
+// With no_record the event is only returned (the launcher records it around its main kernel).
+cudaEvent_t prof_event(genred_ctx *ctx, bool start, cudaStream_t st, bool no_record = false) {
     if (!ctx->profiling || ctx->nprof >= kMaxProfiled) return nullptr;
     const size_t k = (size_t)ctx->nprof * 2 + (start ? 0 : 1);
     while (ctx->ev.size() <= k) {
@@ -207,7 +210,7 @@ cudaEvent_t prof_event(genred_ctx *ctx, bool start, cudaStream_t st) {
         if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); return nullptr; }
         ctx->ev.push_back(e);
     }
-    cudaEventRecord(ctx->ev[k], st);
+    if (!no_record) cudaEventRecord(ctx->ev[k], st);
     if (!start) ctx->nprof++;
     return ctx->ev[k];
 }
@@ -325,6 +328,29 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        return GENRED_OK;
+    }
+
+    // ArgKMin, large D: tcgen05 3xTF32 screening + exact re-rank (knn_tc.cu)
+    if (D > 16) {
+        const size_t need = knn_tc_scratch_bytes(M, N, D, a->K) + 1024;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, need);
+        if (s != GENRED_OK) return s;
+        KnnTcLaunch L;
+        L.x = a->x; L.y = a->y; L.M = M; L.N = N; L.D = D; L.K = a->K;
+        L.dist = (float *)a->out; L.idx = a->out_idx; L.j_offset = a->j_offset;
+        L.scratch = (void *)(((uintptr_t)ctx->scratch + 1023) & ~(uintptr_t)1023);
+        L.num_sms = ctx->num_sms;
+        L.ev_start = prof_event(ctx, true, nullptr, true);
+        L.ev_stop = prof_event(ctx, false, nullptr, true);
+        KnnTcInfo info{};
+        e = launch_knn_tc(L, st, &info);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "tensor-core k-NN");
+        ctx->launches += info.kernels;
+        ctx->fallback_dev = info.fallback_count;
+        ctx->plan.split_j = 1; ctx->plan.rows_per_cta = 128; ctx->plan.ctas = info.ctas;
+        ctx->plan.kernels = info.kernels; ctx->plan.path = 1; ctx->plan.tile_j = 256;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
         return GENRED_OK;
     }
@@ -544,6 +570,15 @@ genred_status genred_merge_topk(genred_ctx *ctx, int64_t M, int32_t K, int32_t G
 genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
     if (!ctx || !plan) return GENRED_E_INVALID;
     *plan = ctx->plan;
+    plan->fallback_rows = -1;
+    if (ctx->plan.path == 1 && ctx->fallback_dev) {
+        int n = -1;
+        if (cudaMemcpy(&n, ctx->fallback_dev, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
+            cudaGetLastError();
+            return GENRED_E_CUDA;
+        }
+        plan->fallback_rows = n;
+    }
     return GENRED_OK;
 }
 

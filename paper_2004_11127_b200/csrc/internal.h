@@ -71,6 +71,27 @@ cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas);
 int argk_occupancy(int D, int K, int R);
 int argk_rows_per_thread(int K);
 
+// Large-D ArgKMin on the tensor cores (knn_tc.cu): 3xTF32 tcgen05 screening + exact re-rank.
+struct KnnTcLaunch {
+    const float *x, *y;
+    int64_t M, N;
+    int D, K;
+    float *dist;
+    int64_t *idx;
+    int64_t j_offset;
+    void *scratch;                     // knn_tc_scratch_bytes(M, N, D, K) bytes, 1024-aligned
+    int num_sms;
+    cudaEvent_t ev_start, ev_stop;     // optional: recorded around the tcgen05 kernel
+};
+struct KnnTcInfo {
+    int kernels;
+    int ctas;
+    int *fallback_count;               // device int: rows rescanned exactly
+};
+int knn_tc_group();
+size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K);
+cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info);
+
 // Deterministic (fixed-order) merges of split-j partials.
 cudaError_t launch_sum_finalize(const double *part, int split, int64_t M, int C, int cols_sum,
                                 const float *g, int E, double scale_sum, double scale_grad,

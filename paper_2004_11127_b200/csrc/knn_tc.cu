@@ -1,0 +1,558 @@
+// knn_tc.cu -- ArgKMin over squared distances for large D on the 5th-generation tensor cores
+// (k-NN; north star (b)).
+//
+//   d_ij = |x_i|^2 + |y_j|^2 - 2 x_i . y_j ,   a_i = K smallest (d_ij, j), ties -> lowest j (R7)
+//
+// a10  prepass: x, y -> tf32 hi/lo split (hi = rna_tf32(v), lo = rna_tf32(v - hi)), rows padded
+//      to Dp (multiple of 32) with zeros; |x|^2, |y|^2 accumulated in fp64; max_j |y_j|.
+// a11  S_ij = x.y with 3xTF32: A_lo.B_hi + A_hi.B_lo + A_hi.B_hi accumulated in one fp32 TMEM
+//      accumulator (tcgen05.mma.cta_group::1.kind::tf32, 128 x 256 x 8), operands staged by TMA
+//      (cp.async.bulk.tensor.2d, 128B swizzle) into a 2-stage shared-memory ring; one thread
+//      issues MMAs, tcgen05.commit releases smem stages / publishes accumulators; the two
+//      256-column accumulators in TMEM (512 columns) let the epilogue of tile t overlap the
+//      MMAs of tile t+1.
+// a12  epilogue: 4 warps read the accumulator with tcgen05.ld (one TMEM lane = one query row per
+//      thread), form d~ = |x|^2 + |y|^2 - 2S and keep a register top-K' (K' = 16 or 32) per row;
+//      partial lists per (ref group, row) are merged, the K' candidates are re-ranked with exact
+//      fp64 direct differences, and the screening is certified by the margin test of reading
+//      R17 (d~_(K') - d~_(K) > 2 delta_i); rows that fail it are rescanned exactly (counted).
+//
+// Work units: (ref group g of kGroup ref tiles, query row tile r), g-major so that concurrently
+// running CTAs share the same ref tiles in L2; CTA c processes units c, c + grid, ...
+#include <cuda.h>
+#include <math.h>
+
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace genred {
+namespace tc {
+
+constexpr int BM = 128;                 // query rows per tile (TMEM lanes)
+constexpr int BN = 256;                 // refs per tile (TMEM columns per accumulator)
+constexpr int BK = 32;                  // fp32/tf32 elements per k-block (128 B rows, SW128)
+constexpr int STAGES = 2;
+constexpr int A_BYTES = BM * BK * 4;    // 16 KB
+constexpr int B_BYTES = BN * BK * 4;    // 32 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // hi + lo of both: 96 KB
+constexpr int NUM_THREADS = 192;        // warp 0 TMA, warp 1 MMA + TMEM alloc, warps 2-5 epilogue
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * BN * 4 + 256 + 1024;   // + y-norm tiles + barriers + align
+
+__device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int c0, int c1,
+                                            uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
+        ::"r"(smem_u32(smem)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;        // SBO
+    d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+    return d;
+}
+
+// kind::tf32 instruction descriptor: D f32, A/B tf32, K-major, M = 128, N = 256.
+constexpr uint32_t kIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                            ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b, uint32_t accum) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
+        ::"r"(d_tmem), "l"(a), "l"(b), "r"(kIdesc), "r"(accum) : "memory");
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
+                 ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+        "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+        "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+          "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+          "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+          "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+__device__ __forceinline__ void named_sync(int id, int n) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+struct Params {
+    int64_t M, N;
+    int Dp;
+    int nk;                  // Dp / BK
+    int n_rtiles, n_ttiles, n_groups, group;
+    const float *xn, *yn;    // squared norms (fp32)
+    float *pd;               // n_groups x M x KP screened distances
+    int32_t *pj;             // n_groups x M x KP indices
+};
+
+template <int KP>
+__device__ __forceinline__ void kp_insert(float (&d)[KP], int32_t (&j)[KP], float cd, int32_t cj,
+                                          float &kth) {
+#pragma unroll
+    for (int k = 0; k < KP; ++k) {
+        const bool sw = cd < d[k] || (cd == d[k] && (uint32_t)cj < (uint32_t)j[k]);
+        const float td = d[k];
+        const int32_t tj = j[k];
+        d[k] = sw ? cd : td;
+        j[k] = sw ? cj : tj;
+        cd = sw ? td : cd;
+        cj = sw ? tj : cj;
+    }
+    kth = d[KP - 1];
+}
+
+template <int KP>
+__global__ void __launch_bounds__(NUM_THREADS, 1)
+knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant__ CUtensorMap map_xlo,
+              const __grid_constant__ CUtensorMap map_yhi, const __grid_constant__ CUtensorMap map_ylo,
+              const Params p) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    // 1024-byte aligned operand ring (SW128 atoms), then y-norm tiles, then barriers
+    unsigned char *base = (unsigned char *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    float *ybuf = reinterpret_cast<float *>(base + STAGES * STAGE_BYTES);          // 2 x BN
+    uint64_t *bars = reinterpret_cast<uint64_t *>(base + STAGES * STAGE_BYTES + 2 * BN * 4);
+    uint64_t *full = bars;                   // [STAGES]
+    uint64_t *empty = bars + STAGES;         // [STAGES]
+    uint64_t *tfull = bars + 2 * STAGES;     // [2]
+    uint64_t *tempty = bars + 2 * STAGES + 2;// [2]
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
+        fence_barrier_init();
+    }
+    if (warp == 1) {                                     // TMEM: 2 accumulators x 256 columns
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;"
+                     ::"r"(smem_u32(tmem_slot)) : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    fence_before();
+    __syncthreads();
+    fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+    const int n_units = p.n_groups * p.n_rtiles;
+
+    if (warp == 0) {
+        // ------------------------------ TMA producer ------------------------------
+        if (lane == 0) {
+            int stage = 0; uint32_t phase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int g = u / p.n_rtiles, r = u % p.n_rtiles;
+                const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
+                for (int t = t0; t < t1; ++t) {
+                    for (int kb = 0; kb < p.nk; ++kb) {
+                        mbar_wait(&empty[stage], phase ^ 1);
+                        unsigned char *sb = base + stage * STAGE_BYTES;
+                        mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                        tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
+                        tma_load_2d(sb + A_BYTES, &map_xlo, kb * BK, r * BM, &full[stage]);
+                        tma_load_2d(sb + 2 * A_BYTES, &map_yhi, kb * BK, t * BN, &full[stage]);
+                        tma_load_2d(sb + 2 * A_BYTES + B_BYTES, &map_ylo, kb * BK, t * BN, &full[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ------------------------------ MMA issuer (one thread) ------------------------------
+        if (lane == 0) {
+            int stage = 0; uint32_t phase = 0;
+            int acc = 0; uint32_t aphase = 0;
+            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+                const int g = u / p.n_rtiles;
+                const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
+                for (int t = t0; t < t1; ++t) {
+                    mbar_wait(&tempty[acc], aphase ^ 1);
+                    fence_after();
+                    const uint32_t d_tmem = tmem_base + acc * BN;
+                    for (int kb = 0; kb < p.nk; ++kb) {
+                        mbar_wait(&full[stage], phase);
+                        fence_after();
+                        const uint32_t sb = smem_u32(base + stage * STAGE_BYTES);
+                        const uint64_t ahi = sw128_desc(sb), alo = sw128_desc(sb + A_BYTES);
+                        const uint64_t bhi = sw128_desc(sb + 2 * A_BYTES);
+                        const uint64_t blo = sw128_desc(sb + 2 * A_BYTES + B_BYTES);
+#pragma unroll
+                        for (int k = 0; k < BK / 8; ++k) {
+                            const uint64_t off = (uint64_t)(k * 32) >> 4;    // 8 tf32 = 32 B
+                            mma_tf32(d_tmem, alo + off, bhi + off, (kb | k) != 0);
+                            mma_tf32(d_tmem, ahi + off, blo + off, 1);
+                            mma_tf32(d_tmem, ahi + off, bhi + off, 1);
+                        }
+                        mma_commit(&empty[stage]);
+                        if (++stage == STAGES) { stage = 0; phase ^= 1; }
+                    }
+                    mma_commit(&tfull[acc]);
+                    if (++acc == 2) { acc = 0; aphase ^= 1; }
+                }
+            }
+        }
+    } else {
+        // ------------------------------ epilogue: 4 warps, one query row per thread ------------
+        const int q = warp & 3;                      // TMEM lane quarter this warp may access
+        const int row_in_tile = q * 32 + lane;
+        const int et = threadIdx.x - 64;             // 0..127
+        int acc = 0; uint32_t aphase = 0;
+        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
+            const int g = u / p.n_rtiles, r = u % p.n_rtiles;
+            const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
+            const int64_t i = (int64_t)r * BM + row_in_tile;
+            const float xn = i < p.M ? __ldg(p.xn + i) : 0.0f;
+            float bd[KP];
+            int32_t bj[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
+            float kth = INFINITY;
+            for (int t = t0; t < t1; ++t) {
+                float *yb = ybuf + acc * BN;
+                for (int c = et; c < BN; c += 128) {
+                    const int64_t j = (int64_t)t * BN + c;
+                    yb[c] = j < p.N ? __ldg(p.yn + j) : INFINITY;      // padded refs never win
+                }
+                named_sync(1, 128);
+                mbar_wait(&tfull[acc], aphase);
+                fence_after();
+                const uint32_t taddr = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+#pragma unroll 1
+                for (int c = 0; c < BN / 32; ++c) {
+                    uint32_t v[32];
+                    tmem_ld32(taddr + c * 32, v);
+#pragma unroll
+                    for (int k = 0; k < 32; ++k) {
+                        const float dt = fmaf(-2.0f, __uint_as_float(v[k]), xn + yb[c * 32 + k]);
+                        if (dt < kth) kp_insert<KP>(bd, bj, dt, t * BN + c * 32 + k, kth);
+                    }
+                }
+                fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&tempty[acc]);
+                if (++acc == 2) { acc = 0; aphase ^= 1; }
+            }
+            if (i < p.M) {
+                float *od = p.pd + ((int64_t)g * p.M + i) * KP;
+                int32_t *oj = p.pj + ((int64_t)g * p.M + i) * KP;
+#pragma unroll
+                for (int k = 0; k < KP; ++k) { od[k] = bd[k]; oj[k] = bj[k]; }
+            }
+        }
+    }
+    __syncthreads();
+    if (warp == 1) {
+        fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
+    }
+}
+
+// ---- a10: tf32 hi/lo split + fp64 squared norms --------------------------------------------------
+__device__ __forceinline__ float rna_tf32(float v) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(v));
+    return __uint_as_float(r);
+}
+
+__global__ void split_kernel(const float *__restrict__ src, int64_t rows, int D, int Dp,
+                             float *__restrict__ hi, float *__restrict__ lo, float *__restrict__ nrm,
+                             unsigned int *maxnorm_bits) {
+    // one warp per row
+    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t i = w; i < rows; i += nw) {
+        double s = 0.0;
+        for (int k = lane; k < Dp; k += 32) {
+            const float v = k < D ? src[i * D + k] : 0.0f;
+            const float h = rna_tf32(v);
+            const float l = rna_tf32(v - h);
+            hi[i * Dp + k] = h;
+            lo[i * Dp + k] = l;
+            s += (double)v * (double)v;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) {
+            nrm[i] = (float)s;
+            if (maxnorm_bits) atomicMax(maxnorm_bits, __float_as_uint((float)sqrt(s) * 1.0000002f));
+        }
+    }
+}
+
+// ---- a12: merge group lists -> K' best screened, exact fp64 re-rank, margin certificate --------
+template <int KP>
+__global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__restrict__ pj,
+                              int n_groups, const float *__restrict__ x, const float *__restrict__ y,
+                              const float *__restrict__ xn, const unsigned int *maxnorm_bits,
+                              int64_t M, int64_t N, int D, int K, float *dist, int64_t *idx,
+                              int64_t j_offset, int *fb_count, int32_t *fb_rows) {
+    __shared__ float s_d[4][KP];
+    __shared__ int32_t s_j[4][KP];
+    __shared__ double s_e[4][KP];
+    const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t i = blockIdx.x * 4 + wl;
+    if (i >= M) return;
+    if (lane == 0) {
+        float bd[KP];
+        int32_t bj[KP];
+        float kth = INFINITY;
+        for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
+        for (int g = 0; g < n_groups; ++g) {
+            const float *gd = pd + ((int64_t)g * M + i) * KP;
+            const int32_t *gj = pj + ((int64_t)g * M + i) * KP;
+            for (int k = 0; k < KP; ++k) {
+                const int32_t j = gj[k];
+                if (j < 0) break;
+                const float d = gd[k];
+                if (d < kth || (d == kth && (uint32_t)j < (uint32_t)bj[KP - 1])) {
+                    int pos = KP - 1;
+                    while (pos > 0 && (d < bd[pos - 1] || (d == bd[pos - 1] && j < bj[pos - 1]))) {
+                        bd[pos] = bd[pos - 1]; bj[pos] = bj[pos - 1]; --pos;
+                    }
+                    bd[pos] = d; bj[pos] = j;
+                    kth = bd[KP - 1];
+                } else {
+                    break;                                  // lists are sorted
+                }
+            }
+        }
+        // margin certificate (R17): every true top-K member is among the K' screened candidates
+        // when d~_(K') - d~_(K) > 2 delta, delta = gamma |x| max|y| + 2^-22 (|x|^2 + max|y|^2)
+        const float ymax = __uint_as_float(*maxnorm_bits);
+        const double xnorm = sqrt((double)xn[i]);
+        const double gamma = 3.0 * D * ldexp(1.0, -23);
+        const double delta = gamma * xnorm * ymax + ldexp(1.0, -22) * ((double)xn[i] + (double)ymax * ymax);
+        const bool all_in = bj[KP - 1] < 0;                 // fewer than K' refs exist at all
+        if (!all_in && !((double)bd[KP - 1] - (double)bd[K - 1] > 2.0 * delta)) {
+            const int slot = atomicAdd(fb_count, 1);
+            fb_rows[slot] = (int32_t)i;
+        }
+        for (int k = 0; k < KP; ++k) { s_d[wl][k] = bd[k]; s_j[wl][k] = bj[k]; }
+    }
+    __syncwarp();
+    // exact fp64 distances of the K' candidates (direct differences, never expanded)
+    for (int k = 0; k < KP; ++k) {
+        const int32_t j = s_j[wl][k];
+        double s = 0.0;
+        if (j >= 0) {
+            for (int c = lane; c < D; c += 32) {
+                const double dv = (double)x[i * D + c] - (double)y[(int64_t)j * D + c];
+                s = fma(dv, dv, s);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+        if (lane == 0) s_e[wl][k] = j >= 0 ? s : INFINITY;
+    }
+    __syncwarp();
+    if (lane == 0) {
+        // sort candidates by (exact d, j) and emit K
+        double ed[KP];
+        int32_t ej[KP];
+        for (int k = 0; k < KP; ++k) { ed[k] = s_e[wl][k]; ej[k] = s_j[wl][k]; }
+        for (int a = 1; a < KP; ++a) {
+            const double vd = ed[a]; const int32_t vj = ej[a];
+            int b = a;
+            while (b > 0 && (vd < ed[b - 1] || (vd == ed[b - 1] && (uint32_t)vj < (uint32_t)ej[b - 1]))) {
+                ed[b] = ed[b - 1]; ej[b] = ej[b - 1]; --b;
+            }
+            ed[b] = vd; ej[b] = vj;
+        }
+        for (int k = 0; k < K; ++k) {
+            dist[i * K + k] = ej[k] >= 0 ? (float)ed[k] : INFINITY;
+            idx[i * K + k] = ej[k] >= 0 ? (int64_t)ej[k] + j_offset : -1;
+        }
+    }
+}
+
+// ---- exact fp64 rescan of rows whose screening was not certified ---------------------------------
+constexpr int FB_THREADS = 64;
+constexpr int FB_LIST = 32;              // >= K: a thread can hold every member of the row's top-K
+
+__global__ void __launch_bounds__(FB_THREADS)
+fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t N, int D, int K,
+                const int *fb_count, const int32_t *fb_rows, float *dist, int64_t *idx,
+                int64_t j_offset) {
+    __shared__ double sd[FB_THREADS * FB_LIST];
+    __shared__ int32_t sj[FB_THREADS * FB_LIST];
+    const int n = *fb_count;
+    for (int f = blockIdx.x; f < n; f += gridDim.x) {
+        const int64_t i = fb_rows[f];
+        double *bd = sd + threadIdx.x * FB_LIST;
+        int32_t *bj = sj + threadIdx.x * FB_LIST;
+        for (int k = 0; k < FB_LIST; ++k) { bd[k] = INFINITY; bj[k] = -1; }
+        for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {       // ascending j per thread
+            double s = 0.0;
+            for (int c = 0; c < D; ++c) {
+                const double dv = (double)x[i * D + c] - (double)y[j * D + c];
+                s = fma(dv, dv, s);
+            }
+            if (s < bd[FB_LIST - 1]) {
+                int pos = FB_LIST - 1;
+                while (pos > 0 && s < bd[pos - 1]) { bd[pos] = bd[pos - 1]; bj[pos] = bj[pos - 1]; --pos; }
+                bd[pos] = s; bj[pos] = (int32_t)j;
+            }
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            for (int k = 0; k < K; ++k) {
+                int best = -1;
+                for (int c = 0; c < FB_THREADS * FB_LIST; ++c) {
+                    if (sj[c] < 0) continue;
+                    if (best < 0 || sd[c] < sd[best] || (sd[c] == sd[best] && sj[c] < sj[best])) best = c;
+                }
+                if (best >= 0) {
+                    dist[i * K + k] = (float)sd[best];
+                    idx[i * K + k] = (int64_t)sj[best] + j_offset;
+                    sj[best] = -1;
+                } else {
+                    dist[i * K + k] = INFINITY;
+                    idx[i * K + k] = -1;
+                }
+            }
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace tc
+
+// ---------------------------------------------------------------------------------------------
+// Host side
+// ---------------------------------------------------------------------------------------------
+#include <cudaTypedefs.h>
+
+static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+
+static cudaError_t get_encoder() {
+    if (g_encode) return cudaSuccess;
+    cudaDriverEntryPointQueryResult q;
+    void *fn = nullptr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q);
+    if (e != cudaSuccess || q != cudaDriverEntryPointSuccess || !fn) return cudaErrorNotSupported;
+    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+    return cudaSuccess;
+}
+
+static cudaError_t make_map(CUtensorMap *m, const float *ptr, int64_t rows, int Dp, int box_rows) {
+    cuuint64_t dims[2] = {(cuuint64_t)Dp, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)Dp * 4};
+    cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, estr,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+int knn_tc_group() { return 8; }
+
+size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K) {
+    const int Dp = (D + tc::BK - 1) / tc::BK * tc::BK;
+    const int KP = K <= 12 ? 16 : 32;
+    const int n_ttiles = (int)((N + tc::BN - 1) / tc::BN);
+    const int n_groups = (n_ttiles + knn_tc_group() - 1) / knn_tc_group();
+    auto al = [](size_t v) { return (v + 1023) & ~size_t(1023); };
+    return al((size_t)M * Dp * 4) * 2 + al((size_t)N * Dp * 4) * 2 + al((size_t)M * 4) +
+           al((size_t)N * 4) + al(64) + al((size_t)n_groups * M * KP * 4) * 2 + al((size_t)M * 4) + al(64);
+}
+
+template <int KP>
+static cudaError_t launch_main(const CUtensorMap *maps, const tc::Params &p, int grid, cudaStream_t st) {
+    auto kern = tc::knn_tc_kernel<KP>;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info) {
+    cudaError_t e = get_encoder();
+    if (e != cudaSuccess) return e;
+    const int64_t M = a.M, N = a.N;
+    const int D = a.D, K = a.K;
+    const int Dp = (D + tc::BK - 1) / tc::BK * tc::BK;
+    const int KP = K <= 12 ? 16 : 32;
+    const int n_rtiles = (int)((M + tc::BM - 1) / tc::BM);
+    const int n_ttiles = (int)((N + tc::BN - 1) / tc::BN);
+    const int group = knn_tc_group();
+    const int n_groups = (n_ttiles + group - 1) / group;
+    auto al = [](size_t v) { return (v + 1023) & ~size_t(1023); };
+    char *s = (char *)a.scratch;
+    float *xhi = (float *)s; s += al((size_t)M * Dp * 4);
+    float *xlo = (float *)s; s += al((size_t)M * Dp * 4);
+    float *yhi = (float *)s; s += al((size_t)N * Dp * 4);
+    float *ylo = (float *)s; s += al((size_t)N * Dp * 4);
+    float *xn = (float *)s; s += al((size_t)M * 4);
+    float *yn = (float *)s; s += al((size_t)N * 4);
+    unsigned int *ymax = (unsigned int *)s; s += al(64);
+    float *pd = (float *)s; s += al((size_t)n_groups * M * KP * 4);
+    int32_t *pj = (int32_t *)s; s += al((size_t)n_groups * M * KP * 4);
+    int32_t *fb_rows = (int32_t *)s; s += al((size_t)M * 4);
+    int *fb_count = (int *)s;
+
+    int kernels = 0;
+    if ((e = cudaMemsetAsync(ymax, 0, 64, st)) != cudaSuccess) return e;
+    tc::split_kernel<<<(unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16), 256, 0, st>>>(a.x, M, D, Dp, xhi, xlo, xn, nullptr);
+    tc::split_kernel<<<(unsigned)std::min<int64_t>((N + 7) / 8, 148 * 16), 256, 0, st>>>(a.y, N, D, Dp, yhi, ylo, yn, ymax);
+    kernels += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+
+    CUtensorMap maps[4];
+    if ((e = make_map(&maps[0], xhi, M, Dp, tc::BM)) != cudaSuccess) return e;
+    if ((e = make_map(&maps[1], xlo, M, Dp, tc::BM)) != cudaSuccess) return e;
+    if ((e = make_map(&maps[2], yhi, N, Dp, tc::BN)) != cudaSuccess) return e;
+    if ((e = make_map(&maps[3], ylo, N, Dp, tc::BN)) != cudaSuccess) return e;
+    tc::Params p;
+    p.M = M; p.N = N; p.Dp = Dp; p.nk = Dp / tc::BK; p.n_rtiles = n_rtiles; p.n_ttiles = n_ttiles;
+    p.n_groups = n_groups; p.group = group; p.xn = xn; p.yn = yn; p.pd = pd; p.pj = pj;
+    const int n_units = n_groups * n_rtiles;
+    const int grid = std::min(n_units, a.num_sms);
+    if (a.ev_start) cudaEventRecord(a.ev_start, st);
+    e = KP == 16 ? launch_main<16>(maps, p, grid, st) : launch_main<32>(maps, p, grid, st);
+    if (a.ev_stop) cudaEventRecord(a.ev_stop, st);
+    if (e != cudaSuccess) return e;
+    kernels += 1;
+    if ((e = cudaMemsetAsync(fb_count, 0, 4, st)) != cudaSuccess) return e;
+    const unsigned rgrid = (unsigned)((M + 3) / 4);
+    if (KP == 16)
+        tc::rerank_kernel<16><<<rgrid, 128, 0, st>>>(pd, pj, n_groups, a.x, a.y, xn, ymax, M, N, D, K,
+                                                     a.dist, a.idx, a.j_offset, fb_count, fb_rows);
+    else
+        tc::rerank_kernel<32><<<rgrid, 128, 0, st>>>(pd, pj, n_groups, a.x, a.y, xn, ymax, M, N, D, K,
+                                                     a.dist, a.idx, a.j_offset, fb_count, fb_rows);
+    tc::fallback_kernel<<<148, tc::FB_THREADS, 0, st>>>(a.x, a.y, N, D, K, fb_count, fb_rows, a.dist, a.idx, a.j_offset);
+    kernels += 2;
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+    if (info) {
+        info->kernels = kernels;
+        info->ctas = grid;
+        info->fallback_count = fb_count;
+    }
+    return cudaSuccess;
+}
+
+}  // namespace genred

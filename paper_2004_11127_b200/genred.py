@@ -56,7 +56,8 @@ class Args(ctypes.Structure):
 class Plan(ctypes.Structure):
     _fields_ = [("split_j", ctypes.c_int32), ("rows_per_cta", ctypes.c_int32),
                 ("ctas", ctypes.c_int32), ("tile_j", ctypes.c_int32), ("kernels", ctypes.c_int32),
-                ("path", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64)]
+                ("path", ctypes.c_int32), ("scratch_bytes", ctypes.c_int64),
+                ("fallback_rows", ctypes.c_int64)]
 
 
 _lib = None

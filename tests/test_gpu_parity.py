@@ -371,3 +371,50 @@ def test_config5_full_size_sampled(G):
     rows = _rows(c.M, 64, 9)
     o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
     assert_sum_parity(host(a)[rows], o, den, what="C5 sum")
+
+
+# ------------------------------------------------------------------------------------------------
+# ArgKMin, large D: tcgen05 3xTF32 screening + exact fp64 re-rank
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("M,N,D,K", [(300, 1000, 32, 10), (200, 700, 50, 5), (129, 257, 17, 1),
+                                     (500, 3000, 784, 10), (130, 2000, 100, 20), (64, 12, 40, 10)])
+def test_argkmin_tensor_path(G, M, N, D, K):
+    rng = np.random.default_rng(M + N + D)
+    if D == 784:
+        x = synth.mnist784(M, 41); y = synth.mnist784(N, 42)
+    else:
+        x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+    plan = G.last_plan()
+    assert plan["path"] == 1
+    od, oj = oracle.argkmin(x, y, K + 1)
+    argk_check(host(d), host(j), od, oj, K, what=f"tc argk {M}x{N} D={D} K={K}")
+
+
+def test_argkmin_tensor_path_fallback_certificate(G):
+    """Refs equidistant from the query defeat any screening margin: the R17 certificate must
+    reject those rows and the exact rescan must return the lowest indices (ties -> lowest j)."""
+    D = 32
+    x = np.zeros((3, D), np.float32); x[1] += 0.5
+    y = np.zeros((600, D), np.float32)
+    for jj in range(600):
+        y[jj, jj % D] = 1.0 if (jj // D) % 2 == 0 else -1.0       # |x0 - y_j| = 1 for all j
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=10)
+    plan = G.last_plan()
+    assert plan["fallback_rows"] >= 1
+    od, oj = oracle.argkmin(x, y, 11)
+    assert host(j)[0].tolist() == list(range(10))
+    argk_check(host(d), host(j), od, oj, 10, what="fallback")
+
+
+def test_config4_full_size_sampled(G):
+    c = synth.config(4); sd = synth.seeds(4)
+    x = synth.mnist784(c.M, sd["x"]); y = synth.mnist784(c.N, sd["y"])
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=c.K)
+    plan = G.last_plan()
+    assert plan["path"] == 1 and plan["fallback_rows"] == 0
+    rows = _rows(c.M, 300, 10)
+    od, oj = oracle.argkmin(x, y, c.K + 1, rows=rows)
+    n_idx, n_dist = argk_check(host(d)[rows], host(j)[rows], od, oj, c.K, what="C4")
+    assert n_idx >= 0.95 * len(rows) * c.K
