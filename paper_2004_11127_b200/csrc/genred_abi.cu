@@ -295,7 +295,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     }
 
     if (red == GENRED_LSE) {
-        Plan pl = make_plan(ctx, a, 1, 4, D, 0, 0);
+        Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0);
         const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
         const int RS = pack_record_stride(pk, D, 1);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);

@@ -57,6 +57,7 @@ struct LseLaunch {
 };
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
 int lse_occupancy(int D, int R);
+int lse_rows_per_thread_max(int D);
 
 struct ArgkLaunch {
     int D, K, R;

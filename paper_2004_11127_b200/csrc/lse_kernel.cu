@@ -47,8 +47,55 @@ struct LseParams {
     double *state;
 };
 
+struct LseRescale {
+    float m;
+    double s64;
+    float c1;
+};
+
+// Out of line so that its registers do not burden the hot loop.
+template <int D, bool HZ, int RS>
+__device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&xr)[D], float negc,
+                                               float m_old, double s64, float2 s32) {
+    float vmax = -INFINITY;
+    for (int q = 0; q < kSub; ++q) {
+        const float *rec = base + q * RS;
+        for (int h = 0; h < 2; ++h) {
+            float q1 = 0.f;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const float dd = xr[d] + rec[2 * d + h];
+                q1 = fmaf(dd, dd, q1);
+            }
+            float hv = 0.0f;
+            if constexpr (!HZ) hv = rec[2 * D + h];
+            vmax = fmaxf(vmax, fmaf(q1, negc, hv));
+        }
+    }
+    LseRescale o;
+    o.m = fmaxf(vmax, m_old);
+    o.s64 = (s64 + (double)s32.x + (double)s32.y) * exp2((double)m_old - (double)o.m);
+    float c1 = 0.f;
+    for (int q = 0; q < kSub; ++q) {
+        const float *rec = base + q * RS;
+        for (int h = 0; h < 2; ++h) {
+            float q1 = 0.f;
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const float dd = xr[d] + rec[2 * d + h];
+                q1 = fmaf(dd, dd, q1);
+            }
+            float hmv = -o.m;
+            if constexpr (!HZ) hmv = (rec[2 * D + h] + (-o.m)) + rec[2 * D + 2 + h];
+            c1 += ex2(fmaf(q1, negc, hmv));
+        }
+    }
+    o.c1 = c1;
+    return o;
+}
+
 template <int D, int R, bool HZ>
-__global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
+__global__ void __maxnreg__(112) lse_kernel(const LseParams p) {   // 2 CTAs x 288 threads x 112 regs
     using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -120,7 +167,7 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                 cs[r] = make_float2(0.f, 0.f);
                 hm0[r] = dup2(-m[r]);
             }
-#pragma unroll
+#pragma unroll 4
             for (int q = 0; q < kSub; ++q) {
                 float f[RS];
 #pragma unroll
@@ -154,44 +201,12 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 if (tm[r] > kTau) {
-                    // ---- rare path: new reference = exact max of v over this sub-chunk ----
-                    float vmax = -INFINITY;
-                    for (int q = 0; q < kSub; ++q) {
-                        const float *rec = base + q * RS;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float q1 = 0.f;
-#pragma unroll
-                            for (int d = 0; d < D; ++d) {
-                                const float dd = xr[r][d] + rec[2 * d + h];
-                                q1 = fmaf(dd, dd, q1);
-                            }
-                            float hv = 0.0f;
-                            if constexpr (!HZ) hv = rec[2 * D + h];
-                            vmax = fmaxf(vmax, fmaf(q1, negc, hv));
-                        }
-                    }
-                    const float mn = fmaxf(vmax, m[r]);
-                    s64[r] = (s64[r] + (double)s32[r].x + (double)s32[r].y) *
-                             exp2((double)m[r] - (double)mn);
-                    m[r] = mn;
-                    float c1 = 0.f;
-                    for (int q = 0; q < kSub; ++q) {
-                        const float *rec = base + q * RS;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float q1 = 0.f;
-#pragma unroll
-                            for (int d = 0; d < D; ++d) {
-                                const float dd = xr[r][d] + rec[2 * d + h];
-                                q1 = fmaf(dd, dd, q1);
-                            }
-                            float hmv = -mn;
-                            if constexpr (!HZ) hmv = (rec[2 * D + h] + (-mn)) + rec[2 * D + 2 + h];
-                            c1 += ex2(fmaf(q1, negc, hmv));
-                        }
-                    }
-                    s32[r] = make_float2(c1, 0.f);
+                    // rare path (a few times per row): new reference m = exact max of v over the
+                    // sub-chunk, fp64 rescale of the accumulated sum, sub-chunk recomputed
+                    const LseRescale rs = lse_rescale<D, HZ, RS>(base, xr[r], negc, m[r], s64[r], s32[r]);
+                    m[r] = rs.m;
+                    s64[r] = rs.s64;
+                    s32[r] = make_float2(rs.c1, 0.f);
                 } else {
                     s32[r] = add2(s32[r], cs[r]);
                 }
@@ -262,10 +277,17 @@ static int occ_lse() {
     return n > 0 ? n : 1;
 }
 
+// Rows per thread that stay spill-free within 112 registers.
+template <int D>
+constexpr int lse_rmax() { return D <= 4 ? 4 : 2; }
+
+int lse_rows_per_thread_max(int D) { return D <= 4 ? 4 : 2; }
+
 template <int D>
 static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    constexpr int RM = lse_rmax<D>();
     if (a.R == 1) return a.h_zero ? run_lse<D, 1, true>(a, st, ctas) : run_lse<D, 1, false>(a, st, ctas);
-    return a.h_zero ? run_lse<D, 4, true>(a, st, ctas) : run_lse<D, 4, false>(a, st, ctas);
+    return a.h_zero ? run_lse<D, RM, true>(a, st, ctas) : run_lse<D, RM, false>(a, st, ctas);
 }
 
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
@@ -283,7 +305,7 @@ cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
 }
 
 int lse_occupancy(int D, int R) {
-#define GENRED_OCC(DD) if (D == DD) return R == 1 ? occ_lse<DD, 1>() : occ_lse<DD, 4>();
+#define GENRED_OCC(DD) if (D == DD) return R == 1 ? occ_lse<DD, 1>() : occ_lse<DD, lse_rmax<DD>()>();
     GENRED_OCC(1) GENRED_OCC(2) GENRED_OCC(3) GENRED_OCC(4)
     GENRED_OCC(5) GENRED_OCC(6) GENRED_OCC(7) GENRED_OCC(8)
 #undef GENRED_OCC
