@@ -21,7 +21,7 @@ struct ArgkCfg {
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
     static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
-    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
 };
 
 struct ArgkParams {
@@ -59,43 +59,19 @@ __device__ __forceinline__ void topk_insert(float (&dist)[KMAX], int32_t (&idx)[
 }
 
 template <int D, int KMAX, int R>
-__global__ void __launch_bounds__(kThreads, 1) argk_kernel(const ArgkParams p) {
+__global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
     using Cfg = ArgkCfg<D>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *tiles = reinterpret_cast<float *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
-    uint64_t *empty = full + kStages;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t itile = blockIdx.x / p.split;
     const int sp = (int)(blockIdx.x % p.split);
     const int64_t t0 = (int64_t)sp * p.tiles_per_split;
     const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
     const int nt = (int)(t1 - t0);
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        if (lane == 0) {
-            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
-            for (int k = 0; k < nt; ++k) {
-                const int s = k % kStages;
-                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
-                         Cfg::STAGE_BYTES, &full[s]);
-            }
-        }
-        return;
-    }
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
 
     const int ct = threadIdx.x;
     const int K = p.K;
@@ -116,9 +92,7 @@ __global__ void __launch_bounds__(kThreads, 1) argk_kernel(const ArgkParams p) {
     }
 
     for (int k = 0; k < nt; ++k) {
-        const int s = k % kStages;
-        mbar_wait(&full[s], (k / kStages) & 1);
-        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+        const float *tile = ring.acquire(k);
         const int32_t jbase = (int32_t)((t0 + k) * kTileJ);
 #pragma unroll 2
         for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
@@ -144,8 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1) argk_kernel(const ArgkParams p) {
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        ring.release(k);
     }
 
 #pragma unroll

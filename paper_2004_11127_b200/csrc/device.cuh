@@ -69,3 +69,62 @@ __device__ __forceinline__ float4 lds128(const float *p) {
 }
 
 }  // namespace genred
+
+namespace genred {
+
+// ---- j-tile ring shared by the FP32/MUFU pair-loop kernels ---------------------------------
+// STAGES shared-memory buffers of `bytes` each, filled by cp.async.bulk (TMA engine) and
+// completing on `full` mbarriers.  No dedicated producer warp: thread 0 issues the prologue
+// loads and, after every warp has released a stage (`empty`, one arrival per warp), refills it
+// with the tile STAGES ahead.  All warps of the CTA are math warps, so a 256-thread CTA keeps
+// 2 (or 3) CTAs per SM within the per-SM-partition register budget (16K registers / SMSP).
+template <int STAGES>
+struct JRing {
+    float *tiles;
+    uint64_t *full, *empty;
+    const float *src;          // first tile of this CTA's j-range
+    int nt;                    // tiles in the range
+    int tile_floats;
+    uint32_t bytes;
+
+    __device__ __forceinline__ void init(unsigned char *smem, int tile_floats_, const float *src_,
+                                         int nt_, int nwarps) {
+        tile_floats = tile_floats_;
+        bytes = (uint32_t)tile_floats_ * 4u;
+        tiles = reinterpret_cast<float *>(smem);
+        full = reinterpret_cast<uint64_t *>(smem + (size_t)STAGES * bytes);
+        empty = full + STAGES;
+        src = src_;
+        nt = nt_;
+        if (threadIdx.x == 0) {
+            for (int s = 0; s < STAGES; ++s) {
+                mbar_init(&full[s], 1);
+                mbar_init(&empty[s], nwarps);
+            }
+            fence_barrier_init();
+            for (int k = 0; k < STAGES && k < nt; ++k) {
+                mbar_arrive_expect_tx(&full[k], bytes);
+                bulk_g2s(tiles + k * tile_floats, src + (int64_t)k * tile_floats, bytes, &full[k]);
+            }
+        }
+        __syncthreads();
+    }
+    __device__ __forceinline__ const float *acquire(int k) {
+        const int s = k % STAGES;
+        mbar_wait(&full[s], (k / STAGES) & 1);
+        return tiles + s * tile_floats;
+    }
+    __device__ __forceinline__ void release(int k) {
+        const int s = k % STAGES;
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
+        if (threadIdx.x == 0 && k + STAGES < nt) {
+            mbar_wait(&empty[s], (k / STAGES) & 1);          // every warp is done with tile k
+            mbar_arrive_expect_tx(&full[s], bytes);
+            bulk_g2s(tiles + s * tile_floats, src + (int64_t)(k + STAGES) * tile_floats, bytes, &full[s]);
+        }
+    }
+    static constexpr int smem_bytes(int tile_floats_) { return STAGES * tile_floats_ * 4 + 2 * STAGES * 8; }
+};
+
+}  // namespace genred

@@ -9,7 +9,7 @@ namespace genred {
 constexpr int kTileJ = 512;                 // j-records per shared-memory stage
 constexpr int kStages = 4;                  // depth of the bulk-copy ring
 constexpr int kConsumerWarps = 8;           // math warps per CTA
-constexpr int kThreads = (kConsumerWarps + 1) * 32;   // + 1 producer (bulk-copy) warp
+constexpr int kThreads = kConsumerWarps * 32;         // all math warps; thread 0 also refills the j-ring
 constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference of an empty LSE state
 
 // Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.

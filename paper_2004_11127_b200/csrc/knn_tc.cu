@@ -385,45 +385,55 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
 }
 
 // ---- exact fp64 rescan of rows whose screening was not certified ---------------------------------
-constexpr int FB_THREADS = 64;
-constexpr int FB_LIST = 32;              // >= K: a thread can hold every member of the row's top-K
+constexpr int FB_THREADS = 256;
+constexpr int FB_WARPS = FB_THREADS / 32;
+constexpr int FB_LIST = 32;              // >= K: one warp's list can hold the whole top-K
 
+// One CTA per flagged row: warp w scans refs j = w, w + 8, ... with its lanes striding over D
+// (coalesced), fp64 direct differences; lane 0 keeps the warp's sorted (d, j) list; thread 0
+// merges the 8 lists.  Rare (rows failing the R17 certificate), so simplicity wins.
 __global__ void __launch_bounds__(FB_THREADS)
 fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t N, int D, int K,
                 const int *fb_count, const int32_t *fb_rows, float *dist, int64_t *idx,
                 int64_t j_offset) {
-    __shared__ double sd[FB_THREADS * FB_LIST];
-    __shared__ int32_t sj[FB_THREADS * FB_LIST];
+    __shared__ double sd[FB_WARPS][FB_LIST];
+    __shared__ int32_t sj[FB_WARPS][FB_LIST];
     const int n = *fb_count;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int f = blockIdx.x; f < n; f += gridDim.x) {
         const int64_t i = fb_rows[f];
-        double *bd = sd + threadIdx.x * FB_LIST;
-        int32_t *bj = sj + threadIdx.x * FB_LIST;
-        for (int k = 0; k < FB_LIST; ++k) { bd[k] = INFINITY; bj[k] = -1; }
-        for (int64_t j = threadIdx.x; j < N; j += blockDim.x) {       // ascending j per thread
+        if (lane == 0)
+            for (int k = 0; k < FB_LIST; ++k) { sd[w][k] = INFINITY; sj[w][k] = -1; }
+        __syncwarp();
+        for (int64_t j = w; j < N; j += FB_WARPS) {
             double s = 0.0;
-            for (int c = 0; c < D; ++c) {
+            for (int c = lane; c < D; c += 32) {
                 const double dv = (double)x[i * D + c] - (double)y[j * D + c];
                 s = fma(dv, dv, s);
             }
-            if (s < bd[FB_LIST - 1]) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+            if (lane == 0 && s < sd[w][FB_LIST - 1]) {          // j ascending within the warp
                 int pos = FB_LIST - 1;
-                while (pos > 0 && s < bd[pos - 1]) { bd[pos] = bd[pos - 1]; bj[pos] = bj[pos - 1]; --pos; }
-                bd[pos] = s; bj[pos] = (int32_t)j;
+                while (pos > 0 && s < sd[w][pos - 1]) { sd[w][pos] = sd[w][pos - 1]; sj[w][pos] = sj[w][pos - 1]; --pos; }
+                sd[w][pos] = s; sj[w][pos] = (int32_t)j;
             }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
+            int head[FB_WARPS] = {0};
             for (int k = 0; k < K; ++k) {
                 int best = -1;
-                for (int c = 0; c < FB_THREADS * FB_LIST; ++c) {
-                    if (sj[c] < 0) continue;
-                    if (best < 0 || sd[c] < sd[best] || (sd[c] == sd[best] && sj[c] < sj[best])) best = c;
+                for (int q = 0; q < FB_WARPS; ++q) {
+                    if (head[q] >= FB_LIST || sj[q][head[q]] < 0) continue;
+                    if (best < 0 || sd[q][head[q]] < sd[best][head[best]] ||
+                        (sd[q][head[q]] == sd[best][head[best]] && sj[q][head[q]] < sj[best][head[best]]))
+                        best = q;
                 }
                 if (best >= 0) {
-                    dist[i * K + k] = (float)sd[best];
-                    idx[i * K + k] = (int64_t)sj[best] + j_offset;
-                    sj[best] = -1;
+                    dist[i * K + k] = (float)sd[best][head[best]];
+                    idx[i * K + k] = (int64_t)sj[best][head[best]] + j_offset;
+                    head[best]++;
                 } else {
                     dist[i * K + k] = INFINITY;
                     idx[i * K + k] = -1;

@@ -33,7 +33,7 @@ struct LseCfg {
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
     static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
-    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
 };
 
 struct LseParams {
@@ -95,43 +95,19 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
 }
 
 template <int D, int R, bool HZ>
-__global__ void __maxnreg__(112) lse_kernel(const LseParams p) {   // 2 CTAs x 288 threads x 112 regs
+__global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
     using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *tiles = reinterpret_cast<float *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
-    uint64_t *empty = full + kStages;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t itile = blockIdx.x / p.split;
     const int sp = (int)(blockIdx.x % p.split);
     const int64_t t0 = (int64_t)sp * p.tiles_per_split;
     const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
     const int nt = (int)(t1 - t0);
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {
-        if (lane == 0) {
-            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
-            for (int k = 0; k < nt; ++k) {
-                const int s = k % kStages;
-                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
-                         Cfg::STAGE_BYTES, &full[s]);
-            }
-        }
-        return;
-    }
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
 
     const int ct = threadIdx.x;
     const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
@@ -153,19 +129,15 @@ __global__ void __maxnreg__(112) lse_kernel(const LseParams p) {   // 2 CTAs x 2
     }
 
     for (int k = 0; k < nt; ++k) {
-        const int s = k % kStages;
-        mbar_wait(&full[s], (k / kStages) & 1);
-        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+        const float *tile = ring.acquire(k);
         for (int sc = 0; sc < Cfg::PAIRS / kSub; ++sc) {
             const float *base = tile + sc * kSub * RS;
             float tm[R];
             float2 cs[R];
-            float2 hm0[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 tm[r] = -INFINITY;
                 cs[r] = make_float2(0.f, 0.f);
-                hm0[r] = dup2(-m[r]);
             }
 #pragma unroll 4
             for (int q = 0; q < kSub; ++q) {
@@ -192,7 +164,7 @@ __global__ void __maxnreg__(112) lse_kernel(const LseParams p) {   // 2 CTAs x 2
                         dd = add2(dup2(xr[r][d]), ny[d]);
                         q2 = fma2(dd, dd, q2);
                     }
-                    const float2 hm = HZ ? hm0[r] : add2(add2(hhi, hm0[r]), hlo);  // (h'-m) exact-ish
+                    const float2 hm = HZ ? dup2(-m[r]) : add2(add2(hhi, dup2(-m[r])), hlo);  // (h'-m)
                     const float2 t = fma2(q2, negc2, hm);          // v - m, log2 units
                     tm[r] = max3(tm[r], t.x, t.y);
                     cs[r] = add2(cs[r], make_float2(ex2(t.x), ex2(t.y)));
@@ -219,8 +191,7 @@ __global__ void __maxnreg__(112) lse_kernel(const LseParams p) {   // 2 CTAs x 2
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        ring.release(k);
     }
 
 #pragma unroll
@@ -279,9 +250,9 @@ static int occ_lse() {
 
 // Rows per thread that stay spill-free within 112 registers.
 template <int D>
-constexpr int lse_rmax() { return D <= 4 ? 4 : 2; }
+constexpr int lse_rmax() { return D <= 3 ? 4 : 2; }
 
-int lse_rows_per_thread_max(int D) { return D <= 4 ? 4 : 2; }
+int lse_rows_per_thread_max(int D) { return D <= 3 ? 4 : 2; }
 
 template <int D>
 static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {

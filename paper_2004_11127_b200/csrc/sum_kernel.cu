@@ -34,7 +34,7 @@ struct SumCfg {
     static constexpr int C = NS + NG;
     static constexpr bool GRAD = NG > 0;
     static constexpr bool EXP = MODE != 3;
-    static constexpr int SMEM = kStages * STAGE_BYTES + 2 * kStages * 8;
+    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
 };
 
 struct SumParams {
@@ -51,43 +51,19 @@ struct SumParams {
 };
 
 template <int MODE, int D, int E, int R>
-__global__ void __launch_bounds__(kThreads, 2) sum_kernel(const SumParams p) {
+__global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *tiles = reinterpret_cast<float *>(smem_raw);
-    uint64_t *full = reinterpret_cast<uint64_t *>(smem_raw + kStages * Cfg::STAGE_BYTES);
-    uint64_t *empty = full + kStages;
 
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t itile = blockIdx.x / p.split;
     const int sp = (int)(blockIdx.x % p.split);
     const int64_t t0 = (int64_t)sp * p.tiles_per_split;
     const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
     const int nt = (int)(t1 - t0);
 
-    if (threadIdx.x == 0) {
-        for (int s = 0; s < kStages; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
-        }
-        fence_barrier_init();
-    }
-    __syncthreads();
-
-    if (warp == kConsumerWarps) {                     // ---- producer: bulk-copy j-tiles ----
-        if (lane == 0) {
-            const float *src = p.J + t0 * Cfg::TILE_FLOATS;
-            for (int k = 0; k < nt; ++k) {
-                const int s = k % kStages;
-                if (k >= kStages) mbar_wait(&empty[s], ((k / kStages) - 1) & 1);
-                mbar_arrive_expect_tx(&full[s], Cfg::STAGE_BYTES);
-                bulk_g2s(tiles + s * Cfg::TILE_FLOATS, src + (int64_t)k * Cfg::TILE_FLOATS,
-                         Cfg::STAGE_BYTES, &full[s]);
-            }
-        }
-        return;
-    }
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
 
     // ---- math warps: R rows per thread, registers only --------------------------------------
     const int ct = threadIdx.x;
@@ -118,9 +94,7 @@ __global__ void __launch_bounds__(kThreads, 2) sum_kernel(const SumParams p) {
     }
 
     for (int k = 0; k < nt; ++k) {
-        const int s = k % kStages;
-        mbar_wait(&full[s], (k / kStages) & 1);
-        const float *tile = tiles + s * Cfg::TILE_FLOATS;
+        const float *tile = ring.acquire(k);
 #pragma unroll 2
         for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
             float f[RS];
@@ -171,8 +145,7 @@ __global__ void __launch_bounds__(kThreads, 2) sum_kernel(const SumParams p) {
                 }
             }
         }
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&empty[s]);
+        ring.release(k);
         // promote the tile's fp32 partials to fp64 (every 512 j)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
@@ -256,10 +229,12 @@ static int occ_sum() {
     return n > 0 ? n : 1;
 }
 
-// Largest rows-per-thread that stays spill-free under __launch_bounds__(288, 2) (96 registers).
+// Largest rows-per-thread that stays spill-free (80 registers for Sum at 3 CTAs/SM, 128 for the
+// gradient modes at 2 CTAs/SM).
 template <int MODE, int D, int E>
 constexpr int sum_rmax() {
-    return (MODE == 0 || MODE == 3) ? ((D + E <= 6) ? 4 : 2) : ((D + E <= 4) ? 2 : 1);
+    return (MODE == 0 || MODE == 3) ? ((D + E <= 4 || (E == 1 && D <= 4)) ? 4 : 2)
+                                    : ((D + E <= 4) ? 4 : (D + E <= 6 ? 2 : 1));
 }
 template <int MODE, int D, int E>
 static cudaError_t run_sum_r(const SumLaunch &a, cudaStream_t st, int *ctas) {

@@ -413,7 +413,7 @@ def test_config4_full_size_sampled(G):
     x = synth.mnist784(c.M, sd["x"]); y = synth.mnist784(c.N, sd["y"])
     d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=c.K)
     plan = G.last_plan()
-    assert plan["path"] == 1 and plan["fallback_rows"] == 0
+    assert plan["path"] == 1 and 0 <= plan["fallback_rows"] <= c.M // 100   # R17 certificate: rare rescans
     rows = _rows(c.M, 300, 10)
     od, oj = oracle.argkmin(x, y, c.K + 1, rows=rows)
     n_idx, n_dist = argk_check(host(d)[rows], host(j)[rows], od, oj, c.K, what="C4")

@@ -23,10 +23,15 @@ def main():
     ap.add_argument("--M", type=int, default=1_000_000)
     ap.add_argument("--N", type=int, default=1_000_000)
     ap.add_argument("--K", type=int, default=10)
+    ap.add_argument("--D", type=int, default=3)
     ap.add_argument("--reps", type=int, default=2)
     a = ap.parse_args()
-    x = torch.from_numpy(synth.uniform3(a.M, 1)).cuda()
-    y = torch.from_numpy(synth.uniform3(a.N, 2)).cuda()
+    if a.D == 784:
+        x = torch.from_numpy(synth.mnist784(a.M, 1)).cuda()
+        y = torch.from_numpy(synth.mnist784(a.N, 2)).cuda()
+    else:
+        x = torch.from_numpy(synth.uniform3(a.M, 1, a.D)).cuda()
+        y = torch.from_numpy(synth.uniform3(a.N, 2, a.D)).cuda()
     b = torch.from_numpy(synth.signal(a.N, 3)).cuda()
     h = torch.from_numpy(np.random.default_rng(4).standard_normal(a.N).astype(np.float32)).cuda()
     for _ in range(a.reps):
