@@ -4,10 +4,10 @@
 //   d_ij = |x_i|^2 + |y_j|^2 - 2 x_i . y_j ,   a_i = K smallest (d_ij, j), ties -> lowest j (R7)
 //
 // a10  prepass: x, y -> tf32 hi/lo split (hi = rna_tf32(v), lo = rna_tf32(v - hi)), rows padded
-//      to Dp (multiple of 32) with zeros; |x|^2, |y|^2 accumulated in fp64; max_j |y_j|.
+//      to Dp (multiple of 16) with zeros; |x|^2, |y|^2 accumulated in fp64; max_j |y_j|.
 // a11  S_ij = x.y with 3xTF32: A_lo.B_hi + A_hi.B_lo + A_hi.B_hi accumulated in one fp32 TMEM
 //      accumulator (tcgen05.mma.cta_group::1.kind::tf32, 128 x 256 x 8), operands staged by TMA
-//      (cp.async.bulk.tensor.2d, 128B swizzle) into a 2-stage shared-memory ring; one thread
+//      (cp.async.bulk.tensor.2d, 64B swizzle) into a 4-stage shared-memory ring; one thread
 //      issues MMAs, tcgen05.commit releases smem stages / publishes accumulators; the two
 //      256-column accumulators in TMEM (512 columns) let the epilogue of tile t overlap the
 //      MMAs of tile t+1.
@@ -22,6 +22,8 @@
 #include <cuda.h>
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <algorithm>
 
 #include "device.cuh"
@@ -32,13 +34,15 @@ namespace tc {
 
 constexpr int BM = 128;                 // query rows per tile (TMEM lanes)
 constexpr int BN = 256;                 // refs per tile (TMEM columns per accumulator)
-constexpr int BK = 32;                  // fp32/tf32 elements per k-block (128 B rows, SW128)
-constexpr int STAGES = 2;
-constexpr int A_BYTES = BM * BK * 4;    // 16 KB
-constexpr int B_BYTES = BN * BK * 4;    // 32 KB
-constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // hi + lo of both: 96 KB
+constexpr int BK = 16;                  // fp32/tf32 elements per k-block (64 B rows, 64B swizzle)
+constexpr int STAGES = 4;
+constexpr int A_BYTES = BM * BK * 4;    // 8 KB
+constexpr int B_BYTES = BN * BK * 4;    // 16 KB
+constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // hi + lo of both: 48 KB
 constexpr int NUM_THREADS = 192;        // warp 0 TMA, warp 1 MMA + TMEM alloc, warps 2-5 epilogue
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * BN * 4 + 256 + 1024;   // + y-norm tiles + barriers + align
+constexpr int CB = 16;                  // per-thread candidate buffer (epilogue)
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 2 * BN * 4 + 256 + 2 * CB * 128 * 4 + 1024;
+static_assert(SMEM_BYTES <= 232448, "exceeds the 227 KB per-CTA shared memory");
 
 __device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, int c0, int c1,
                                             uint64_t *bar) {
@@ -50,14 +54,14 @@ __device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
 __device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
 
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row groups 1024 B apart (SBO), version 1.
-__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+// K-major operand, 64-byte swizzle: rows of BK*4 = 64 B, 8-row groups 512 B apart (SBO), version 1.
+__device__ __forceinline__ uint64_t sw_desc(uint32_t saddr) {
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)1 << 16;                  // LBO (unused for swizzled K-major)
-    d |= (uint64_t)(1024 >> 4) << 32;        // SBO
+    d |= (uint64_t)((8 * BK * 4) >> 4) << 32;// SBO: one 8-row swizzle atom
     d |= (uint64_t)1 << 46;                  // descriptor version (sm_100)
-    d |= (uint64_t)2 << 61;                  // SWIZZLE_128B
+    d |= (uint64_t)4 << 61;                  // SWIZZLE_64B
     return d;
 }
 
@@ -101,6 +105,8 @@ struct Params {
     int nk;                  // Dp / BK
     int n_rtiles, n_ttiles, n_groups, group;
     const float *xn, *yn;    // squared norms (fp32)
+    int dbg;                 // experiments only: bit0 = 1 MMA per k-step, bit1 = skip lo loads
+    unsigned int *row_thr;   // M: best known K'-th screened value per row (float bits, >= 0)
     float *pd;               // n_groups x M x KP screened distances
     int32_t *pj;             // n_groups x M x KP indices
 };
@@ -136,6 +142,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
     uint64_t *tfull = bars + 2 * STAGES;     // [2]
     uint64_t *tempty = bars + 2 * STAGES + 2;// [2]
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(bars + 2 * STAGES + 4);
+    float *cand_d = reinterpret_cast<float *>(base + STAGES * STAGE_BYTES + 2 * BN * 4 + 256);
+    int32_t *cand_j = reinterpret_cast<int32_t *>(cand_d + CB * 128);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
@@ -165,11 +173,17 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
                     for (int kb = 0; kb < p.nk; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         unsigned char *sb = base + stage * STAGE_BYTES;
+                        if (p.dbg & 2) {
+                            mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
+                            tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
+                            tma_load_2d(sb + 2 * A_BYTES, &map_yhi, kb * BK, t * BN, &full[stage]);
+                        } else {
                         mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
                         tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
                         tma_load_2d(sb + A_BYTES, &map_xlo, kb * BK, r * BM, &full[stage]);
                         tma_load_2d(sb + 2 * A_BYTES, &map_yhi, kb * BK, t * BN, &full[stage]);
                         tma_load_2d(sb + 2 * A_BYTES + B_BYTES, &map_ylo, kb * BK, t * BN, &full[stage]);
+                        }
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                 }
@@ -191,15 +205,19 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
                         mbar_wait(&full[stage], phase);
                         fence_after();
                         const uint32_t sb = smem_u32(base + stage * STAGE_BYTES);
-                        const uint64_t ahi = sw128_desc(sb), alo = sw128_desc(sb + A_BYTES);
-                        const uint64_t bhi = sw128_desc(sb + 2 * A_BYTES);
-                        const uint64_t blo = sw128_desc(sb + 2 * A_BYTES + B_BYTES);
+                        const uint64_t ahi = sw_desc(sb), alo = sw_desc(sb + A_BYTES);
+                        const uint64_t bhi = sw_desc(sb + 2 * A_BYTES);
+                        const uint64_t blo = sw_desc(sb + 2 * A_BYTES + B_BYTES);
 #pragma unroll
                         for (int k = 0; k < BK / 8; ++k) {
                             const uint64_t off = (uint64_t)(k * 32) >> 4;    // 8 tf32 = 32 B
+                            if (p.dbg & 1) {
+                                mma_tf32(d_tmem, ahi + off, bhi + off, (kb | k) != 0);
+                            } else {
                             mma_tf32(d_tmem, alo + off, bhi + off, (kb | k) != 0);
                             mma_tf32(d_tmem, ahi + off, blo + off, 1);
                             mma_tf32(d_tmem, ahi + off, bhi + off, 1);
+                            }
                         }
                         mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -211,9 +229,15 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
         }
     } else {
         // ------------------------------ epilogue: 4 warps, one query row per thread ------------
+        // Per value: d~ = fma(-2, S, |x|^2 + |y|^2) and one compare with the row's K'-th best;
+        // hits are appended to a per-thread candidate buffer in shared memory (a few instructions,
+        // so warp divergence on hits stays cheap) and merged into the sorted register list at the
+        // end of every tile or when the buffer fills.
         const int q = warp & 3;                      // TMEM lane quarter this warp may access
         const int row_in_tile = q * 32 + lane;
         const int et = threadIdx.x - 64;             // 0..127
+        float *cbd = cand_d + et;                    // column et of a [CB][128] array
+        int32_t *cbj = cand_j + et;
         int acc = 0; uint32_t aphase = 0;
         for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
             const int g = u / p.n_rtiles, r = u % p.n_rtiles;
@@ -225,6 +249,11 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
 #pragma unroll
             for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
             float kth = INFINITY;
+            // Units of the same row in other CTAs publish their K'-th best: anything not below
+            // it cannot enter the row's global top-K' (R17 screening), so it is not a candidate.
+            float thr = i < p.M ? __uint_as_float(atomicAdd(p.row_thr + i, 0u)) : INFINITY;
+            float lim = fminf(kth, thr);
+            int nc = 0;
             for (int t = t0; t < t1; ++t) {
                 float *yb = ybuf + acc * BN;
                 for (int c = et; c < BN; c += 128) {
@@ -240,16 +269,43 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
                     uint32_t v[32];
                     tmem_ld32(taddr + c * 32, v);
 #pragma unroll
-                    for (int k = 0; k < 32; ++k) {
-                        const float dt = fmaf(-2.0f, __uint_as_float(v[k]), xn + yb[c * 32 + k]);
-                        if (dt < kth) kp_insert<KP>(bd, bj, dt, t * BN + c * 32 + k, kth);
+                    for (int k4 = 0; k4 < 8; ++k4) {
+                        const float4 y4 = *reinterpret_cast<const float4 *>(yb + c * 32 + 4 * k4);
+                        const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+                        for (int e = 0; e < 4; ++e) {
+                            const int k = 4 * k4 + e;
+                            const float dt = fmaf(-2.0f, __uint_as_float(v[k]), xn + yv[e]);
+                            if (dt < lim) {
+                                cbd[nc * 128] = dt;
+                                cbj[nc * 128] = t * BN + c * 32 + k;
+                                ++nc;
+                            }
+                        }
+                        if (nc > CB - 4) {                // room for the next 4 values
+                            for (int m = 0; m < nc; ++m) {
+                                const float dd = cbd[m * 128];
+                                if (dd < kth) kp_insert<KP>(bd, bj, dd, cbj[m * 128], kth);
+                            }
+                            nc = 0;
+                            lim = fminf(kth, thr);
+                        }
                     }
                 }
                 fence_before();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&tempty[acc]);
                 if (++acc == 2) { acc = 0; aphase ^= 1; }
+                for (int m = 0; m < nc; ++m) {
+                    const float dd = cbd[m * 128];
+                    if (dd < kth) kp_insert<KP>(bd, bj, dd, cbj[m * 128], kth);
+                }
+                nc = 0;
+                if (i < p.M) thr = fminf(thr, __uint_as_float(atomicAdd(p.row_thr + i, 0u)));
+                lim = fminf(kth, thr);
             }
+            if (i < p.M && bj[KP - 1] >= 0)
+                atomicMin(p.row_thr + i, __float_as_uint(fmaxf(bd[KP - 1], 0.0f)));
             if (i < p.M) {
                 float *od = p.pd + ((int64_t)g * p.M + i) * KP;
                 int32_t *oj = p.pj + ((int64_t)g * p.M + i) * KP;
@@ -385,13 +441,14 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
 }
 
 // ---- exact fp64 rescan of rows whose screening was not certified ---------------------------------
-constexpr int FB_THREADS = 256;
+constexpr int FB_THREADS = 512;
 constexpr int FB_WARPS = FB_THREADS / 32;
 constexpr int FB_LIST = 32;              // >= K: one warp's list can hold the whole top-K
+constexpr int FB_ILP = 4;                // refs per warp iteration (independent load streams)
 
-// One CTA per flagged row: warp w scans refs j = w, w + 8, ... with its lanes striding over D
-// (coalesced), fp64 direct differences; lane 0 keeps the warp's sorted (d, j) list; thread 0
-// merges the 8 lists.  Rare (rows failing the R17 certificate), so simplicity wins.
+// One CTA per flagged row: warp w scans refs w*4 .. w*4+3, then + 64, ..., its lanes striding
+// over D (coalesced), fp64 direct differences; lane 0 keeps the warp's sorted (d, j) list;
+// thread 0 merges the 16 lists.  Rare (rows failing the R17 certificate).
 __global__ void __launch_bounds__(FB_THREADS)
 fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t N, int D, int K,
                 const int *fb_count, const int32_t *fb_rows, float *dist, int64_t *idx,
@@ -405,23 +462,42 @@ fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_
         if (lane == 0)
             for (int k = 0; k < FB_LIST; ++k) { sd[w][k] = INFINITY; sj[w][k] = -1; }
         __syncwarp();
-        for (int64_t j = w; j < N; j += FB_WARPS) {
-            double s = 0.0;
+        for (int64_t j0 = (int64_t)w * FB_ILP; j0 < N; j0 += (int64_t)FB_WARPS * FB_ILP) {
+            double s[FB_ILP];
+#pragma unroll
+            for (int u = 0; u < FB_ILP; ++u) s[u] = 0.0;
             for (int c = lane; c < D; c += 32) {
-                const double dv = (double)x[i * D + c] - (double)y[j * D + c];
-                s = fma(dv, dv, s);
+                const double xv = (double)x[i * D + c];
+#pragma unroll
+                for (int u = 0; u < FB_ILP; ++u) {
+                    if (j0 + u < N) {
+                        const double dv = xv - (double)y[(j0 + u) * D + c];
+                        s[u] = fma(dv, dv, s[u]);
+                    }
+                }
             }
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-            if (lane == 0 && s < sd[w][FB_LIST - 1]) {          // j ascending within the warp
-                int pos = FB_LIST - 1;
-                while (pos > 0 && s < sd[w][pos - 1]) { sd[w][pos] = sd[w][pos - 1]; sj[w][pos] = sj[w][pos - 1]; --pos; }
-                sd[w][pos] = s; sj[w][pos] = (int32_t)j;
+            for (int u = 0; u < FB_ILP; ++u) {
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+            }
+            if (lane == 0) {
+#pragma unroll
+                for (int u = 0; u < FB_ILP; ++u) {                  // j ascending within the warp
+                    if (j0 + u < N && s[u] < sd[w][FB_LIST - 1]) {
+                        int pos = FB_LIST - 1;
+                        while (pos > 0 && s[u] < sd[w][pos - 1]) {
+                            sd[w][pos] = sd[w][pos - 1]; sj[w][pos] = sj[w][pos - 1]; --pos;
+                        }
+                        sd[w][pos] = s[u]; sj[w][pos] = (int32_t)(j0 + u);
+                    }
+                }
             }
         }
         __syncthreads();
         if (threadIdx.x == 0) {
-            int head[FB_WARPS] = {0};
+            int head[FB_WARPS];
+            for (int q = 0; q < FB_WARPS; ++q) head[q] = 0;
             for (int k = 0; k < K; ++k) {
                 int best = -1;
                 for (int q = 0; q < FB_WARPS; ++q) {
@@ -469,7 +545,7 @@ static cudaError_t make_map(CUtensorMap *m, const float *ptr, int64_t rows, int 
     cuuint32_t box[2] = {(cuuint32_t)tc::BK, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)ptr, dims, strides, box, estr,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
 }
@@ -483,7 +559,7 @@ size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K) {
     const int n_groups = (n_ttiles + knn_tc_group() - 1) / knn_tc_group();
     auto al = [](size_t v) { return (v + 1023) & ~size_t(1023); };
     return al((size_t)M * Dp * 4) * 2 + al((size_t)N * Dp * 4) * 2 + al((size_t)M * 4) +
-           al((size_t)N * 4) + al(64) + al((size_t)n_groups * M * KP * 4) * 2 + al((size_t)M * 4) + al(64);
+           al((size_t)N * 4) + al(64) + al((size_t)n_groups * M * KP * 4) * 2 + al((size_t)M * 4) * 2 + al(64);
 }
 
 template <int KP>
@@ -520,6 +596,7 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     float *yn = (float *)s; s += al((size_t)N * 4);
     unsigned int *ymax = (unsigned int *)s; s += al(64);
     float *pd = (float *)s; s += al((size_t)n_groups * M * KP * 4);
+    unsigned int *row_thr = (unsigned int *)s; s += al((size_t)M * 4);
     int32_t *pj = (int32_t *)s; s += al((size_t)n_groups * M * KP * 4);
     int32_t *fb_rows = (int32_t *)s; s += al((size_t)M * 4);
     int *fb_count = (int *)s;
@@ -539,6 +616,9 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     tc::Params p;
     p.M = M; p.N = N; p.Dp = Dp; p.nk = Dp / tc::BK; p.n_rtiles = n_rtiles; p.n_ttiles = n_ttiles;
     p.n_groups = n_groups; p.group = group; p.xn = xn; p.yn = yn; p.pd = pd; p.pj = pj;
+    p.dbg = getenv("GENRED_KNN_DBG") ? atoi(getenv("GENRED_KNN_DBG")) : 0;
+    p.row_thr = row_thr;
+    if ((e = cudaMemsetAsync(row_thr, 0x7f, (size_t)M * 4, st)) != cudaSuccess) return e;   // 3.4e38
     const int n_units = n_groups * n_rtiles;
     const int grid = std::min(n_units, a.num_sms);
     if (a.ev_start) cudaEventRecord(a.ev_start, st);
