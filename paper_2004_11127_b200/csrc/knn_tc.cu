@@ -441,79 +441,136 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
 }
 
 // ---- exact fp64 rescan of rows whose screening was not certified ---------------------------------
-constexpr int FB_THREADS = 512;
+// Rare (rows failing the R17 certificate) but a full scan of N refs x D per row: every CTA of the
+// grid takes one chunk of the refs of each flagged row (warps over refs, lanes over D, fp64
+// direct differences), writes its sorted partial list, and the last CTA to finish a row merges
+// the G lists (threadfence + counter).  Rows beyond FB_CAP fall back to a single-CTA scan.
+constexpr int FB_THREADS = 256;
 constexpr int FB_WARPS = FB_THREADS / 32;
-constexpr int FB_LIST = 32;              // >= K: one warp's list can hold the whole top-K
-constexpr int FB_ILP = 4;                // refs per warp iteration (independent load streams)
+constexpr int FB_LIST = 32;              // >= K
+constexpr int FB_ILP = 4;                // refs per warp iteration
+constexpr int FB_CAP = 64;               // rows handled grid-wide
+constexpr int FB_GRID = 296;
 
-// One CTA per flagged row: warp w scans refs w*4 .. w*4+3, then + 64, ..., its lanes striding
-// over D (coalesced), fp64 direct differences; lane 0 keeps the warp's sorted (d, j) list;
-// thread 0 merges the 16 lists.  Rare (rows failing the R17 certificate).
-__global__ void __launch_bounds__(FB_THREADS)
-fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t N, int D, int K,
-                const int *fb_count, const int32_t *fb_rows, float *dist, int64_t *idx,
-                int64_t j_offset) {
-    __shared__ double sd[FB_WARPS][FB_LIST];
-    __shared__ int32_t sj[FB_WARPS][FB_LIST];
-    const int n = *fb_count;
+__device__ void fb_scan_chunk(const float *__restrict__ x, const float *__restrict__ y, int64_t i,
+                              int64_t jlo, int64_t jhi, int D, double (*sd)[FB_LIST],
+                              int32_t (*sj)[FB_LIST]) {
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int f = blockIdx.x; f < n; f += gridDim.x) {
-        const int64_t i = fb_rows[f];
-        if (lane == 0)
-            for (int k = 0; k < FB_LIST; ++k) { sd[w][k] = INFINITY; sj[w][k] = -1; }
-        __syncwarp();
-        for (int64_t j0 = (int64_t)w * FB_ILP; j0 < N; j0 += (int64_t)FB_WARPS * FB_ILP) {
-            double s[FB_ILP];
+    if (lane == 0)
+        for (int k = 0; k < FB_LIST; ++k) { sd[w][k] = INFINITY; sj[w][k] = -1; }
+    __syncwarp();
+    for (int64_t j0 = jlo + (int64_t)w * FB_ILP; j0 < jhi; j0 += (int64_t)FB_WARPS * FB_ILP) {
+        double s[FB_ILP];
 #pragma unroll
-            for (int u = 0; u < FB_ILP; ++u) s[u] = 0.0;
-            for (int c = lane; c < D; c += 32) {
-                const double xv = (double)x[i * D + c];
-#pragma unroll
-                for (int u = 0; u < FB_ILP; ++u) {
-                    if (j0 + u < N) {
-                        const double dv = xv - (double)y[(j0 + u) * D + c];
-                        s[u] = fma(dv, dv, s[u]);
-                    }
-                }
-            }
+        for (int u = 0; u < FB_ILP; ++u) s[u] = 0.0;
+        for (int c = lane; c < D; c += 32) {
+            const double xv = (double)x[i * D + c];
 #pragma unroll
             for (int u = 0; u < FB_ILP; ++u) {
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
-            }
-            if (lane == 0) {
-#pragma unroll
-                for (int u = 0; u < FB_ILP; ++u) {                  // j ascending within the warp
-                    if (j0 + u < N && s[u] < sd[w][FB_LIST - 1]) {
-                        int pos = FB_LIST - 1;
-                        while (pos > 0 && s[u] < sd[w][pos - 1]) {
-                            sd[w][pos] = sd[w][pos - 1]; sj[w][pos] = sj[w][pos - 1]; --pos;
-                        }
-                        sd[w][pos] = s[u]; sj[w][pos] = (int32_t)(j0 + u);
-                    }
+                if (j0 + u < jhi) {
+                    const double dv = xv - (double)y[(j0 + u) * D + c];
+                    s[u] = fma(dv, dv, s[u]);
                 }
             }
         }
-        __syncthreads();
+#pragma unroll
+        for (int u = 0; u < FB_ILP; ++u) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) s[u] += __shfl_xor_sync(0xffffffffu, s[u], o);
+        }
+        if (lane == 0) {
+#pragma unroll
+            for (int u = 0; u < FB_ILP; ++u) {                      // j ascending within the warp
+                if (j0 + u < jhi && s[u] < sd[w][FB_LIST - 1]) {
+                    int pos = FB_LIST - 1;
+                    while (pos > 0 && s[u] < sd[w][pos - 1]) {
+                        sd[w][pos] = sd[w][pos - 1]; sj[w][pos] = sj[w][pos - 1]; --pos;
+                    }
+                    sd[w][pos] = s[u]; sj[w][pos] = (int32_t)(j0 + u);
+                }
+            }
+        }
+    }
+    __syncthreads();
+}
+
+// Merge `nl` sorted (d, j) lists (stride `ld` apart) into the first `K` of (od, oj).
+__device__ void fb_merge(const double *ld_d, const int32_t *ld_j, int nl, int ld, int K,
+                         double *od, int32_t *oj) {
+    int head[FB_GRID > FB_WARPS ? FB_GRID : FB_WARPS];
+    for (int q = 0; q < nl; ++q) head[q] = 0;
+    for (int k = 0; k < K; ++k) {
+        int best = -1;
+        for (int q = 0; q < nl; ++q) {
+            if (head[q] >= FB_LIST) continue;
+            const int32_t j = ld_j[q * ld + head[q]];
+            if (j < 0) continue;
+            const double d = ld_d[q * ld + head[q]];
+            if (best < 0 || d < ld_d[best * ld + head[best]] ||
+                (d == ld_d[best * ld + head[best]] && j < ld_j[best * ld + head[best]]))
+                best = q;
+        }
+        if (best >= 0) {
+            od[k] = ld_d[best * ld + head[best]];
+            oj[k] = ld_j[best * ld + head[best]];
+            head[best]++;
+        } else {
+            od[k] = INFINITY;
+            oj[k] = -1;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(FB_THREADS)
+fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_t N, int D, int K,
+                const int *fb_count, const int32_t *fb_rows, double *part_d, int32_t *part_j,
+                unsigned int *done, float *dist, int64_t *idx, int64_t j_offset) {
+    __shared__ double sd[FB_WARPS][FB_LIST];
+    __shared__ int32_t sj[FB_WARPS][FB_LIST];
+    __shared__ int is_last;
+    const int n = *fb_count;
+    const int ncap = n < FB_CAP ? n : FB_CAP;
+    const int G = gridDim.x;
+    // grid-wide rows
+    for (int f = 0; f < ncap; ++f) {
+        const int64_t i = fb_rows[f];
+        const int64_t jlo = N * blockIdx.x / G, jhi = N * (blockIdx.x + 1) / G;
+        fb_scan_chunk(x, y, i, jlo, jhi, D, sd, sj);
         if (threadIdx.x == 0) {
-            int head[FB_WARPS];
-            for (int q = 0; q < FB_WARPS; ++q) head[q] = 0;
+            double md[FB_LIST];
+            int32_t mj[FB_LIST];
+            fb_merge(&sd[0][0], &sj[0][0], FB_WARPS, FB_LIST, FB_LIST, md, mj);
+            double *pd = part_d + ((int64_t)f * G + blockIdx.x) * FB_LIST;
+            int32_t *pj = part_j + ((int64_t)f * G + blockIdx.x) * FB_LIST;
+            for (int k = 0; k < FB_LIST; ++k) { pd[k] = md[k]; pj[k] = mj[k]; }
+            __threadfence();
+            is_last = atomicAdd(done + f, 1u) == (unsigned)(G - 1);
+        }
+        __syncthreads();
+        if (is_last && threadIdx.x == 0) {
+            __threadfence();
+            double md[FB_LIST];
+            int32_t mj[FB_LIST];
+            fb_merge(part_d + (int64_t)f * G * FB_LIST, part_j + (int64_t)f * G * FB_LIST, G, FB_LIST,
+                     K, md, mj);
             for (int k = 0; k < K; ++k) {
-                int best = -1;
-                for (int q = 0; q < FB_WARPS; ++q) {
-                    if (head[q] >= FB_LIST || sj[q][head[q]] < 0) continue;
-                    if (best < 0 || sd[q][head[q]] < sd[best][head[best]] ||
-                        (sd[q][head[q]] == sd[best][head[best]] && sj[q][head[q]] < sj[best][head[best]]))
-                        best = q;
-                }
-                if (best >= 0) {
-                    dist[i * K + k] = (float)sd[best][head[best]];
-                    idx[i * K + k] = (int64_t)sj[best][head[best]] + j_offset;
-                    head[best]++;
-                } else {
-                    dist[i * K + k] = INFINITY;
-                    idx[i * K + k] = -1;
-                }
+                dist[i * K + k] = mj[k] >= 0 ? (float)md[k] : INFINITY;
+                idx[i * K + k] = mj[k] >= 0 ? (int64_t)mj[k] + j_offset : -1;
+            }
+        }
+        __syncthreads();
+    }
+    // rows beyond the cap: one CTA per row
+    for (int f = FB_CAP + blockIdx.x; f < n; f += G) {
+        const int64_t i = fb_rows[f];
+        fb_scan_chunk(x, y, i, 0, N, D, sd, sj);
+        if (threadIdx.x == 0) {
+            double md[FB_LIST];
+            int32_t mj[FB_LIST];
+            fb_merge(&sd[0][0], &sj[0][0], FB_WARPS, FB_LIST, K, md, mj);
+            for (int k = 0; k < K; ++k) {
+                dist[i * K + k] = mj[k] >= 0 ? (float)md[k] : INFINITY;
+                idx[i * K + k] = mj[k] >= 0 ? (int64_t)mj[k] + j_offset : -1;
             }
         }
         __syncthreads();
@@ -559,7 +616,8 @@ size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K) {
     const int n_groups = (n_ttiles + knn_tc_group() - 1) / knn_tc_group();
     auto al = [](size_t v) { return (v + 1023) & ~size_t(1023); };
     return al((size_t)M * Dp * 4) * 2 + al((size_t)N * Dp * 4) * 2 + al((size_t)M * 4) +
-           al((size_t)N * 4) + al(64) + al((size_t)n_groups * M * KP * 4) * 2 + al((size_t)M * 4) * 2 + al(64);
+           al((size_t)N * 4) + al(64) + al((size_t)n_groups * M * KP * 4) * 2 + al((size_t)M * 4) * 2 + al(64) +
+           al((size_t)tc::FB_CAP * tc::FB_GRID * tc::FB_LIST * 12) + al((size_t)tc::FB_CAP * 4) + 2048;
 }
 
 template <int KP>
@@ -599,6 +657,9 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     unsigned int *row_thr = (unsigned int *)s; s += al((size_t)M * 4);
     int32_t *pj = (int32_t *)s; s += al((size_t)n_groups * M * KP * 4);
     int32_t *fb_rows = (int32_t *)s; s += al((size_t)M * 4);
+    double *fb_pd = (double *)s; s += al((size_t)tc::FB_CAP * tc::FB_GRID * tc::FB_LIST * 8);
+    int32_t *fb_pj = (int32_t *)s; s += al((size_t)tc::FB_CAP * tc::FB_GRID * tc::FB_LIST * 4);
+    unsigned int *fb_done = (unsigned int *)s; s += al((size_t)tc::FB_CAP * 4);
     int *fb_count = (int *)s;
 
     int kernels = 0;
@@ -634,7 +695,10 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     else
         tc::rerank_kernel<32><<<rgrid, 128, 0, st>>>(pd, pj, n_groups, a.x, a.y, xn, ymax, M, N, D, K,
                                                      a.dist, a.idx, a.j_offset, fb_count, fb_rows);
-    tc::fallback_kernel<<<148, tc::FB_THREADS, 0, st>>>(a.x, a.y, N, D, K, fb_count, fb_rows, a.dist, a.idx, a.j_offset);
+    if ((e = cudaMemsetAsync(fb_done, 0, tc::FB_CAP * 4, st)) != cudaSuccess) return e;
+    tc::fallback_kernel<<<tc::FB_GRID, tc::FB_THREADS, 0, st>>>(a.x, a.y, N, D, K, fb_count, fb_rows,
+                                                                fb_pd, fb_pj, fb_done, a.dist, a.idx,
+                                                                a.j_offset);
     kernels += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
     if (info) {

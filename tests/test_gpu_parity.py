@@ -396,15 +396,16 @@ def test_argkmin_tensor_path_fallback_certificate(G):
     """Refs equidistant from the query defeat any screening margin: the R17 certificate must
     reject those rows and the exact rescan must return the lowest indices (ties -> lowest j)."""
     D = 32
-    x = np.zeros((3, D), np.float32); x[1] += 0.5
+    x = np.zeros((70, D), np.float32); x[1] += 0.5     # 69 equidistant rows: > FB_CAP (64) flagged
     y = np.zeros((600, D), np.float32)
     for jj in range(600):
         y[jj, jj % D] = 1.0 if (jj // D) % 2 == 0 else -1.0       # |x0 - y_j| = 1 for all j
     d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=10)
     plan = G.last_plan()
-    assert plan["fallback_rows"] >= 1
+    assert plan["fallback_rows"] >= 65
     od, oj = oracle.argkmin(x, y, 11)
     assert host(j)[0].tolist() == list(range(10))
+    assert host(j)[69].tolist() == list(range(10))
     argk_check(host(d), host(j), od, oj, 10, what="fallback")
 
 
