@@ -4,16 +4,49 @@
 //     points (monoid merges),
 //   * neutral outputs for an empty reduction axis.
 #include <math.h>
+#include <string.h>
+
+#include <cmath>
 
 #include "device.cuh"
+#include "geo.cuh"
 #include "internal.h"
 
 namespace genred {
 
 __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *__restrict__ b,
                             int64_t N, int D, int E, float s, double hscale, int64_t npairs, int RS,
-                            float *__restrict__ J) {
+                            float *__restrict__ J, const uint32_t *geo_enc) {
     const float NEG_INF = -INFINITY;
+    if (kind == PACK_GAUSS_AUTO) {
+        // Gaussian Sum records: [2D coords][w pair][2E signal]; expanded or direct per geo
+        const Geo geo = geo_decode(geo_enc, D, s);
+        for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
+             p += (int64_t)gridDim.x * blockDim.x) {
+            float *rec = J + p * RS;
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = 2 * p + h;
+                const bool valid = j < N;
+                double w = 0.0;
+                for (int d = 0; d < D; ++d) {
+                    const float v = valid ? y[j * D + d] : 0.0f;
+                    float r;
+                    if (geo.expanded) {
+                        r = valid ? s * (v - geo.c[d]) : 0.0f;        // y' = s (y - c)
+                        w += (double)r * (double)r;
+                    } else {
+                        r = valid ? -(s * v) : 0.0f;
+                    }
+                    rec[2 * d + h] = r;
+                }
+                rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;   // w = -|y'|^2
+                for (int e = 0; e < E; ++e)                           // padding: b = 0
+                    rec[2 * D + 2 + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
+            }
+            for (int k = 2 * (D + 1 + E); k < RS; ++k) rec[k] = 0.0f;
+        }
+        return;
+    }
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
          p += (int64_t)gridDim.x * blockDim.x) {
         float *rec = J + p * RS;
@@ -46,19 +79,94 @@ __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *
 }
 
 int pack_record_stride(int kind, int D, int E) {
+    if (kind == PACK_GAUSS_AUTO) return record_stride(D + 1, E);
     if (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) return record_stride(D, 0);
     if (kind == PACK_LSE_H) return record_stride(D, 2);
     return record_stride(D, E);
 }
 
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E, float s,
-                        double hscale, int64_t npairs, float *J, cudaStream_t st) {
+                        double hscale, int64_t npairs, float *J, cudaStream_t st, const uint32_t *geo) {
     const int RS = pack_record_stride(kind, D, E);
     int64_t blocks = (npairs + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
-    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind, y, b, N, D, E, s, hscale, npairs, RS, J);
+    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind, y, b, N, D, E, s, hscale, npairs, RS, J, geo);
     return cudaGetLastError();
+}
+
+// ---- per-coordinate bounding box of x and y (order-preserving uint encodings, geo.cuh) -------
+__global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float *__restrict__ y,
+                            int64_t N, int D, uint32_t *geo) {
+    float lo[8], hi[8];
+#pragma unroll
+    for (int d = 0; d < 8; ++d) { lo[d] = INFINITY; hi[d] = -INFINITY; }
+    const int64_t rows = M + N;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const float *pt = t < M ? x + t * D : y + (t - M) * D;
+#pragma unroll
+        for (int d = 0; d < 8; ++d) {
+            if (d < D) {
+                const float v = pt[d];
+                lo[d] = fminf(lo[d], v);
+                hi[d] = fmaxf(hi[d], v);
+            }
+        }
+    }
+#pragma unroll
+    for (int d = 0; d < 8; ++d) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            lo[d] = fminf(lo[d], __shfl_xor_sync(0xffffffffu, lo[d], o));
+            hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
+        }
+    }
+    if ((threadIdx.x & 31) == 0) {
+        for (int d = 0; d < D; ++d) {
+            if (lo[d] <= hi[d]) {
+                atomicMin(geo + d, f2ord(lo[d]));
+                atomicMax(geo + 8 + d, f2ord(hi[d]));
+            }
+        }
+    }
+}
+
+cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, int D, uint32_t *geo,
+                        cudaStream_t st) {
+    cudaError_t e = cudaMemsetAsync(geo, 0xff, 8 * sizeof(uint32_t), st);      // minima: max code
+    if (e == cudaSuccess) e = cudaMemsetAsync(geo + 8, 0x00, 8 * sizeof(uint32_t), st);
+    if (e != cudaSuccess) return e;
+    int64_t blocks = (M + N + 255) / 256;
+    if (blocks > 148 * 4) blocks = 148 * 4;
+    if (blocks < 1) blocks = 1;
+    bbox_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, M, y, N, D, geo);
+    return cudaGetLastError();
+}
+
+bool geo_expanded_host(const uint32_t *geo_dev, int D, float s) {
+    uint32_t h[16];
+    if (cudaMemcpy(h, geo_dev, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    auto dec = [](uint32_t e) {
+        uint32_t u = (e & 0x80000000u) ? (e & 0x7fffffffu) : ~e;
+        float f;
+        memcpy(&f, &u, 4);
+        return f;
+    };
+    float r2 = 0.0f;
+    bool ok = true;
+    for (int d = 0; d < D; ++d) {
+        const float lo = dec(h[d]), hi = dec(h[8 + d]);
+        ok = ok && std::isfinite(lo) && std::isfinite(hi);
+        const float c = 0.5f * lo + 0.5f * hi;
+        const float hh = fmaxf(hi - c, c - lo) * 1.0001f;
+        const float sh = s * hh;
+        r2 = fmaf(sh, sh, r2);
+    }
+    return ok && r2 <= kExpandedR2Max;
 }
 
 // ---- Sum / gradient: out = scale * sum_{split} part[split] in split order ----------------------

@@ -31,6 +31,9 @@ struct genred_ctx {
     int64_t launches = 0;
     std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
     int *fallback_dev = nullptr;                               // k-NN rows rescanned exactly
+    const uint32_t *geo_dev = nullptr;                         // Gaussian Sum bounding box
+    int geo_D = 0;
+    float geo_s = 0.f;
     bool profiling = false;
     std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
     int nprof = 0;
@@ -227,6 +230,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     const int D = a->D, E = a->E;
     ctx->plan = genred_plan{};
     ctx->plan.tile_j = kTileJ;
+    ctx->geo_dev = nullptr;
     if (M == 0) return GENRED_OK;
     const int out_f64 = a->out_dtype == GENRED_F64;
     cudaError_t e;
@@ -250,15 +254,17 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
                        : (f == GENRED_GAUSS_SUM_GRADX) ? 2 : 3;
         const int rmax = sum_rows_per_thread_max(mode, D, E);
         Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
-        const int RS = record_stride(D, E);
+        const int pk = mode == 3 ? PACK_SQDIST_SUM : (mode == 0 ? PACK_GAUSS_AUTO : PACK_GAUSS);
+        const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
-        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes);
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256);
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
+        uint32_t *geo = (uint32_t *)((char *)ctx->scratch + jbytes + pbytes);
         // parameter folding in fp64, rounded once to fp32 (R15, R18)
         float sc = 1.0f;
         double scale_grad = 0.0;
@@ -267,19 +273,24 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             sc = (float)(sqrt(kLog2e) / sig);                   // 2^(-|s x - s y|^2) = e^(-|x-y|^2/sig^2)
             scale_grad = -2.0 / (sig * sig * (double)sc);        // (x - y) = (x' - y') / s
         }
-        e = launch_pack(mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st);
+        int kernels = 2;
+        if (mode == 0) {
+            e = launch_bbox(a->x, M, a->y, N, D, geo, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
+            kernels++;
+        }
+        e = launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         SumLaunch L;
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
         L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
-        L.out_grad = a->out_grad; L.part = part;
+        L.out_grad = a->out_grad; L.part = part; L.geo = geo;
         int ctas = 0;
         prof_event(ctx, true, st);
         e = launch_sum(L, st, &ctas);
         prof_event(ctx, false, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
-        int kernels = 2;
         if (pl.split > 1) {
             const int cols_sum = (mode == 1) ? 0 : E;
             e = launch_sum_finalize(part, pl.split, M, C, cols_sum, a->g, E, 1.0, scale_grad, mode,
@@ -291,6 +302,9 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->geo_dev = mode == 0 ? geo : nullptr;
+        ctx->geo_D = D;
+        ctx->geo_s = sc;
         return GENRED_OK;
     }
 
@@ -571,6 +585,8 @@ genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
     if (!ctx || !plan) return GENRED_E_INVALID;
     *plan = ctx->plan;
     plan->fallback_rows = -1;
+    if (ctx->plan.path == 0 && ctx->geo_dev && geo_expanded_host(ctx->geo_dev, ctx->geo_D, ctx->geo_s))
+        plan->path = 2;                                        // expanded form + FMA-pipe exp2
     if (ctx->plan.path == 1 && ctx->fallback_dev) {
         int n = -1;
         if (cudaMemcpy(&n, ctx->fallback_dev, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {

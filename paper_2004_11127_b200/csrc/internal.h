@@ -15,7 +15,8 @@ constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference
 // Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
 
-enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4 };
+enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4,
+                PACK_GAUSS_AUTO = 5 };
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
 // kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
@@ -23,14 +24,23 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 // h'lo[2p+1]) with h' = hscale * h split into fp32 hi + lo (LSE with h).  Records past N
 // (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf (LSE, ArgKMin),
 // which contribute nothing.
+// PACK_GAUSS_AUTO (Gaussian Sum): decodes the bounding box `geo` (geo.cuh) and writes either the
+// expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-s y, 0, b).
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
-                        float s, double hscale, int64_t npairs, float *J, cudaStream_t st);
+                        float s, double hscale, int64_t npairs, float *J, cudaStream_t st,
+                        const uint32_t *geo = nullptr);
+// Per-coordinate bounding box of x (M x D) and y (N x D) into geo[16] (encoded, geo.cuh).
+cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, int D, uint32_t *geo,
+                        cudaStream_t st);
+// Host mirror of the device path decision (reads geo back; synchronises; introspection only).
+bool geo_expanded_host(const uint32_t *geo_dev, int D, float s);
 int pack_record_stride(int kind, int D, int E);
 
 struct SumLaunch {
     int mode;                 // 0 SUM, 1 GRADX, 2 SUM_GRADX, 3 SQDIST_SUM
     int D, E, R;              // R = rows per consumer thread
     const float *x, *J, *g;
+    const uint32_t *geo;      // MODE 0: encoded bounding box (geo.cuh)
     int64_t M;
     int split;                // number of j-splits (grid = itiles * split)
     int64_t tiles_per_split, ntiles;

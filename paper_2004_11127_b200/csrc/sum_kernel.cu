@@ -19,16 +19,19 @@
 #include <math.h>
 
 #include "device.cuh"
+#include "geo.cuh"
 #include "internal.h"
 
 namespace genred {
 
 template <int MODE, int D, int E>
 struct SumCfg {
-    static constexpr int RS = ((2 * (D + E)) + 3) / 4 * 4;       // floats per record pair
+    // record pair: 2D coordinates, then (MODE 0 only) the pair slot of w = -|y'|^2 used by the
+    // expanded form, then 2E signal values; padded to a multiple of 16 bytes
+    static constexpr int BOFF = (MODE == 0) ? 2 * (D + 1) : 2 * D;
+    static constexpr int RS = ((BOFF + 2 * E) + 3) / 4 * 4;       // floats per record pair
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
-    static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
     static constexpr int NS = (MODE == 1) ? 0 : E;                // sum columns
     static constexpr int NG = (MODE == 1 || MODE == 2) ? D : 0;   // gradient columns
     static constexpr int C = NS + NG;
@@ -39,6 +42,7 @@ struct SumCfg {
 
 struct SumParams {
     const float *x, *J, *g;
+    const uint32_t *geo;      // MODE 0: encoded bounding box (geo.cuh)
     int64_t M;
     int split;
     int64_t tiles_per_split, ntiles;
@@ -50,32 +54,56 @@ struct SumParams {
     double *part;
 };
 
-template <int MODE, int D, int E, int R>
-__global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) sum_kernel(const SumParams p) {
+// 2^u for u in [-24, 6] (the expanded path's range, geo.cuh) on the FP32 pipe: u = n + f with
+// n = rint(u) from the 1.5*2^23 shifter, f in [-1/2, 1/2], a degree-5 near-minimax polynomial
+// (max relative error 7.5e-8; 2.3e-7 through fp32 Horner, on par with MUFU.EX2), and n added
+// to the exponent field with one integer LEA.  Two values per packed FADD2/FFMA2.
+__device__ __forceinline__ float2 ex2_poly2(float2 u) {
+    const float2 shifter = dup2(12582912.0f);
+    const float2 t = add2(u, shifter);
+    const float2 n = add2(t, dup2(-12582912.0f));
+    const float2 f = fma2(n, dup2(-1.0f), u);                       // u - n, exact
+    float2 q = fma2(dup2(1.327647129073739e-03f), f, dup2(9.675541892647743e-03f));
+    q = fma2(q, f, dup2(5.550713092088699e-02f));
+    q = fma2(q, f, dup2(2.402212023735046e-01f));
+    q = fma2(q, f, dup2(6.931469440460205e-01f));
+    q = fma2(q, f, dup2(1.000000119209290e+00f));
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
+// The pair loop + epilogue.  XP selects the expanded form of the Gaussian Sum (MODE 0 only):
+//   exp(-|x-y|^2/sigma^2) = 2^(-|x'|^2) * 2^(u),  u = 2 x'.y' - |y'|^2,  x' = s (x - c)
+// so a pair costs 3 FFMA (u, packed over two j's) + exp + 1 FFMA instead of 7 FP32 ops; the row
+// factor 2^(-|x'|^2) is applied in fp64 at the end.  With R = 4 the last row of every thread
+// evaluates its exps with ex2_poly2 on the FP32 pipe (1/4 of the exps), which balances the MUFU
+// pipe (16/clk/SM) against the FP32 pipes (128/clk/SM): 21.3 pairs/clk/SM instead of 16.
+template <int MODE, int D, int E, int R, bool XP>
+__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt,
+                                         int64_t row0, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
-    constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C;
-    extern __shared__ __align__(128) unsigned char smem_raw[];
-
-    const int64_t itile = blockIdx.x / p.split;
-    const int sp = (int)(blockIdx.x % p.split);
-    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
-    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-    const int nt = (int)(t1 - t0);
-
-    JRing<kStages> ring;
-    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
-
-    // ---- math warps: R rows per thread, registers only --------------------------------------
+    constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
+    constexpr bool POLY = XP && R == 4;
     const int ct = threadIdx.x;
-    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
     float xr[R][D];
     float gr[R][E];
+    double xsq[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
         const bool ok = i < p.M;
+        xsq[r] = 0.0;
 #pragma unroll
-        for (int d = 0; d < D; ++d) xr[r][d] = ok ? p.s * __ldg(p.x + i * D + d) : 0.0f;
+        for (int d = 0; d < D; ++d) {
+            const float v = ok ? __ldg(p.x + i * D + d) : 0.0f;
+            if constexpr (XP) {
+                const float xs = ok ? p.s * (v - geo.c[d]) : 0.0f;        // x' = s (x - c)
+                xsq[r] += (double)xs * (double)xs;
+                xr[r][d] = 2.0f * xs;                                      // exact doubling
+            } else {
+                xr[r][d] = p.s * v;
+            }
+        }
 #pragma unroll
         for (int e = 0; e < E; ++e)
             gr[r][e] = (Cfg::GRAD && E > 1 && ok && p.g) ? __ldg(p.g + i * E + e) : 1.0f;
@@ -107,7 +135,21 @@ __global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) su
 #pragma unroll
             for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
 #pragma unroll
-            for (int e = 0; e < E; ++e) bv[e] = make_float2(f[2 * D + 2 * e], f[2 * D + 2 * e + 1]);
+            for (int e = 0; e < E; ++e) bv[e] = make_float2(f[BOFF + 2 * e], f[BOFF + 2 * e + 1]);
+            if constexpr (XP) {
+                const float2 w = make_float2(f[2 * D], f[2 * D + 1]);              // -|y'|^2
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 u = fma2(dup2(xr[r][0]), ny[0], w);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(dup2(xr[r][d]), ny[d], u);   // 2x'.y' - |y'|^2
+                    float2 ex;
+                    if (POLY && r == R - 1) ex = ex2_poly2(u);
+                    else ex = make_float2(ex2(u.x), ex2(u.y));
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                }
+            } else {
 #pragma unroll
             for (int r = 0; r < R; ++r) {
                 float2 dd[D];
@@ -144,6 +186,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) su
                     }
                 }
             }
+            }
         }
         ring.release(k);
         // promote the tile's fp32 partials to fp64 (every 512 j)
@@ -167,6 +210,11 @@ __global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) su
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
         if (i >= p.M) continue;
+        if constexpr (XP) {
+            const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
+#pragma unroll
+            for (int c = 0; c < NS; ++c) acc64[r][c] *= fac;
+        }
         if (p.split > 1) {
             double *dst = p.part + ((int64_t)sp * p.M + i) * C;
 #pragma unroll
@@ -193,6 +241,30 @@ __global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) su
     }
 }
 
+template <int MODE, int D, int E, int R>
+__global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) sum_kernel(const SumParams p) {
+    using Cfg = SumCfg<MODE, D, E>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
+    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+    const int nt = (int)(t1 - t0);
+
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    if constexpr (MODE == 0) {
+        const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
+        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, sp, geo);
+        else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, sp, geo);
+    } else {
+        Geo geo{};
+        sum_body<MODE, D, E, R, false>(p, ring, nt, row0, sp, geo);
+    }
+}
+
 // ---- host-side dispatch over (MODE, D, E, R) ------------------------------------------------
 template <int MODE, int D, int E, int R>
 static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
@@ -209,7 +281,7 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;
     p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.s = a.s;
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
-    p.out_grad = a.out_grad; p.part = a.part;
+    p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
     const int64_t grid = itiles * a.split;

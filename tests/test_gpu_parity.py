@@ -419,3 +419,27 @@ def test_config4_full_size_sampled(G):
     od, oj = oracle.argkmin(x, y, c.K + 1, rows=rows)
     n_idx, n_dist = argk_check(host(d)[rows], host(j)[rows], od, oj, c.K, what="C4")
     assert n_idx >= 0.95 * len(rows) * c.K
+
+
+# ------------------------------------------------------------------------------------------------
+# Gaussian Sum: expanded form (+ FP32-pipe exp2 share) vs direct form, chosen on the device
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("case", ["unit_cube", "far_offset", "wide_direct", "gmm_signed", "small_M"])
+def test_gauss_sum_expanded_and_direct_paths(G, case):
+    rng = np.random.default_rng(hash(case) % 1000)
+    M, N, sigma, expect = 3000, 5000, 0.5, 2
+    x = synth.uniform3(M, 61); y = synth.uniform3(N, 62); b = synth.signal(N, 63)
+    if case == "far_offset":            # centring makes the expanded form exact-enough anywhere
+        x = (x + 1000.0).astype(np.float32); y = (y + 1000.0).astype(np.float32)
+    if case == "wide_direct":           # extent >> sigma: R^2 > 6 -> direct form
+        sigma, expect = 0.05, 0
+    if case == "gmm_signed":
+        x = synth.gmm3(M, 64); y = synth.gmm3(N, 65); b = synth.signal(N, 66, signed=True)
+    if case == "small_M":
+        M = 300; x = x[:M].copy()
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=sigma)
+    plan = G.last_plan()
+    assert plan["path"] == expect, plan
+    o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+    assert_sum_parity(host(a), o, den, what=f"gauss {case}")
