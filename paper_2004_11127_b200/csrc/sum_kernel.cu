@@ -17,6 +17,7 @@
 //   * j-splits (grid = i-tiles x splits) fill all 148 SMs; their fp64 partials are merged in a
 //     fixed order by sum_finalize (deterministic, no float atomics).
 #include <math.h>
+#include <stdlib.h>
 
 #include "device.cuh"
 #include "geo.cuh"
@@ -72,18 +73,22 @@ __device__ __forceinline__ float2 ex2_poly2(float2 u) {
                        __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
 }
 
+// Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
+// 14.90 with every exp on MUFU (M = N = 1e6, B200): the packed FFMA2s of the expanded form read
+// three register pairs and already load the FP32 pipe close to the MUFU time, so the share is off.
+constexpr bool kPolyShare = false;
+
 // The pair loop + epilogue.  XP selects the expanded form of the Gaussian Sum (MODE 0 only):
 //   exp(-|x-y|^2/sigma^2) = 2^(-|x'|^2) * 2^(u),  u = 2 x'.y' - |y'|^2,  x' = s (x - c)
-// so a pair costs 3 FFMA (u, packed over two j's) + exp + 1 FFMA instead of 7 FP32 ops; the row
-// factor 2^(-|x'|^2) is applied in fp64 at the end.  With R = 4 the last row of every thread
-// evaluates its exps with ex2_poly2 on the FP32 pipe (1/4 of the exps), which balances the MUFU
-// pipe (16/clk/SM) against the FP32 pipes (128/clk/SM): 21.3 pairs/clk/SM instead of 16.
+// so a pair costs 3 FFMA (u, packed over two j's) + exp + 1 FFMA instead of 7 FP32 ops, which
+// leaves the MUFU pipe (16 ex2/clk/SM) as the only bound; the row factor 2^(-|x'|^2) is applied
+// in fp64 at the end.
 template <int MODE, int D, int E, int R, bool XP>
 __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt,
                                          int64_t row0, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
-    constexpr bool POLY = XP && R == 4;
+    constexpr bool POLY = kPolyShare && XP && R == 4;
     const int ct = threadIdx.x;
     float xr[R][D];
     float gr[R][E];
@@ -123,8 +128,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-#pragma unroll 2
-        for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
+        for (int pp2 = 0; pp2 < Cfg::PAIRS; pp2 += 2) {
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+            const int pp = pp2 + hh;
             float f[RS];
 #pragma unroll
             for (int q = 0; q < RS / 4; ++q) {
@@ -144,7 +151,8 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
                     for (int d = 1; d < D; ++d) u = fma2(dup2(xr[r][d]), ny[d], u);   // 2x'.y' - |y'|^2
                     float2 ex;
-                    if (POLY && r == R - 1) ex = ex2_poly2(u);
+                    // FP32-pipe exp2 share (kPolyShare, off: see DESIGN.md Sec. 6 measurements)
+                    if (POLY && r == R - 1 && hh == 0) ex = ex2_poly2(u);
                     else ex = make_float2(ex2(u.x), ex2(u.y));
 #pragma unroll
                     for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
@@ -187,6 +195,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                 }
             }
             }
+        }
         }
         ring.release(k);
         // promote the tile's fp32 partials to fp64 (every 512 j)
