@@ -58,10 +58,11 @@ def measured_peaks() -> dict:
 def workload(cid: int) -> dict:
     """Per-config step definition: formula, algorithmic FP32 lane-ops and exps per pair (D=3)."""
     c = synth.config(cid)
-    if cid in (1, 5):
-        return dict(cfg=c, formula="gauss", reduction="sum", fp32=7, mufu=1, out_dtype="float32")
-    if cid == 2:   # Sum + gradient in one fused pass: 7 + (w=e*b) + 3 grad FMA + sum add = 12
-        return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=12, mufu=1,
+    if cid in (1, 5):  # expanded form: u = 2x'.y' - |y'|^2 (3 FFMA) + acc (1 FFMA) = 4 lane-ops
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=4, mufu=1, out_dtype="float32")
+    if cid == 2:   # Sum + gradient, one fused pass, expanded form: u (3 FFMA) + w = e b + S0 += w
+        #            + S += w y' (3 FFMA) = 8 lane-ops (the direct form needs 12)
+        return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=8, mufu=1,
                     out_dtype="float32")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")

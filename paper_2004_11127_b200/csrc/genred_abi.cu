@@ -254,7 +254,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
                        : (f == GENRED_GAUSS_SUM_GRADX) ? 2 : 3;
         const int rmax = sum_rows_per_thread_max(mode, D, E);
         Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
-        const int pk = mode == 3 ? PACK_SQDIST_SUM : (mode == 0 ? PACK_GAUSS_AUTO : PACK_GAUSS);
+        const int pk = mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
@@ -274,7 +274,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             scale_grad = -2.0 / (sig * sig * (double)sc);        // (x - y) = (x' - y') / s
         }
         int kernels = 2;
-        if (mode == 0) {
+        if (mode != 3) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
@@ -302,7 +302,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
-        ctx->geo_dev = mode == 0 ? geo : nullptr;
+        ctx->geo_dev = mode != 3 ? geo : nullptr;
         ctx->geo_D = D;
         ctx->geo_s = sc;
         return GENRED_OK;

@@ -8,8 +8,8 @@
 //   * RAW differences d = x - y (no pre-scaling of coordinates: the query shift of a pre-scaled
 //     x costs up to 1.35e-6 in a_i);
 //   * t = fma(negc, |d|^2, h' - m) then MUFU.EX2; two j's per packed FADD2/FFMA2;
-//   * lazy rescale: terms are summed per 16-j sub-chunk into a fresh fp32 pair; the sub-chunk's
-//     max t (FMNMX3) is checked once; if it exceeds TAU = 8 the sub-chunk is discarded, m is
+//   * lazy rescale: terms are summed per 16-j sub-chunk into a fresh fp32 pair; if that sum
+//     exceeds 2^16 (or overflows) the sub-chunk is discarded, m is
 //     set to the sub-chunk's exact max v (never m + t), s is rescaled in fp64 and the sub-chunk
 //     is recomputed -- rare (a few times per row);
 //   * fp32 partials are promoted to fp64 every 128 j; the output is finalised in fp64:
@@ -22,9 +22,19 @@
 
 namespace genred {
 
-constexpr float kTau = 8.0f;          // lazy-rescale threshold, log2 units
-constexpr int kSub = 8;               // record pairs per sub-chunk (16 j)
-constexpr int kPromote = 8;           // sub-chunks per fp64 promotion (128 j)
+// Lazy rescale: a sub-chunk is accepted while its fp32 sum of 2 kSub terms 2^(v - m) stays
+// <= kSumMax (or is not finite): every accepted term is then < 2^16, so the reference m may lag
+// the running max by up to 16 (log2) without overflow or loss of relative precision, and the
+// check costs one FMNMX + FSETP per row and sub-chunk instead of a max per pair.
+constexpr float kSumMax = 65536.0f;
+#ifndef GENRED_LSE_SUB
+#define GENRED_LSE_SUB 8
+#endif
+#ifndef GENRED_LSE_MINB
+#define GENRED_LSE_MINB 2
+#endif
+constexpr int kSub = GENRED_LSE_SUB;  // record pairs per sub-chunk (2 kSub j)
+constexpr int kPromote = 64 / kSub;   // sub-chunks per fp64 promotion (128 j)
 
 template <int D, bool HZ>
 struct LseCfg {
@@ -95,7 +105,7 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
 }
 
 template <int D, int R, bool HZ>
-__global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
+__global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const LseParams p) {
     using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -132,14 +142,12 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
         const float *tile = ring.acquire(k);
         for (int sc = 0; sc < Cfg::PAIRS / kSub; ++sc) {
             const float *base = tile + sc * kSub * RS;
-            float tm[R];
             float2 cs[R];
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                tm[r] = -INFINITY;
                 cs[r] = make_float2(0.f, 0.f);
             }
-#pragma unroll 4
+#pragma unroll
             for (int q = 0; q < kSub; ++q) {
                 float f[RS];
 #pragma unroll
@@ -166,13 +174,12 @@ __global__ void __launch_bounds__(kThreads, 2) lse_kernel(const LseParams p) {
                     }
                     const float2 hm = HZ ? dup2(-m[r]) : add2(add2(hhi, dup2(-m[r])), hlo);  // (h'-m)
                     const float2 t = fma2(q2, negc2, hm);          // v - m, log2 units
-                    tm[r] = max3(tm[r], t.x, t.y);
                     cs[r] = add2(cs[r], make_float2(ex2(t.x), ex2(t.y)));
                 }
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
-                if (tm[r] > kTau) {
+                if (!(fmaxf(cs[r].x, cs[r].y) <= kSumMax)) {          // also catches inf / NaN
                     // rare path (a few times per row): new reference m = exact max of v over the
                     // sub-chunk, fp64 rescale of the accumulated sum, sub-chunk recomputed
                     const LseRescale rs = lse_rescale<D, HZ, RS>(base, xr[r], negc, m[r], s64[r], s32[r]);
@@ -250,9 +257,12 @@ static int occ_lse() {
 
 // Rows per thread that stay spill-free within 112 registers.
 template <int D>
-constexpr int lse_rmax() { return D <= 3 ? 4 : 2; }
+#ifndef GENRED_LSE_R4
+#define GENRED_LSE_R4 1
+#endif
+constexpr int lse_rmax() { return (D <= 3 && GENRED_LSE_R4) ? 4 : 2; }
 
-int lse_rows_per_thread_max(int D) { return D <= 3 ? 4 : 2; }
+int lse_rows_per_thread_max(int D) { return (D <= 3 && GENRED_LSE_R4) ? 4 : 2; }
 
 template <int D>
 static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {

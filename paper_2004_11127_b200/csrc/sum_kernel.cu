@@ -29,7 +29,7 @@ template <int MODE, int D, int E>
 struct SumCfg {
     // record pair: 2D coordinates, then (MODE 0 only) the pair slot of w = -|y'|^2 used by the
     // expanded form, then 2E signal values; padded to a multiple of 16 bytes
-    static constexpr int BOFF = (MODE == 0) ? 2 * (D + 1) : 2 * D;
+    static constexpr int BOFF = (MODE != 3) ? 2 * (D + 1) : 2 * D;
     static constexpr int RS = ((BOFF + 2 * E) + 3) / 4 * 4;       // floats per record pair
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
@@ -43,7 +43,7 @@ struct SumCfg {
 
 struct SumParams {
     const float *x, *J, *g;
-    const uint32_t *geo;      // MODE 0: encoded bounding box (geo.cuh)
+    const uint32_t *geo;      // Gaussian modes: encoded bounding box (geo.cuh)
     int64_t M;
     int split;
     int64_t tiles_per_split, ntiles;
@@ -116,6 +116,16 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     float2 acc[R][NS > 0 ? NS : 1];
     float2 accg[R][NG > 0 ? NG : 1];
     double acc64[R][C];
+    // expanded gradient: G_i ~ x'_i S0_i - S_i with S0 = sum_j w_ij, S = sum_j w_ij y'_j; S0 is the
+    // Sum itself when MODE == 2 and E == 1 (w = e b), else it has its own accumulator
+    constexpr bool OWN_S0 = XP && NG > 0 && !(MODE == 2 && E == 1);
+    float2 s0[R];
+    double s064[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        s0[r] = make_float2(0.f, 0.f);
+        s064[r] = 0.0;
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -154,8 +164,31 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                     // FP32-pipe exp2 share (kPolyShare, off: see DESIGN.md Sec. 6 measurements)
                     if (POLY && r == R - 1 && hh == 0) ex = ex2_poly2(u);
                     else ex = make_float2(ex2(u.x), ex2(u.y));
+                    if constexpr (NG == 0) {
 #pragma unroll
-                    for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                        for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                    } else {
+                        float2 wt;
+                        if constexpr (E == 1) {
+                            wt = mul2(ex, bv[0]);                       // e b (g_i applied later)
+                        } else {
+                            float2 bg = mul2(bv[0], dup2(gr[r][0]));
+#pragma unroll
+                            for (int e = 1; e < E; ++e) bg = fma2(bv[e], dup2(gr[r][e]), bg);
+                            wt = mul2(ex, bg);                          // e <b, g_i>
+                        }
+                        if constexpr (MODE == 2 && E == 1) {
+                            acc[r][0] = add2(acc[r][0], wt);           // Sum == S0
+                        } else {
+                            if constexpr (MODE == 2) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                            }
+                            s0[r] = add2(s0[r], wt);
+                        }
+#pragma unroll
+                        for (int d = 0; d < D; ++d) accg[r][d] = fma2(wt, ny[d], accg[r][d]);   // w y'
+                    }
                 }
             } else {
 #pragma unroll
@@ -211,6 +244,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                 acc64[r][NS + c] += (double)accg[r][c].x + (double)accg[r][c].y;
                 accg[r][c] = make_float2(0.f, 0.f);
             }
+            if constexpr (OWN_S0) {
+                s064[r] += (double)s0[r].x + (double)s0[r].y;
+                s0[r] = make_float2(0.f, 0.f);
+            }
         }
     }
 
@@ -221,8 +258,15 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         if (i >= p.M) continue;
         if constexpr (XP) {
             const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
+            if constexpr (NG > 0) {
+                // sum_j w_ij (x'_i - y'_j) = x'_i S0_i - S_i  (the kernel's d' convention)
+                const double S0 = OWN_S0 ? s064[r] : acc64[r][0];
 #pragma unroll
-            for (int c = 0; c < NS; ++c) acc64[r][c] *= fac;
+                for (int c = 0; c < NG; ++c)
+                    acc64[r][NS + c] = 0.5 * (double)xr[r][c] * S0 - acc64[r][NS + c];
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc64[r][c] *= fac;
         }
         if (p.split > 1) {
             double *dst = p.part + ((int64_t)sp * p.M + i) * C;
@@ -251,7 +295,8 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 }
 
 template <int MODE, int D, int E, int R>
-__global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) sum_kernel(const SumParams p) {
+__global__ void __launch_bounds__(kThreads, ((MODE == 0 || MODE == 3) && D + E <= 4 && R == 4) ? 3 : 2)
+sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
@@ -264,7 +309,7 @@ __global__ void __launch_bounds__(kThreads, (MODE == 0 || MODE == 3) ? 3 : 2) su
     JRing<kStages> ring;
     ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
     const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
-    if constexpr (MODE == 0) {
+    if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
         if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, sp, geo);
         else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, sp, geo);

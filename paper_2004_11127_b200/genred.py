@@ -19,7 +19,7 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
-LIB_PATH = os.path.join(HERE, "libgenred.so")
+LIB_PATH = os.environ.get("GENRED_LIB") or os.path.join(HERE, "libgenred.so")
 HEADER = os.path.join(ROOT, "include", "genred.h")
 
 ABI_VERSION = 1

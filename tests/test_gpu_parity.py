@@ -443,3 +443,30 @@ def test_gauss_sum_expanded_and_direct_paths(G, case):
     assert plan["path"] == expect, plan
     o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
     assert_sum_parity(host(a), o, den, what=f"gauss {case}")
+
+
+@pytest.mark.parametrize("formula", ["gauss_gradx", "gauss_sum_gradx"])
+@pytest.mark.parametrize("case", ["expanded", "far_offset", "direct", "E2_g"])
+def test_gradient_expanded_and_direct_paths(G, formula, case):
+    """Gradient in the expanded form uses x' S0 - S (sum of w y'): checked against the oracle on
+    both sides of the device-side path decision."""
+    M, N, sigma, E = 2500, 3100, 0.5, 1
+    x = synth.gmm3(M, 71); y = synth.gmm3(N, 72)
+    if case == "far_offset":
+        x = (x - 500.0).astype(np.float32); y = (y - 500.0).astype(np.float32)
+    if case == "direct":
+        sigma = 0.06
+    if case == "E2_g":
+        E = 2
+    b = synth.signal(N, 73, E=E, signed=True)
+    g = synth.cotangent(M, 74, E=E)
+    res = G.eval(formula, "sum", dev(x), dev(y), dev(b), dev(g), scale=sigma)
+    assert G.last_plan()["path"] == (0 if case == "direct" else 2)
+    og, deng = oracle.gauss_gradx(x, y, b, g, sigma=sigma)
+    if formula == "gauss_sum_gradx":
+        s, gr = res
+        os_, dens = oracle.gauss_sum(x, y, b, sigma=sigma)
+        assert_sum_parity(host(s), os_, dens, what=f"fused sum {case}")
+    else:
+        gr = res
+    assert_sum_parity(host(gr), og, deng, what=f"{formula} grad {case}")
