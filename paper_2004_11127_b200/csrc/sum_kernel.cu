@@ -295,7 +295,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 }
 
 template <int MODE, int D, int E, int R>
-__global__ void __launch_bounds__(kThreads, ((MODE == 0 || MODE == 3) && D + E <= 4 && R == 4) ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, ((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ? 3 : 2)
 sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
