@@ -470,3 +470,26 @@ def test_gradient_expanded_and_direct_paths(G, formula, case):
     else:
         gr = res
     assert_sum_parity(host(gr), og, deng, what=f"{formula} grad {case}")
+
+
+# ------------------------------------------------------------------------------------------------
+# torch.autograd through libgenred (gradients in x, y and b)
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("E", [1, 2])
+def test_autograd_gauss_sum_all_inputs(G, E):
+    from paper_2004_11127_b200.autograd import gauss_sum
+    M, N, sigma = 1400, 2100, 0.5
+    x = synth.gmm3(M, 81); y = synth.uniform3(N, 82); b = synth.signal(N, 83, E=E, signed=True)
+    g = synth.cotangent(M, 84, E=E)
+    xt, yt, bt = (dev(a).requires_grad_(True) for a in (x, y, b))
+    a = gauss_sum(xt, yt, bt, sigma)
+    a.backward(dev(g))
+    o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+    assert_sum_parity(host(a), o, den, what="fwd")
+    ogx, dx = oracle.gauss_gradx(x, y, b, g, sigma=sigma)
+    ogy, dy = oracle.gauss_gradx(y, x, g, b, sigma=sigma)       # pinned in test_vjp_pins.py
+    ogb, db = oracle.gauss_sum(y, x, g, sigma=sigma)            # pinned in test_vjp_pins.py
+    assert_sum_parity(host(xt.grad), ogx, dx, what="grad x")
+    assert_sum_parity(host(yt.grad), ogy, dy, what="grad y")
+    assert_sum_parity(host(bt.grad), ogb, db, what="grad b")
