@@ -367,30 +367,55 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
     const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = blockIdx.x * 4 + wl;
     if (i >= M) return;
-    if (lane == 0) {
-        float bd[KP];
-        int32_t bj[KP];
-        float kth = INFINITY;
-        for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
-        for (int g = 0; g < n_groups; ++g) {
-            const float *gd = pd + ((int64_t)g * M + i) * KP;
-            const int32_t *gj = pj + ((int64_t)g * M + i) * KP;
-            for (int k = 0; k < KP; ++k) {
-                const int32_t j = gj[k];
-                if (j < 0) break;
-                const float d = gd[k];
-                if (d < kth || (d == kth && (uint32_t)j < (uint32_t)bj[KP - 1])) {
-                    int pos = KP - 1;
-                    while (pos > 0 && (d < bd[pos - 1] || (d == bd[pos - 1] && j < bj[pos - 1]))) {
-                        bd[pos] = bd[pos - 1]; bj[pos] = bj[pos - 1]; --pos;
-                    }
-                    bd[pos] = d; bj[pos] = j;
-                    kth = bd[KP - 1];
-                } else {
-                    break;                                  // lists are sorted
-                }
+    // (1) each lane merges the group lists g = lane, lane + 32, ... into a sorted register list
+    float bd[KP];
+    int32_t bj[KP];
+    float kth = INFINITY;
+#pragma unroll
+    for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
+    for (int g = lane; g < n_groups; g += 32) {
+        const float *gd = pd + ((int64_t)g * M + i) * KP;
+        const int32_t *gj = pj + ((int64_t)g * M + i) * KP;
+        for (int k = 0; k < KP; ++k) {
+            const int32_t j = gj[k];
+            if (j < 0) break;
+            const float d = gd[k];
+            if (!(d < kth || (d == kth && (uint32_t)j < (uint32_t)bj[KP - 1]))) break;   // sorted
+            kp_insert<KP>(bd, bj, d, j, kth);
+        }
+    }
+    // (2) warp-wide K'-way merge of the 32 lane lists: K' rounds of a lexicographic (d, j)
+    //     argmin over the lanes' heads; the winning lane pops its head
+    {
+        int head = 0;
+        for (int k = 0; k < KP; ++k) {
+            float hd = INFINITY;
+            int32_t hj = -1;
+#pragma unroll
+            for (int q = 0; q < KP; ++q)
+                if (q == head) { hd = bd[q]; hj = bj[q]; }
+            if (hj < 0) hd = INFINITY;
+            float wd = hd;
+            int32_t wj = hj < 0 ? INT32_MAX : hj;
+            int wl_ = lane;
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) {
+                const float od = __shfl_xor_sync(0xffffffffu, wd, o);
+                const int32_t oj = __shfl_xor_sync(0xffffffffu, wj, o);
+                const int ol = __shfl_xor_sync(0xffffffffu, wl_, o);
+                if (od < wd || (od == wd && oj < wj)) { wd = od; wj = oj; wl_ = ol; }
+            }
+            if (lane == wl_) ++head;
+            if (lane == 0) {
+                s_d[wl][k] = wd;
+                s_j[wl][k] = wj == INT32_MAX ? -1 : wj;
             }
         }
+    }
+    __syncwarp();
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < KP; ++k) { bd[k] = s_d[wl][k]; bj[k] = s_j[wl][k]; }
         // margin certificate (R17): every true top-K member is among the K' screened candidates
         // when d~_(K') - d~_(K) > 2 delta, delta = gamma |x| max|y| + 2^-22 (|x|^2 + max|y|^2)
         const float ymax = __uint_as_float(*maxnorm_bits);
@@ -402,7 +427,6 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
             const int slot = atomicAdd(fb_count, 1);
             fb_rows[slot] = (int32_t)i;
         }
-        for (int k = 0; k < KP; ++k) { s_d[wl][k] = bd[k]; s_j[wl][k] = bj[k]; }
     }
     __syncwarp();
     // exact fp64 distances of the K' candidates (direct differences, never expanded)
@@ -547,15 +571,50 @@ fallback_kernel(const float *__restrict__ x, const float *__restrict__ y, int64_
             is_last = atomicAdd(done + f, 1u) == (unsigned)(G - 1);
         }
         __syncthreads();
-        if (is_last && threadIdx.x == 0) {
+        if (is_last) {
+            // block-parallel K-way merge of the G partial lists: thread t owns lists t, t + 256,
+            // ...; K rounds of a block-wide lexicographic (d, j) argmin over the list heads
             __threadfence();
-            double md[FB_LIST];
-            int32_t mj[FB_LIST];
-            fb_merge(part_d + (int64_t)f * G * FB_LIST, part_j + (int64_t)f * G * FB_LIST, G, FB_LIST,
-                     K, md, mj);
+            __shared__ double rd[FB_WARPS];
+            __shared__ int32_t rj[FB_WARPS];
+            __shared__ int rq[FB_WARPS];
+            const double *LD = part_d + (int64_t)f * G * FB_LIST;
+            const int32_t *LJ = part_j + (int64_t)f * G * FB_LIST;
+            int heads[(FB_GRID + FB_THREADS - 1) / FB_THREADS];
+            for (int u = 0; u * FB_THREADS + (int)threadIdx.x < G; ++u) heads[u] = 0;
+            const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
             for (int k = 0; k < K; ++k) {
-                dist[i * K + k] = mj[k] >= 0 ? (float)md[k] : INFINITY;
-                idx[i * K + k] = mj[k] >= 0 ? (int64_t)mj[k] + j_offset : -1;
+                double bd = INFINITY;
+                int32_t bj = INT32_MAX;
+                int bq = -1;
+                for (int u = 0; u * FB_THREADS + (int)threadIdx.x < G; ++u) {
+                    const int q = u * FB_THREADS + threadIdx.x;
+                    if (heads[u] >= FB_LIST) continue;
+                    const int32_t j = LJ[q * FB_LIST + heads[u]];
+                    if (j < 0) continue;
+                    const double d = LD[q * FB_LIST + heads[u]];
+                    if (d < bd || (d == bd && j < bj)) { bd = d; bj = j; bq = q; }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    const double od = __shfl_xor_sync(0xffffffffu, bd, o);
+                    const int32_t oj = __shfl_xor_sync(0xffffffffu, bj, o);
+                    const int oq = __shfl_xor_sync(0xffffffffu, bq, o);
+                    if (od < bd || (od == bd && oj < bj)) { bd = od; bj = oj; bq = oq; }
+                }
+                if (lane == 0) { rd[w] = bd; rj[w] = bj; rq[w] = bq; }
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    for (int q = 1; q < FB_WARPS; ++q)
+                        if (rd[q] < rd[0] || (rd[q] == rd[0] && rj[q] < rj[0])) { rd[0] = rd[q]; rj[0] = rj[q]; rq[0] = rq[q]; }
+                    const bool ok = rq[0] >= 0;
+                    dist[i * K + k] = ok ? (float)rd[0] : INFINITY;
+                    idx[i * K + k] = ok ? (int64_t)rj[0] + j_offset : -1;
+                }
+                __syncthreads();
+                const int win = rq[0];
+                if (win >= 0 && win % FB_THREADS == (int)threadIdx.x) heads[win / FB_THREADS]++;
+                __syncthreads();
             }
         }
         __syncthreads();
