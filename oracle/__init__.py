@@ -5,5 +5,5 @@ may import this package.  The product path (paper_2004_11127_b200) never does.
 """
 from .oracle import (  # noqa: F401
     build, lib_path, num_threads,
-    gauss_sum, gauss_gradx, lse, argkmin, sqdist_sum,
+    gauss_sum, gauss_gradx, lse, argkmin, sqdist_sum, softmax_grad,
 )

@@ -21,6 +21,7 @@
  *                                                                          PAPER.md:85, 134 (R5)
  *   oracle_argkmin      O4  K smallest (|x_i-y_j|^2, j) in lexicographic order   PAPER.md:85, 134 (R7-R9)
  *   oracle_sqdist_sum   O5  sum_j |x_i-y_j|^2 b_j  (test combination)
+ *   oracle_softmax_grad O6  softmax-weighted sums / gradients (LSE backward)
  *
  * Every function takes an optional row subset (rows != NULL: evaluate only those rows, outputs
  * indexed by position in `rows`) so large configurations can be checked on a seeded sample.
@@ -221,5 +222,48 @@ void oracle_sqdist_sum(int64_t M, int64_t N, int D, int E,
         }
         free(acc);
         free(den);
+    }
+}
+
+/* O6 (the backward of O3): softmax-weighted reductions
+ *     p_ij   = exp(-|x_i - y_j|^2 / eps + alpha_i + beta_j)
+ *     S_i    = sum_j sig_j p_ij                                   (out_sum, M)
+ *     G_i[d] = coef_i sum_j sig_j p_ij (-2/eps) (x_i[d] - y_j[d])  (out_grad, M x D)
+ * With alpha_i = -a_i (a = O3's LSE), beta = h, sig = coef = 1: S_i = 1 and G_i = da_i/dx_i
+ * (the gradient of a reduction is another reduction).  NULL alpha/beta -> 0,
+ * NULL sig/coef -> 1.  Denominators: sum_j |sig_j| p_ij and coef-scaled sum of |terms|. */
+void oracle_softmax_grad(int64_t M, int64_t N, int D, double eps,
+                         const double *x, const double *y, const double *alpha, const double *beta,
+                         const double *sig, const double *coef,
+                         const int64_t *rows, int64_t nrows,
+                         double *out_sum, double *out_grad, double *den_sum, double *den_grad) {
+    int64_t R = rows ? nrows : M;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t i = row_of(rows, r);
+        nsum s = {0.0, 0.0}, sd = {0.0, 0.0};
+        nsum *g = calloc((size_t)D, sizeof(nsum));
+        nsum *gd = calloc((size_t)D, sizeof(nsum));
+        double c = coef ? coef[i] : 1.0;
+        for (int64_t j = 0; j < N; ++j) {
+            double p = exp(-sqdist(x + i * D, y + j * D, D) / eps + (alpha ? alpha[i] : 0.0) +
+                           (beta ? beta[j] : 0.0));
+            double w = (sig ? sig[j] : 1.0) * p;
+            nsum_add(&s, w);
+            nsum_add(&sd, fabs(w));
+            for (int d = 0; d < D; ++d) {
+                double t = c * w * (-2.0 / eps) * (x[i * D + d] - y[j * D + d]);
+                nsum_add(&g[d], t);
+                nsum_add(&gd[d], fabs(t));
+            }
+        }
+        out_sum[r] = nsum_get(&s);
+        if (den_sum) den_sum[r] = nsum_get(&sd);
+        for (int d = 0; d < D; ++d) {
+            out_grad[r * D + d] = nsum_get(&g[d]);
+            if (den_grad) den_grad[r * D + d] = nsum_get(&gd[d]);
+        }
+        free(g);
+        free(gd);
     }
 }

@@ -327,3 +327,36 @@ def test_empty_reduction_axis():
     assert np.all(l == -math.inf)
     d, j = oracle.argkmin(x, y, 2)
     assert np.all(j == -1) and np.all(d == math.inf)
+
+
+# --------------------------------------------------------------------------------------------
+# O6 (LSE backward): pinned by the softmax identity and finite differences
+# of O3 in x, y and h
+# --------------------------------------------------------------------------------------------
+
+def test_softmax_grad_is_lse_gradient():
+    rng = np.random.default_rng(31)
+    M, N, D, eps = 9, 40, 3, 0.3
+    x = rng.random((M, D)); y = rng.random((N, D)); h = rng.standard_normal(N)
+    g = rng.standard_normal(M)
+    a, _ = oracle.lse(x, y, h, eps=eps)
+    S, G, dS, dG = oracle.softmax_grad(x, y, alpha=-a, beta=h, eps=eps)
+    np.testing.assert_allclose(S, 1.0, rtol=1e-13)                 # softmax weights sum to 1
+    step = 1e-6
+    for d in range(D):                                              # d a_i / d x_i
+        xp = x.copy(); xp[:, d] += step
+        xm = x.copy(); xm[:, d] -= step
+        fd = (oracle.lse(xp, y, h, eps=eps)[0] - oracle.lse(xm, y, h, eps=eps)[0]) / (2 * step)
+        assert np.all(np.abs(G[:, d] - fd) <= 1e-7 * dG[:, d] + 1e-9)
+    # transposed: d/dh_j sum_i g_i a_i = sum_i g_i p_ij ;  d/dy_j = G of the swapped call
+    Sh, Gy, dSh, dGy = oracle.softmax_grad(y, x, alpha=h, beta=-a, sig=g, eps=eps)
+    for j in (0, 7, 39):
+        hp = h.copy(); hp[j] += step
+        hm = h.copy(); hm[j] -= step
+        fd = (g * (oracle.lse(x, y, hp, eps=eps)[0] - oracle.lse(x, y, hm, eps=eps)[0])).sum() / (2 * step)
+        assert abs(Sh[j] - fd) <= 1e-7 * dSh[j] + 1e-9
+        for d in range(D):
+            yp = y.copy(); yp[j, d] += step
+            ym = y.copy(); ym[j, d] -= step
+            fd = (g * (oracle.lse(x, yp, h, eps=eps)[0] - oracle.lse(x, ym, h, eps=eps)[0])).sum() / (2 * step)
+            assert abs(Gy[j, d] - fd) <= 1e-7 * dGy[j, d] + 1e-9
