@@ -37,7 +37,7 @@
 extern "C" {
 #endif
 
-#define GENRED_ABI_VERSION 1
+#define GENRED_ABI_VERSION 2
 
 typedef struct genred_ctx genred_ctx;
 
@@ -50,18 +50,27 @@ typedef enum {
     GENRED_E_CUDA = 5          /* a CUDA runtime call or launch failed (message has the reason) */
 } genred_status;
 
-/* Formulas F (readings R1, R2, R5, R10 in DESIGN.md):
+/* Formulas F (readings R1, R2, R5, R10 in DESIGN.md; LSE_GRAD: SURVEY 8(f) row 2):
  *   GAUSS           F_ij = exp(-|x_i - y_j|^2 / sigma^2) * b_j                 (E outputs)
  *   GAUSS_GRADX     F_ij = d/dx_i of the above, contracted with the cotangent g_i:
  *                   (-2/sigma^2) (x_i - y_j) exp(-|x_i-y_j|^2/sigma^2) <b_j, g_i>  (D outputs)
  *   GAUSS_SUM_GRADX both of the above in one pass (out: M x E sum, out_grad: M x D gradient)
  *   SQDIST          F_ij = |x_i - y_j|^2; under LSE: F_ij = -|x_i - y_j|^2 / eps + h_j,
- *                   with h = b (N values, E = 1; NULL means h = 0).                          */
+ *                   with h = b (N values, E = 1; NULL means h = 0).
+ *   LSE_GRAD        the backward of the LSE reduction: with
+ *                   p_ij = exp(-|x_i - y_j|^2/eps + alpha_i + beta_j) (alpha = row_shift,
+ *                   beta = col_shift, fp64, NULL = 0; b = sig (N), g = coef (M), NULL = 1):
+ *                   out = S_i = sum_j sig_j p_ij (M values) and
+ *                   out_grad = coef_i (-2/eps) sum_j sig_j p_ij (x_i - y_j) (M x D, fp32).
+ *                   alpha = -a (the forward LSE), beta = h gives S = 1 and out_grad = da/dx;
+ *                   rows y, reduced x, alpha = h, beta = -a, sig = g gives dL/dh and dL/dy.
+ *                   Not max-shifted: the caller keeps alpha_i + beta_j - |x-y|^2/eps <= ~80.    */
 typedef enum {
     GENRED_GAUSS = 0,
     GENRED_GAUSS_GRADX = 1,
     GENRED_SQDIST = 2,
-    GENRED_GAUSS_SUM_GRADX = 3
+    GENRED_GAUSS_SUM_GRADX = 3,
+    GENRED_LSE_GRAD = 4
 } genred_formula;
 
 /* Reductions:
@@ -77,7 +86,7 @@ typedef enum { GENRED_MEM_DEVICE = 0, GENRED_MEM_HOST = 1 } genred_memory;
 /* Supported (formula, reduction) pairs and shapes:
  *   (GAUSS, SUM), (GAUSS_GRADX, SUM), (GAUSS_SUM_GRADX, SUM): 1 <= D <= 8, 1 <= E <= 4
  *   (SQDIST, SUM): 1 <= D <= 8, 1 <= E <= 4 (closed-form test combination)
- *   (SQDIST, LSE): 1 <= D <= 8, E == 1
+ *   (SQDIST, LSE), (LSE_GRAD, SUM): 1 <= D <= 8, E == 1
  *   (SQDIST, ARGKMIN): E == 1 and either 1 <= D <= 16, 1 <= K <= 32 (FP32 path), or
  *                      17 <= D <= 16384, 1 <= K <= 28 (tcgen05 3xTF32 screening + exact fp64
  *                      re-rank of the K' best candidates, PAPER.md:97 k-NN)
@@ -105,6 +114,8 @@ typedef struct {
     double  *lse_state;      /* optional, LSE only: M x 2 (m_i in log2 units, s_i) so that
                                 a_i = ln2 * (m_i + log2 s_i); input of genred_combine_lse      */
     int64_t  j_offset;       /* added to every reported index (j-sharded evaluation) */
+    const double *row_shift; /* LSE_GRAD: alpha (M values) */
+    const double *col_shift; /* LSE_GRAD: beta (N values) */
 } genred_args;
 
 /* Library-level information. */

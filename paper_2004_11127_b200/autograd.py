@@ -46,3 +46,45 @@ class GaussSum(torch.autograd.Function):
 def gauss_sum(x, y, b, sigma: float):
     """Differentiable a_i = sum_j exp(-|x_i - y_j|^2 / sigma^2) b_j (all three inputs)."""
     return GaussSum.apply(x, y, b, sigma)
+
+
+class LogSumExp(torch.autograd.Function):
+    """a = LogSumExp.apply(x, y, h, eps): a_i = log sum_j exp(-|x_i - y_j|^2/eps + h_j) (fp64 out).
+
+    Backward = two GENRED_LSE_GRAD reductions with the saved a as the
+    max shift (softmax weights p_ij = exp(F_ij - a_i), never above 1):
+        dL/dx_i = g_i sum_j p_ij (-2/eps)(x_i - y_j)            rows x, alpha = -a, beta = h
+        dL/dh_j = sum_i g_i p_ij, dL/dy_j = sum_i g_i p_ij (-2/eps)(y_j - x_i)
+                                                                rows y, alpha = h, beta = -a, sig = g
+    """
+
+    @staticmethod
+    def forward(ctx, x, y, h, eps: float):
+        x, y = x.contiguous(), y.contiguous()
+        h = None if h is None else h.contiguous().to(torch.float32)
+        a = genred.eval("sqdist", "lse", x, y, h, scale=float(eps), out_dtype="float64")
+        ctx.save_for_backward(x, y, h if h is not None else torch.empty(0, device=x.device), a)
+        ctx.has_h = h is not None
+        ctx.eps = float(eps)
+        return a
+
+    @staticmethod
+    def backward(ctx, g):
+        x, y, h, a = ctx.saved_tensors
+        h = h if ctx.has_h else None
+        g32 = g.contiguous().to(torch.float32)
+        neg_a = (-a).contiguous()                        # the max shift (argument marshalling)
+        h64 = None if h is None else h.to(torch.float64).contiguous()
+        gx = gy = gh = None
+        if ctx.needs_input_grad[0]:
+            _, gx = genred.eval("lse_grad", "sum", x, y, None, g32, scale=ctx.eps,
+                                row_shift=neg_a, col_shift=h64)
+        if ctx.needs_input_grad[1] or ctx.needs_input_grad[2]:
+            gh, gy = genred.eval("lse_grad", "sum", y, x, g32, None, scale=ctx.eps,
+                                 row_shift=h64, col_shift=neg_a)
+        return gx, gy, (gh if ctx.has_h else None), None
+
+
+def logsumexp(x, y, h, eps: float):
+    """Differentiable a_i = log sum_j exp(-|x_i - y_j|^2 / eps + h_j) (in x, y and h)."""
+    return LogSumExp.apply(x, y, h, eps)

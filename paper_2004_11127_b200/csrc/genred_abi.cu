@@ -68,13 +68,14 @@ genred_status validate(const genred_args *a, std::string &msg) {
         (f == GENRED_GAUSS || f == GENRED_GAUSS_GRADX || f == GENRED_GAUSS_SUM_GRADX || f == GENRED_SQDIST);
     const bool lse_pair = r == GENRED_LSE && f == GENRED_SQDIST;
     const bool argk_pair = r == GENRED_ARGKMIN && f == GENRED_SQDIST;
-    if (!sum_pair && !lse_pair && !argk_pair) {
+    const bool smg_pair = r == GENRED_SUM && f == GENRED_LSE_GRAD;
+    if (!sum_pair && !lse_pair && !argk_pair && !smg_pair) {
         msg = "unsupported (formula, reduction) pair"; return GENRED_E_UNSUPPORTED;
     }
     if (sum_pair && (a->D > 8 || a->E > 4)) {
         msg = "Sum formulas support 1 <= D <= 8 and 1 <= E <= 4"; return GENRED_E_UNSUPPORTED;
     }
-    if (lse_pair && (a->D > 8 || a->E != 1)) {
+    if ((lse_pair || smg_pair) && (a->D > 8 || a->E != 1)) {
         msg = "log-sum-exp supports 1 <= D <= 8 and E == 1 (scalar formula)"; return GENRED_E_UNSUPPORTED;
     }
     if (argk_pair) {
@@ -86,7 +87,7 @@ genred_status validate(const genred_args *a, std::string &msg) {
         if (a->N > (int64_t)INT32_MAX - kTileJ) { msg = "ArgKMin requires N < 2^31"; return GENRED_E_SHAPE; }
         if (a->out_dtype != GENRED_F32) { msg = "ArgKMin distances are fp32 (out_dtype F32)"; return GENRED_E_INVALID; }
     }
-    if ((f == GENRED_GAUSS || f == GENRED_GAUSS_GRADX || f == GENRED_GAUSS_SUM_GRADX || lse_pair) &&
+    if ((f == GENRED_GAUSS || f == GENRED_GAUSS_GRADX || f == GENRED_GAUSS_SUM_GRADX || lse_pair || smg_pair) &&
         !(isfinite(a->scale) && a->scale > 0.0)) {
         msg = "scale (sigma or eps) must be finite and > 0"; return GENRED_E_INVALID;
     }
@@ -97,7 +98,7 @@ genred_status validate(const genred_args *a, std::string &msg) {
         if (!a->out) { msg = "out is NULL"; return GENRED_E_INVALID; }
         if (a->N > 0 && !a->x) { msg = "x is NULL"; return GENRED_E_INVALID; }
         if (argk_pair && !a->out_idx) { msg = "out_idx is NULL"; return GENRED_E_INVALID; }
-        if (f == GENRED_GAUSS_SUM_GRADX && !a->out_grad) { msg = "out_grad is NULL"; return GENRED_E_INVALID; }
+        if ((f == GENRED_GAUSS_SUM_GRADX || smg_pair) && !a->out_grad) { msg = "out_grad is NULL"; return GENRED_E_INVALID; }
     }
     if (a->N > 0 && a->M > 0 && !a->y) { msg = "y is NULL"; return GENRED_E_INVALID; }
     const void *fp[] = {a->x, a->y, a->b, a->g, a->out_grad};
@@ -106,8 +107,9 @@ genred_status validate(const genred_args *a, std::string &msg) {
     if (a->out && !aligned(a->out, a->out_dtype == GENRED_F64 ? 8 : 4)) {
         msg = "out is misaligned for its dtype"; return GENRED_E_INVALID;
     }
-    if ((a->out_idx && !aligned(a->out_idx, 8)) || (a->lse_state && !aligned(a->lse_state, 8))) {
-        msg = "out_idx / lse_state must be 8-byte aligned"; return GENRED_E_INVALID;
+    if ((a->out_idx && !aligned(a->out_idx, 8)) || (a->lse_state && !aligned(a->lse_state, 8)) ||
+        (a->row_shift && !aligned(a->row_shift, 8)) || (a->col_shift && !aligned(a->col_shift, 8))) {
+        msg = "out_idx / lse_state / row_shift / col_shift must be 8-byte aligned"; return GENRED_E_INVALID;
     }
     msg.clear();
     return GENRED_OK;
@@ -120,6 +122,7 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
     int n = 1;
     if (kind == 0) n = sum_occupancy(a, b, c, R);
     else if (kind == 1) n = lse_occupancy(a, R);
+    else if (kind == 3) n = softmax_grad_occupancy(a, R);
     else n = argk_occupancy(a, b, R);
     ctx->occ[key] = n;
     return n;
@@ -238,7 +241,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     if (N == 0) {                                               // neutral outputs (R11)
         int kind, C = 0, K = 0;
         if (red == GENRED_SUM) {
-            if (f == GENRED_GAUSS_SUM_GRADX) { kind = 1; C = E; K = D; }
+            if (f == GENRED_GAUSS_SUM_GRADX || f == GENRED_LSE_GRAD) { kind = 1; C = E; K = D; }
             else { kind = 0; C = (f == GENRED_GAUSS_GRADX) ? D : E; }
         } else if (red == GENRED_LSE) kind = 2;
         else { kind = 3; K = a->K; }
@@ -246,6 +249,44 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (e != cudaSuccess) return cuda_fail(ctx, e, "fill kernel");
         ctx->launches += 1;
         ctx->plan.kernels = 1;
+        return GENRED_OK;
+    }
+
+    if (f == GENRED_LSE_GRAD) {                                   // LSE backward (8(f) row 2)
+        const int rmax = sm_rows_per_thread_max(D);
+        Plan pl = make_plan(ctx, a, 3, rmax, D, 0, 0);
+        const int RS = softmax_record_stride(D);
+        const int64_t npairs = pl.ntiles * (kTileJ / 2);
+        const int C = 1 + D;
+        const size_t jbytes = al256((size_t)npairs * RS * 4);
+        const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes);
+        if (s != GENRED_OK) return s;
+        float *J = (float *)ctx->scratch;
+        double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
+        e = launch_pack_softmax(a->y, a->b, a->col_shift, N, D, npairs, J, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
+        SmLaunch L;
+        L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.coef = a->g; L.alpha = a->row_shift; L.M = M;
+        L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+        L.negc = (float)(-kLog2e / a->scale); L.scale_grad = -2.0 / a->scale;
+        L.out = a->out; L.out_f64 = out_f64; L.out_grad = a->out_grad; L.part = part;
+        int ctas = 0;
+        prof_event(ctx, true, st);
+        e = launch_softmax_grad(L, st, &ctas);
+        prof_event(ctx, false, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "softmax-grad kernel");
+        int kernels = 2;
+        if (pl.split > 1) {
+            e = launch_sum_finalize(part, pl.split, M, C, 1, a->g, 1, 1.0, L.scale_grad, 2, a->out,
+                                    out_f64, a->out_grad, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "finalize kernel");
+            kernels++;
+        }
+        ctx->launches += kernels;
+        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
         return GENRED_OK;
     }
 
@@ -410,7 +451,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
 
 // Byte sizes of every operand, for host-pointer staging.
 struct Sizes {
-    size_t x, y, b, g, out, grad, idx, state;
+    size_t x, y, b, g, out, grad, idx, state, rs, cs;
 };
 Sizes operand_sizes(const genred_args *a) {
     Sizes z{};
@@ -418,14 +459,17 @@ Sizes operand_sizes(const genred_args *a) {
     z.x = M * a->D * 4;
     z.y = N * a->D * 4;
     const bool lse = a->reduction == GENRED_LSE, argk = a->reduction == GENRED_ARGKMIN;
-    z.b = a->b ? (lse ? N * 4 : N * a->E * 4) : 0;
+    const bool smg = a->formula == GENRED_LSE_GRAD;
+    z.b = a->b ? ((lse || smg) ? N * 4 : N * a->E * 4) : 0;
+    z.rs = a->row_shift ? M * 8 : 0;
+    z.cs = a->col_shift ? N * 8 : 0;
     z.g = a->g ? M * a->E * 4 : 0;
     const size_t es = a->out_dtype == GENRED_F64 ? 8 : 4;
     if (argk) z.out = M * a->K * 4;
-    else if (lse) z.out = M * es;
+    else if (lse || smg) z.out = M * es;
     else if (a->formula == GENRED_GAUSS_GRADX) z.out = M * a->D * es;
     else z.out = M * a->E * es;
-    z.grad = a->formula == GENRED_GAUSS_SUM_GRADX ? M * a->D * 4 : 0;
+    z.grad = (a->formula == GENRED_GAUSS_SUM_GRADX || smg) ? M * a->D * 4 : 0;
     z.idx = argk ? M * a->K * 8 : 0;
     z.state = (lse && a->lse_state) ? M * 16 : 0;
     return z;
@@ -514,21 +558,23 @@ genred_status genred_eval(genred_ctx *ctx, const genred_args *args, void *stream
     } else {
         // Host pointers: stage through context-owned device buffers, H2D -> eval -> D2H.
         Sizes z = operand_sizes(args);
-        size_t off[8], tot = 0;
-        size_t sz[8] = {z.x, z.y, z.b, z.g, z.out, z.grad, z.idx, z.state};
-        for (int k = 0; k < 8; ++k) { off[k] = tot; tot += al256(sz[k]); }
+        size_t off[10], tot = 0;
+        size_t sz[10] = {z.x, z.y, z.b, z.g, z.out, z.grad, z.idx, z.state, z.rs, z.cs};
+        for (int k = 0; k < 10; ++k) { off[k] = tot; tot += al256(sz[k]); }
         s = ensure(ctx, &ctx->stage, &ctx->stage_cap, tot + 256);
         if (s == GENRED_OK) {
             char *base = (char *)ctx->stage;
             genred_args d = *args;
             d.memory = GENRED_MEM_DEVICE;
-            const void *src[4] = {args->x, args->y, args->b, args->g};
-            const void **dst[4] = {(const void **)&d.x, (const void **)&d.y, (const void **)&d.b,
-                                   (const void **)&d.g};
-            for (int k = 0; k < 4 && s == GENRED_OK; ++k) {
-                if (!src[k] || sz[k] == 0) continue;
-                *dst[k] = base + off[k];
-                cudaError_t e = cudaMemcpyAsync(base + off[k], src[k], sz[k], cudaMemcpyHostToDevice, st);
+            const void *src[6] = {args->x, args->y, args->b, args->g, args->row_shift, args->col_shift};
+            const void **dst[6] = {(const void **)&d.x, (const void **)&d.y, (const void **)&d.b,
+                                   (const void **)&d.g, (const void **)&d.row_shift,
+                                   (const void **)&d.col_shift};
+            const int slot[6] = {0, 1, 2, 3, 8, 9};
+            for (int k = 0; k < 6 && s == GENRED_OK; ++k) {
+                if (!src[k] || sz[slot[k]] == 0) continue;
+                *dst[k] = base + off[slot[k]];
+                cudaError_t e = cudaMemcpyAsync(base + off[slot[k]], src[k], sz[slot[k]], cudaMemcpyHostToDevice, st);
                 if (e != cudaSuccess) s = cuda_fail(ctx, e, "H2D copy");
             }
             d.out = args->out ? base + off[4] : nullptr;

@@ -82,6 +82,27 @@ cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas);
 int argk_occupancy(int D, int K, int R);
 int argk_rows_per_thread(int K);
 
+// Softmax-weighted sums / gradients (the LSE backward, softmax_grad_kernel.cu).
+struct SmLaunch {
+    int D, R;
+    const float *x, *J, *coef;
+    const double *alpha;
+    int64_t M;
+    int split;
+    int64_t tiles_per_split, ntiles;
+    float negc;
+    double scale_grad;
+    void *out; int out_f64;
+    float *out_grad;
+    double *part;
+};
+cudaError_t launch_softmax_grad(const SmLaunch &a, cudaStream_t st, int *ctas);
+int softmax_grad_occupancy(int D, int R);
+int sm_rows_per_thread_max(int D);
+int softmax_record_stride(int D);
+cudaError_t launch_pack_softmax(const float *y, const float *sig, const double *beta, int64_t N,
+                                int D, int64_t npairs, float *J, cudaStream_t st);
+
 // Large-D ArgKMin on the tensor cores (knn_tc.cu): 3xTF32 tcgen05 screening + exact re-rank.
 struct KnnTcLaunch {
     const float *x, *y;

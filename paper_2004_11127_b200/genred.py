@@ -22,11 +22,11 @@ ROOT = os.path.dirname(HERE)
 LIB_PATH = os.environ.get("GENRED_LIB") or os.path.join(HERE, "libgenred.so")
 HEADER = os.path.join(ROOT, "include", "genred.h")
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 OK, E_INVALID, E_UNSUPPORTED, E_SHAPE, E_NOMEM, E_CUDA = range(6)
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_SHAPE", 4: "E_NOMEM", 5: "E_CUDA"}
 
-FORMULAS = {"gauss": 0, "gauss_gradx": 1, "sqdist": 2, "gauss_sum_gradx": 3}
+FORMULAS = {"gauss": 0, "gauss_gradx": 1, "sqdist": 2, "gauss_sum_gradx": 3, "lse_grad": 4}
 REDUCTIONS = {"sum": 0, "lse": 1, "argkmin": 2}
 F32, F64 = 0, 1
 MEM_DEVICE, MEM_HOST = 0, 1
@@ -50,6 +50,7 @@ class Args(ctypes.Structure):
         ("g", ctypes.c_void_p), ("out", ctypes.c_void_p), ("out_dtype", ctypes.c_int32),
         ("pad0", ctypes.c_int32), ("out_grad", ctypes.c_void_p), ("out_idx", ctypes.c_void_p),
         ("lse_state", ctypes.c_void_p), ("j_offset", ctypes.c_int64),
+        ("row_shift", ctypes.c_void_p), ("col_shift", ctypes.c_void_p),
     ]
 
 
@@ -179,7 +180,7 @@ def _check(t, name, dtype_ok=("float32",)):
 
 def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1.0, K: int = 1,
          out=None, out_dtype: str = "float32", out_grad=None, out_idx=None, lse_state=None,
-         split_j: int = 0, j_offset: int = 0, stream=None):
+         split_j: int = 0, j_offset: int = 0, stream=None, row_shift=None, col_shift=None):
     """Evaluate a_i = Reduction_j F(x_i, y_j) (Eq. 1) through genred_eval.
 
     x: (M, D), y: (N, D), b: (N, E) (or h: (N,) for LSE), g: (M, E); fp32, contiguous, all CUDA
@@ -192,7 +193,9 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     N = int(y.shape[0])
     f, r = FORMULAS[formula], REDUCTIONS[reduction]
     E = 1
-    if b is not None and r != REDUCTIONS["lse"]:
+    if f == FORMULAS["lse_grad"]:
+        pass
+    elif b is not None and r != REDUCTIONS["lse"]:
         E = int(b.shape[1]) if b.ndim == 2 else 1
     elif g is not None:
         E = int(g.shape[1]) if g.ndim == 2 else 1
@@ -202,7 +205,7 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     if out is None:
         if r == REDUCTIONS["argkmin"]:
             oshape, odtype = (M, K), "float32"
-        elif r == REDUCTIONS["lse"]:
+        elif r == REDUCTIONS["lse"] or f == FORMULAS["lse_grad"]:
             oshape, odtype = (M,), out_dtype
         elif f == FORMULAS["gauss_gradx"]:
             oshape, odtype = (M, D), out_dtype
@@ -213,7 +216,7 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
         else:
             import torch
             out = torch.empty(oshape, dtype=getattr(torch, odtype), device=x.device)
-    if f == FORMULAS["gauss_sum_gradx"] and out_grad is None:
+    if f in (FORMULAS["gauss_sum_gradx"], FORMULAS["lse_grad"]) and out_grad is None:
         if host:
             out_grad = np.empty((M, D), np.float32)
         else:
@@ -236,6 +239,7 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     a.out, a.out_dtype = _ptr(out), odt
     a.out_grad, a.out_idx, a.lse_state = _ptr(out_grad), _ptr(out_idx), _ptr(lse_state)
     a.j_offset = int(j_offset)
+    a.row_shift, a.col_shift = _ptr(row_shift), _ptr(col_shift)
     if host:
         dev, sptr = None, None
     else:
@@ -249,7 +253,7 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
         raise GenredError(st, load().genred_last_error(ctx).decode())
     if r == REDUCTIONS["argkmin"]:
         return out, out_idx
-    if f == FORMULAS["gauss_sum_gradx"]:
+    if f in (FORMULAS["gauss_sum_gradx"], FORMULAS["lse_grad"]):
         return out, out_grad
     return out
 

@@ -493,3 +493,48 @@ def test_autograd_gauss_sum_all_inputs(G, E):
     assert_sum_parity(host(xt.grad), ogx, dx, what="grad x")
     assert_sum_parity(host(yt.grad), ogy, dy, what="grad y")
     assert_sum_parity(host(bt.grad), ogb, db, what="grad b")
+
+
+# ------------------------------------------------------------------------------------------------
+# LSE backward: GENRED_LSE_GRAD against oracle O6, and torch.autograd
+# ------------------------------------------------------------------------------------------------
+
+@pytest.mark.parametrize("D", [2, 3, 5])
+@pytest.mark.parametrize("split", [0, 3])
+def test_lse_grad_kernel(G, D, split):
+    rng = np.random.default_rng(90 + D)
+    M, N, eps = 1300, 2900, 0.1
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    h = rng.standard_normal(N).astype(np.float32)
+    g = rng.standard_normal(M).astype(np.float32)
+    a, _ = oracle.lse(x, y, h, eps=eps)
+    S, gx = G.eval("lse_grad", "sum", dev(x), dev(y), None, dev(g), scale=eps, out_dtype="float64",
+                   row_shift=dev(-a), col_shift=dev(h.astype(np.float64)), split_j=split)
+    oS, oG, dS, dG = oracle.softmax_grad(x, y, alpha=-a, beta=h, coef=g, eps=eps)
+    assert_sum_parity(host(S), oS, dS, what="softmax sum")
+    assert np.max(np.abs(host(S) - 1.0)) < 1e-5
+    assert_sum_parity(host(gx), oG, dG, what="lse grad x")
+    # transposed: rows y, alpha = h, beta = -a, sig = g
+    Sh, gy = G.eval("lse_grad", "sum", dev(y), dev(x), dev(g), None, scale=eps, out_dtype="float64",
+                    row_shift=dev(h.astype(np.float64)), col_shift=dev(-a))
+    oSh, oGy, dSh, dGy = oracle.softmax_grad(y, x, alpha=h, beta=-a, sig=g, eps=eps)
+    assert_sum_parity(host(Sh), oSh, dSh, what="grad h")
+    assert_sum_parity(host(gy), oGy, dGy, what="grad y")
+
+
+def test_autograd_logsumexp(G):
+    from paper_2004_11127_b200.autograd import logsumexp
+    M, N, eps = 900, 2500, 0.05
+    x = synth.uniform3(M, 91); y = synth.gmm3(N, 92)
+    h = (np.random.default_rng(93).standard_normal(N) * 0.5).astype(np.float32)
+    g = np.random.default_rng(94).standard_normal(M)
+    xt, yt, ht = (dev(v).requires_grad_(True) for v in (x, y, h))
+    a = logsumexp(xt, yt, ht, eps)
+    a.backward(torch.from_numpy(g).cuda())
+    oa, _ = oracle.lse(x, y, h, eps=eps)
+    assert_lse_parity(host(a), oa, what="lse fwd")
+    _, oGx, _, dGx = oracle.softmax_grad(x, y, alpha=-oa, beta=h, coef=g, eps=eps)
+    oSh, oGy, dSh, dGy = oracle.softmax_grad(y, x, alpha=h, beta=-oa, sig=g, eps=eps)
+    assert_sum_parity(host(xt.grad), oGx, dGx, what="autograd x")
+    assert_sum_parity(host(yt.grad), oGy, dGy, what="autograd y")
+    assert_sum_parity(host(ht.grad), oSh, dSh, what="autograd h")
