@@ -95,6 +95,60 @@ cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int
     return cudaGetLastError();
 }
 
+// ---- range-packed j-records (block-sparse ranges) -----------------------------------------------
+// Record pair p belongs to the gathered interval k with copies[k].dst <= p < copies[k+1].dst; its
+// two j's are js + 2 (p - dst) + {0, 1}, valid while < je.  Invalid halves and padding pairs hold
+// zero-contribution records (b = 0).  Layouts as pack_kernel (GAUSS_AUTO or SQDIST_SUM).
+__global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const float *__restrict__ b,
+                                   int64_t N, int D, int E, float s, const RangeCopy *__restrict__ copies,
+                                   int ncopies, int64_t npairs, int RS, float *__restrict__ J,
+                                   const uint32_t *geo_enc) {
+    const Geo geo = kind == PACK_GAUSS_AUTO ? geo_decode(geo_enc, D, s) : Geo{};
+    const int boff = kind == PACK_GAUSS_AUTO ? 2 * (D + 1) : 2 * D;
+    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
+         p += (int64_t)gridDim.x * blockDim.x) {
+        int lo = 0, hi = ncopies - 1;                          // last copy with dst <= p
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (copies[mid].dst <= p) lo = mid; else hi = mid - 1;
+        }
+        const RangeCopy c = copies[lo];
+        float *rec = J + p * RS;
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = c.js + 2 * (p - c.dst) + h;
+            const bool valid = j < c.je && j < N;
+            double w = 0.0;
+            for (int d = 0; d < D; ++d) {
+                const float v = valid ? y[j * D + d] : 0.0f;
+                float r;
+                if (kind == PACK_GAUSS_AUTO && geo.expanded) {
+                    r = valid ? s * (v - geo.c[d]) : 0.0f;
+                    w += (double)r * (double)r;
+                } else {
+                    r = valid ? -(s * v) : 0.0f;
+                }
+                rec[2 * d + h] = r;
+            }
+            if (kind == PACK_GAUSS_AUTO) rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;
+            for (int e = 0; e < E; ++e)
+                rec[boff + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
+        }
+        for (int k = boff + 2 * E; k < RS; ++k) rec[k] = 0.0f;
+    }
+}
+
+cudaError_t launch_pack_ranges(int kind, const float *y, const float *b, int64_t N, int D, int E,
+                               float s, const RangeCopy *copies, int ncopies, int64_t npairs,
+                               float *J, cudaStream_t st, const uint32_t *geo) {
+    const int RS = pack_record_stride(kind, D, E);
+    int64_t blocks = (npairs + 255) / 256;
+    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks < 1) blocks = 1;
+    pack_ranges_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind, y, b, N, D, E, s, copies, ncopies,
+                                                         npairs, RS, J, geo);
+    return cudaGetLastError();
+}
+
 // ---- per-coordinate bounding box of x and y (order-preserving uint encodings, geo.cuh) -------
 __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float *__restrict__ y,
                             int64_t N, int D, uint32_t *geo) {

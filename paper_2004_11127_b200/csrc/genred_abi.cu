@@ -94,6 +94,26 @@ genred_status validate(const genred_args *a, std::string &msg) {
     if (a->out_dtype != GENRED_F32 && a->out_dtype != GENRED_F64) {
         msg = "out_dtype must be GENRED_F32 or GENRED_F64"; return GENRED_E_INVALID;
     }
+    if (a->n_ranges < 0) { msg = "n_ranges must be >= 0"; return GENRED_E_SHAPE; }
+    if (a->n_ranges > 0) {
+        if (!(sum_pair)) { msg = "block-sparse ranges are supported for the Sum reductions"; return GENRED_E_UNSUPPORTED; }
+        if (!a->ranges_i || !a->slices || !a->ranges_j) { msg = "ranges_i / slices / ranges_j is NULL"; return GENRED_E_INVALID; }
+        int64_t prev_ie = 0, prev_slice = 0;
+        for (int64_t c = 0; c < a->n_ranges; ++c) {
+            const int64_t is = a->ranges_i[2 * c], ie = a->ranges_i[2 * c + 1];
+            if (is < prev_ie || ie < is || ie > a->M) { msg = "ranges_i must be sorted, disjoint and within [0, M]"; return GENRED_E_SHAPE; }
+            prev_ie = ie;
+            const int64_t s1 = a->slices[c];
+            if (s1 < prev_slice) { msg = "slices must be non-decreasing"; return GENRED_E_SHAPE; }
+            int64_t prev_je = 0;
+            for (int64_t k = prev_slice; k < s1; ++k) {
+                const int64_t js = a->ranges_j[2 * k], je = a->ranges_j[2 * k + 1];
+                if (js < prev_je || je < js || je > a->N) { msg = "a cluster's ranges_j must be sorted, disjoint and within [0, N]"; return GENRED_E_SHAPE; }
+                prev_je = je;
+            }
+            prev_slice = s1;
+        }
+    }
     if (a->M > 0) {
         if (!a->out) { msg = "out is NULL"; return GENRED_E_INVALID; }
         if (a->N > 0 && !a->x) { msg = "x is NULL"; return GENRED_E_INVALID; }
@@ -226,6 +246,96 @@ genred_status cuda_fail(genred_ctx *ctx, cudaError_t e, const char *where) {
     return fail(ctx, GENRED_E_CUDA, std::string(where) + ": " + cudaGetErrorString(e));
 }
 
+// Block-sparse ranges (Sum family): gather every cluster's j-intervals into a contiguous,
+// tile-padded "range-packed" J, then one CTA per (cluster, row tile) streams only its tiles.
+genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st, int mode, int rmax) {
+    const int64_t M = a->M, N = a->N;
+    const int D = a->D, E = a->E;
+    const int out_f64 = a->out_dtype == GENRED_F64;
+    const int64_t pairs_per_tile = kTileJ / 2;
+    std::vector<RangeCopy> copies;
+    std::vector<RangeUnit> units;
+    int64_t cursor = 0, rows_total = 0;
+    for (int64_t c = 0; c < a->n_ranges; ++c) rows_total += a->ranges_i[2 * c + 1] - a->ranges_i[2 * c];
+    const int R = (a->n_ranges > 0 && rows_total / a->n_ranges >= 1024) ? rmax : 1;
+    const int64_t RT = (int64_t)kConsumerWarps * 32 * R;
+    int64_t s0 = 0;
+    for (int64_t c = 0; c < a->n_ranges; ++c) {
+        const int64_t is = a->ranges_i[2 * c], ie = a->ranges_i[2 * c + 1], s1 = a->slices[c];
+        const int64_t tile0 = cursor / pairs_per_tile;
+        for (int64_t k = s0; k < s1; ++k) {
+            const int64_t js = a->ranges_j[2 * k], je = a->ranges_j[2 * k + 1];
+            if (je <= js) continue;
+            copies.push_back({cursor, js, je});
+            cursor += (je - js + 1) / 2;
+        }
+        s0 = s1;
+        const int64_t pad = (pairs_per_tile - cursor % pairs_per_tile) % pairs_per_tile;
+        if (pad) { copies.push_back({cursor, 0, 0}); cursor += pad; }
+        const int64_t ntiles = cursor / pairs_per_tile - tile0;
+        if (ntiles == 0) continue;
+        for (int64_t r = is; r < ie; r += RT) units.push_back({r, std::min(r + RT, ie), tile0, ntiles});
+    }
+    copies.push_back({cursor, 0, 0});
+    const int pk = mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
+    const int RS = pack_record_stride(pk, D, E);
+    const size_t jbytes = al256((size_t)std::max<int64_t>(cursor, 1) * RS * 4);
+    const size_t cbytes = al256(copies.size() * sizeof(RangeCopy));
+    const size_t ubytes = al256(std::max<size_t>(units.size(), 1) * sizeof(RangeUnit));
+    genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + cbytes + ubytes + 256);
+    if (s != GENRED_OK) return s;
+    char *base = (char *)ctx->scratch;
+    float *J = (float *)base;
+    RangeCopy *dcopies = (RangeCopy *)(base + jbytes);
+    RangeUnit *dunits = (RangeUnit *)(base + jbytes + cbytes);
+    uint32_t *geo = (uint32_t *)(base + jbytes + cbytes + ubytes);
+    cudaError_t e = cudaMemcpyAsync(dcopies, copies.data(), copies.size() * sizeof(RangeCopy),
+                                    cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && !units.empty())
+        e = cudaMemcpyAsync(dunits, units.data(), units.size() * sizeof(RangeUnit), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "range table copy");
+    // neutral outputs for every row first; cluster rows are overwritten by the kernel
+    const int fill_kind = mode == 2 ? 1 : 0;
+    const int fill_C = mode == 1 ? D : E;
+    e = launch_fill(fill_kind, M, fill_C, D, a->out, out_f64, a->out_grad, nullptr, nullptr, st);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "fill kernel");
+    int kernels = 1;
+    float sc = 1.0f;
+    double scale_grad = 0.0;
+    if (mode != 3) {
+        sc = (float)(sqrt(kLog2e) / a->scale);
+        scale_grad = -2.0 / (a->scale * a->scale * (double)sc);
+        e = launch_bbox(a->x, M, a->y, N, D, geo, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
+        kernels++;
+    }
+    e = launch_pack_ranges(pk, a->y, a->b, N, D, E, sc, dcopies, (int)copies.size(), cursor, J, st, geo);
+    if (e != cudaSuccess) return cuda_fail(ctx, e, "range pack kernel");
+    kernels++;
+    SumLaunch L;
+    L.mode = mode; L.D = D; L.E = E; L.R = R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
+    L.split = 1; L.tiles_per_split = 0; L.ntiles = 0; L.s = sc;
+    L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
+    L.out_grad = a->out_grad; L.part = nullptr; L.geo = geo;
+    L.units = dunits; L.n_units = (int64_t)units.size();
+    int ctas = 0;
+    if (!units.empty()) {
+        prof_event(ctx, true, st);
+        e = launch_sum(L, st, &ctas);
+        prof_event(ctx, false, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel (ranges)");
+        kernels++;
+    }
+    ctx->launches += kernels;
+    ctx->plan.split_j = 1; ctx->plan.rows_per_cta = (int32_t)RT; ctx->plan.ctas = ctas;
+    ctx->plan.kernels = kernels; ctx->plan.path = 0;
+    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+    ctx->geo_dev = mode != 3 ? geo : nullptr;
+    ctx->geo_D = D;
+    ctx->geo_s = sc;
+    return GENRED_OK;
+}
+
 // Device-pointer evaluation (the path itself).
 genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st) {
     const int f = a->formula, red = a->reduction;
@@ -294,6 +404,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         const int mode = (f == GENRED_GAUSS) ? 0 : (f == GENRED_GAUSS_GRADX) ? 1
                        : (f == GENRED_GAUSS_SUM_GRADX) ? 2 : 3;
         const int rmax = sum_rows_per_thread_max(mode, D, E);
+        if (a->n_ranges > 0) return eval_ranges(ctx, a, st, mode, rmax);
         Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
         const int pk = mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
@@ -326,7 +437,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
         L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
-        L.out_grad = a->out_grad; L.part = part; L.geo = geo;
+        L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
         int ctas = 0;
         prof_event(ctx, true, st);
         e = launch_sum(L, st, &ctas);

@@ -36,6 +36,21 @@ cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, in
 bool geo_expanded_host(const uint32_t *geo_dev, int D, float s);
 int pack_record_stride(int kind, int D, int E);
 
+// Block-sparse ranges ("cluster-wise block-sparsity patterns"): one CTA per unit,
+// the rows [row0, row_end) of one i-cluster against the ntiles j-tiles starting at tile0 of the
+// range-packed J (the cluster's j-intervals gathered contiguously, padded to whole tiles).
+struct RangeUnit {
+    int64_t row0, row_end, tile0, ntiles;
+};
+// One gathered j-interval: destination record pair `dst`, source j-interval [js, je)
+// (js = je = 0 marks padding records).
+struct RangeCopy {
+    int64_t dst, js, je;
+};
+cudaError_t launch_pack_ranges(int kind, const float *y, const float *b, int64_t N, int D, int E,
+                               float s, const RangeCopy *copies, int ncopies, int64_t npairs,
+                               float *J, cudaStream_t st, const uint32_t *geo);
+
 struct SumLaunch {
     int mode;                 // 0 SUM, 1 GRADX, 2 SUM_GRADX, 3 SQDIST_SUM
     int D, E, R;              // R = rows per consumer thread
@@ -49,6 +64,8 @@ struct SumLaunch {
     void *out; int out_f64;   // sum output (SUM / SUM_GRADX / SQDIST_SUM) or gradient (GRADX)
     float *out_grad;          // SUM_GRADX gradient output
     double *part;             // split > 1: split x M x C fp64 partials
+    const RangeUnit *units;   // block-sparse ranges (device), or nullptr
+    int64_t n_units;
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
 int sum_occupancy(int mode, int D, int E, int R);

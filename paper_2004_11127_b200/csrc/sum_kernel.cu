@@ -53,6 +53,7 @@ struct SumParams {
     int out_f64;
     float *out_grad;
     double *part;
+    const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
 };
 
 // 2^u for u in [-24, 6] (the expanded path's range, geo.cuh) on the FP32 pipe: u = n + f with
@@ -85,7 +86,7 @@ constexpr bool kPolyShare = false;
 // in fp64 at the end.
 template <int MODE, int D, int E, int R, bool XP>
 __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt,
-                                         int64_t row0, int sp, const Geo &geo) {
+                                         int64_t row0, int64_t row_end, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
     constexpr bool POLY = kPolyShare && XP && R == 4;
@@ -96,7 +97,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        const bool ok = i < p.M;
+        const bool ok = i < row_end;
         xsq[r] = 0.0;
 #pragma unroll
         for (int d = 0; d < D; ++d) {
@@ -263,7 +264,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        if (i >= p.M) continue;
+        if (i >= row_end) continue;
         if constexpr (XP) {
             const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
             if constexpr (NG > 0) {
@@ -308,22 +309,30 @@ sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
-    const int64_t itile = blockIdx.x / p.split;
-    const int sp = (int)(blockIdx.x % p.split);
-    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
-    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-    const int nt = (int)(t1 - t0);
+    int64_t row0, row_end, t0;
+    int sp, nt;
+    if (p.units) {                                     // block-sparse: rows of one cluster
+        const RangeUnit u = p.units[blockIdx.x];
+        row0 = u.row0; row_end = u.row_end; t0 = u.tile0; nt = (int)u.ntiles; sp = 0;
+    } else {
+        const int64_t itile = blockIdx.x / p.split;
+        sp = (int)(blockIdx.x % p.split);
+        t0 = (int64_t)sp * p.tiles_per_split;
+        const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+        nt = (int)(t1 - t0);
+        row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+        row_end = p.M;
+    }
 
     JRing<kStages> ring;
     ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
-    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
-        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, sp, geo);
-        else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, sp, geo);
+        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, row_end, sp, geo);
+        else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
     } else {
         Geo geo{};
-        sum_body<MODE, D, E, R, false>(p, ring, nt, row0, sp, geo);
+        sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
     }
 }
 
@@ -343,10 +352,11 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;
     p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.s = a.s;
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
-    p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo;
+    p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = a.units;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
-    const int64_t grid = itiles * a.split;
+    const int64_t grid = a.units ? a.n_units : itiles * a.split;
+    if (grid == 0) { *ctas = 0; return cudaSuccess; }
     *ctas = (int)grid;
     kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
     return cudaGetLastError();

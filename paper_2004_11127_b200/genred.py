@@ -22,7 +22,7 @@ ROOT = os.path.dirname(HERE)
 LIB_PATH = os.environ.get("GENRED_LIB") or os.path.join(HERE, "libgenred.so")
 HEADER = os.path.join(ROOT, "include", "genred.h")
 
-ABI_VERSION = 2
+ABI_VERSION = 3
 OK, E_INVALID, E_UNSUPPORTED, E_SHAPE, E_NOMEM, E_CUDA = range(6)
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_UNSUPPORTED", 3: "E_SHAPE", 4: "E_NOMEM", 5: "E_CUDA"}
 
@@ -51,6 +51,8 @@ class Args(ctypes.Structure):
         ("pad0", ctypes.c_int32), ("out_grad", ctypes.c_void_p), ("out_idx", ctypes.c_void_p),
         ("lse_state", ctypes.c_void_p), ("j_offset", ctypes.c_int64),
         ("row_shift", ctypes.c_void_p), ("col_shift", ctypes.c_void_p),
+        ("n_ranges", ctypes.c_int64), ("ranges_i", ctypes.c_void_p), ("slices", ctypes.c_void_p),
+        ("ranges_j", ctypes.c_void_p),
     ]
 
 
@@ -180,7 +182,8 @@ def _check(t, name, dtype_ok=("float32",)):
 
 def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1.0, K: int = 1,
          out=None, out_dtype: str = "float32", out_grad=None, out_idx=None, lse_state=None,
-         split_j: int = 0, j_offset: int = 0, stream=None, row_shift=None, col_shift=None):
+         split_j: int = 0, j_offset: int = 0, stream=None, row_shift=None, col_shift=None,
+         ranges=None):
     """Evaluate a_i = Reduction_j F(x_i, y_j) (Eq. 1) through genred_eval.
 
     x: (M, D), y: (N, D), b: (N, E) (or h: (N,) for LSE), g: (M, E); fp32, contiguous, all CUDA
@@ -240,6 +243,10 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     a.out_grad, a.out_idx, a.lse_state = _ptr(out_grad), _ptr(out_idx), _ptr(lse_state)
     a.j_offset = int(j_offset)
     a.row_shift, a.col_shift = _ptr(row_shift), _ptr(col_shift)
+    if ranges is not None:              # (ranges_i (C,2), slices (C,), ranges_j (L,2)) host int64
+        ri, sl, rj = (np.ascontiguousarray(np.asarray(v, dtype=np.int64)) for v in ranges)
+        a.n_ranges = int(ri.shape[0])
+        a.ranges_i, a.slices, a.ranges_j = ri.ctypes.data, sl.ctypes.data, rj.ctypes.data
     if host:
         dev, sptr = None, None
     else:

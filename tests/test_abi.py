@@ -102,3 +102,23 @@ def test_no_cpu_fallback_without_device(lib):
     assert lib.genred_create(0, ctypes.byref(h)) == G.E_CUDA
     with pytest.raises(G.GenredError):
         G.context(0)
+
+
+def test_ranges_validation(lib):
+    import numpy as np
+    ri = np.array([[0, 5], [5, 10]], np.int64); sl = np.array([1, 2], np.int64)
+    rj = np.array([[0, 20], [3, 7]], np.int64)
+    def args(ri, sl, rj, **kw):
+        a = _args(M=10, N=20, **kw)
+        a.n_ranges = ri.shape[0]
+        a.ranges_i, a.slices, a.ranges_j = ri.ctypes.data, sl.ctypes.data, rj.ctypes.data
+        return a
+    assert G.validate(args(ri, sl, rj))[0] == G.OK
+    bad_i = np.array([[0, 6], [5, 10]], np.int64)                   # overlapping clusters
+    assert G.validate(args(bad_i, sl, rj))[0] == G.E_SHAPE
+    bad_j = np.array([[0, 21], [3, 7]], np.int64)                   # beyond N
+    assert G.validate(args(ri, sl, bad_j))[0] == G.E_SHAPE
+    rj2 = np.array([[5, 9], [3, 7]], np.int64); sl2 = np.array([2, 2], np.int64)   # unsorted in cluster
+    assert G.validate(args(ri, sl2, np.array([[5, 9], [3, 7]], np.int64)))[0] == G.E_SHAPE
+    a = args(ri, sl, rj, formula=2, reduction=1)                    # LSE with ranges
+    assert G.validate(a)[0] == G.E_UNSUPPORTED

@@ -538,3 +538,78 @@ def test_autograd_logsumexp(G):
     assert_sum_parity(host(xt.grad), oGx, dGx, what="autograd x")
     assert_sum_parity(host(yt.grad), oGy, dGy, what="autograd y")
     assert_sum_parity(host(ht.grad), oSh, dSh, what="autograd h")
+
+
+# ------------------------------------------------------------------------------------------------
+# Block-sparse ranges (PAPER.md:228 cluster-wise block-sparsity)
+# ------------------------------------------------------------------------------------------------
+
+def _clustered(n_clusters, per, seed, D=3, std=0.03):
+    rng = np.random.default_rng(seed)
+    centers = rng.uniform(0.1, 0.9, (n_clusters, D))
+    sizes = rng.integers(max(1, per // 2), per * 2, n_clusters)
+    pts = np.concatenate([centers[c] + std * rng.standard_normal((sizes[c], D)) for c in range(n_clusters)])
+    bounds = np.concatenate([[0], np.cumsum(sizes)])
+    return pts.astype(np.float32), bounds, centers
+
+
+def _ranges(bx, cx, by, cy, thr):
+    ri, sl, rj = [], [], []
+    for c in range(len(cx)):
+        ri.append((bx[c], bx[c + 1]))
+        for k in range(len(cy)):
+            if np.linalg.norm(cx[c] - cy[k]) < thr:
+                rj.append((by[k], by[k + 1]))
+        sl.append(len(rj))
+    return (np.array(ri, np.int64), np.array(sl, np.int64), np.array(rj, np.int64).reshape(-1, 2))
+
+
+@pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
+def test_block_sparse_ranges(G, formula):
+    x, bx, cx = _clustered(24, 150, 101)
+    y, by, cy = _clustered(30, 120, 102)
+    b = synth.signal(len(y), 103)
+    ranges = _ranges(bx, cx, by, cy, 0.35)
+    ri, sl, rj = ranges
+    sigma = 0.1
+    res = G.eval(formula, "sum", dev(x), dev(y), dev(b), None, scale=sigma, ranges=ranges)
+    out = host(res[0] if isinstance(res, tuple) else res)
+    grad = host(res[1]) if isinstance(res, tuple) else (out if formula == "gauss_gradx" else None)
+    s0 = 0
+    for c in range(len(ri)):
+        rows = np.arange(ri[c, 0], ri[c, 1])
+        exp_s = 0.0; den_s = 0.0; exp_g = 0.0; den_g = 0.0
+        for k in range(s0, sl[c]):
+            js, je = rj[k]
+            if formula == "sqdist":
+                o, d = oracle.sqdist_sum(x[rows], y[js:je], b[js:je])
+            else:
+                o, d = oracle.gauss_sum(x[rows], y[js:je], b[js:je], sigma=sigma)
+            og, dg = oracle.gauss_gradx(x[rows], y[js:je], b[js:je], None, sigma=sigma)
+            exp_s = exp_s + o; den_s = den_s + d; exp_g = exp_g + og; den_g = den_g + dg
+        s0 = sl[c]
+        if formula in ("gauss", "sqdist", "gauss_sum_gradx"):
+            assert_sum_parity(out[rows], np.broadcast_to(exp_s, out[rows].shape),
+                              np.broadcast_to(np.maximum(den_s, 1e-30), out[rows].shape), what=f"ranges sum c={c}")
+        if formula in ("gauss_gradx", "gauss_sum_gradx"):
+            assert_sum_parity(grad[rows], np.broadcast_to(exp_g, grad[rows].shape),
+                              np.broadcast_to(np.maximum(den_g, 1e-30), grad[rows].shape), what=f"ranges grad c={c}")
+
+
+def test_ranges_full_cover_equals_dense_and_uncovered_rows_are_zero(G):
+    x, bx, cx = _clustered(10, 300, 111)
+    y = synth.uniform3(2500, 112); b = synth.signal(2500, 113)
+    M = len(x)
+    # clusters cover all rows but the first cluster; each covered cluster reduces over all j
+    ri = np.array([(bx[c], bx[c + 1]) for c in range(1, 10)], np.int64)
+    sl = np.arange(1, 10, dtype=np.int64)
+    rj = np.array([(0, 2500)] * 9, np.int64)
+    a = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, ranges=(ri, sl, rj)))
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+    assert np.all(a[:bx[1]] == 0.0)
+    assert_sum_parity(a[bx[1]:], o[bx[1]:], den[bx[1]:], what="full cover")
+    # split intervals (same union) give the same numbers within tolerance
+    rj2 = np.array([(0, 1001), (1001, 1777), (1777, 2500)] * 9, np.int64)
+    sl2 = np.arange(3, 28, 3, dtype=np.int64)
+    a2 = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, ranges=(ri, sl2, rj2)))
+    assert_sum_parity(a2[bx[1]:], o[bx[1]:], den[bx[1]:], what="split intervals")
