@@ -1,0 +1,69 @@
+"""Workloads on top of the Genred kernels ("k-means
+clustering", "interface with the iterative linear solvers ... solve large kernel
+linear systems efficiently").
+
+* ``gauss_cg``: matrix-free conjugate gradients for (K + alpha I) x = b with K_ij =
+  exp(-|p_i - p_j|^2 / sigma^2) (kernel ridge / GP / Kriging systems).  Every product K v is one
+  libgenred Gaussian Sum over the same points (optionally block-sparse ``ranges``); the O(N)
+  vector updates run as torch device ops (plumbing: they are not Genred reductions).
+* ``kmeans``: Lloyd iterations whose assignment step is libgenred ArgKMin with K = 1 (ties to the
+  lowest centroid index, R7) and whose update is a device scatter-add.
+"""
+from __future__ import annotations
+
+import torch
+
+from . import genred
+
+
+def gauss_matvec(p, v, sigma: float, ranges=None):
+    """K v with K_ij = exp(-|p_i - p_j|^2 / sigma^2): one Genred Sum (v: (N, E))."""
+    return genred.eval("gauss", "sum", p, p, v.contiguous(), scale=sigma, ranges=ranges)
+
+
+def gauss_cg(p, b, sigma: float, alpha: float, tol: float = 1e-6, max_iter: int = 500, x0=None,
+             ranges=None):
+    """Solve (K + alpha I) x = b by conjugate gradients (K is SPD for distinct points, alpha > 0).
+
+    p: (N, D) fp32 CUDA points, b: (N,) or (N, E) right-hand side.  Residual norms are tracked in
+    fp64; matvecs run in libgenred (fp32 data, fp64 tile accumulation).  Returns (x, info)."""
+    squeeze = b.dim() == 1
+    B = (b[:, None] if squeeze else b).to(torch.float32).contiguous()
+    X = torch.zeros_like(B) if x0 is None else (x0[:, None] if squeeze else x0).clone().float()
+    r = B - (gauss_matvec(p, X, sigma, ranges) + alpha * X) if x0 is not None else B.clone()
+    d = r.clone()
+    rr = (r.double() * r.double()).sum(0)
+    bnorm = torch.sqrt((B.double() * B.double()).sum(0))
+    it = 0
+    for it in range(1, max_iter + 1):
+        Ad = gauss_matvec(p, d, sigma, ranges) + alpha * d
+        step = rr / (d.double() * Ad.double()).sum(0)
+        X = X + step.float() * d
+        r = r - step.float() * Ad
+        rr_new = (r.double() * r.double()).sum(0)
+        if bool(torch.all(torch.sqrt(rr_new) <= tol * bnorm)):
+            rr = rr_new
+            break
+        d = r + (rr_new / rr).float() * d
+        rr = rr_new
+    info = {"iterations": it, "rel_residual": (torch.sqrt(rr) / bnorm).max().item()}
+    return (X[:, 0] if squeeze else X), info
+
+
+def kmeans(x, k: int, iters: int = 10, init=None):
+    """Lloyd's algorithm.  x: (N, D) fp32 CUDA.  Returns (labels (N,) int64, centroids (k, D),
+    objective per iteration).  Assignment = libgenred ArgKMin K=1 (exact distances)."""
+    N, D = x.shape
+    c = (x[:k].clone() if init is None else init.clone().float()).contiguous()
+    hist = []
+    labels = None
+    for _ in range(iters):
+        d, j = genred.eval("sqdist", "argkmin", x, c, K=1)
+        labels = j[:, 0]
+        hist.append(float(d.double().sum().item()))
+        sums = torch.zeros((k, D), dtype=torch.float64, device=x.device)
+        sums.index_add_(0, labels, x.double())
+        counts = torch.bincount(labels, minlength=k).double()
+        keep = counts > 0
+        c = torch.where(keep[:, None], (sums / counts.clamp_min(1)[:, None]).float(), c).contiguous()
+    return labels, c, hist

@@ -613,3 +613,30 @@ def test_ranges_full_cover_equals_dense_and_uncovered_rows_are_zero(G):
     sl2 = np.arange(3, 28, 3, dtype=np.int64)
     a2 = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, ranges=(ri, sl2, rj2)))
     assert_sum_parity(a2[bx[1]:], o[bx[1]:], den[bx[1]:], what="split intervals")
+
+
+# ------------------------------------------------------------------------------------------------
+# Workloads on the kernels: kernel CG solve and k-means
+# ------------------------------------------------------------------------------------------------
+
+def test_gauss_cg_solves_kernel_system(G):
+    from paper_2004_11127_b200.solvers import gauss_cg
+    N, sigma, alpha = 3000, 0.1, 0.1
+    p = synth.uniform3(N, 121); rhs = synth.signal(N, 122, signed=True)[:, 0]
+    xs, info = gauss_cg(dev(p), dev(rhs), sigma, alpha, tol=1e-5, max_iter=400)
+    assert info["rel_residual"] <= 1e-5
+    sol = host(xs).astype(np.float64)
+    Kx, _ = oracle.gauss_sum(p, p, sol, sigma=sigma)               # residual with the oracle matvec
+    res = Kx[:, 0] + alpha * sol - rhs
+    assert np.linalg.norm(res) <= 5e-5 * np.linalg.norm(rhs)
+
+
+def test_kmeans_assignment_and_monotone_objective(G):
+    from paper_2004_11127_b200.solvers import kmeans
+    x = synth.gmm3(20000, 131)
+    labels, c, hist = kmeans(dev(x), 32, iters=8)
+    assert all(b <= a * (1 + 1e-6) for a, b in zip(hist, hist[1:]))   # Lloyd never increases
+    # final assignment = exact nearest centroid (oracle ArgKMin K=1 on the returned centroids)
+    d, j = G.eval("sqdist", "argkmin", dev(x), c.contiguous(), K=1)
+    od, oj = oracle.argkmin(x, host(c), 2)
+    argk_check(host(d), host(j), od, oj, 1, what="kmeans assign")
