@@ -640,3 +640,17 @@ def test_kmeans_assignment_and_monotone_objective(G):
     d, j = G.eval("sqdist", "argkmin", dev(x), c.contiguous(), K=1)
     od, oj = oracle.argkmin(x, host(c), 2)
     argk_check(host(d), host(j), od, oj, 1, what="kmeans assign")
+
+
+def test_ishard_rows_bitwise_equal_to_single_gpu(G):
+    """8(e): an i-shard computes its rows with exactly the single-GPU arithmetic when the j-split
+    is the same, so sharded outputs are bitwise equal (emulated shards on one GPU)."""
+    M, N = 5000, 20000
+    x = synth.uniform3(M, 141); y = synth.uniform3(N, 142); b = synth.signal(N, 143)
+    full = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=2))
+    for lo, hi in ((0, 1250), (1250, 3333), (3333, 5000)):
+        part = host(G.eval("gauss", "sum", dev(x[lo:hi]), dev(y), dev(b), scale=0.5, split_j=2))
+        np.testing.assert_array_equal(part, full[lo:hi])
+    lf = host(G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
+    lp = host(G.eval("sqdist", "lse", dev(x[1000:2000]), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
+    np.testing.assert_array_equal(lp, lf[1000:2000])
