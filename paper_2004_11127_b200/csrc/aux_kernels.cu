@@ -6,6 +6,7 @@
 #include <math.h>
 #include <string.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "device.cuh"
@@ -150,15 +151,18 @@ cudaError_t launch_pack_ranges(int kind, const float *y, const float *b, int64_t
 }
 
 // ---- per-coordinate bounding box of x and y (order-preserving uint encodings, geo.cuh) -------
+// blockIdx.y = 0: y into geo[0..15]; blockIdx.y = 1: x into geo[16..31]
 __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float *__restrict__ y,
                             int64_t N, int D, uint32_t *geo) {
     float lo[8], hi[8];
 #pragma unroll
     for (int d = 0; d < 8; ++d) { lo[d] = INFINITY; hi[d] = -INFINITY; }
-    const int64_t rows = M + N;
+    const float *src = blockIdx.y == 0 ? y : x;
+    const int64_t rows = blockIdx.y == 0 ? N : M;
+    const int off = blockIdx.y == 0 ? 0 : 16;
     for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows;
          t += (int64_t)gridDim.x * blockDim.x) {
-        const float *pt = t < M ? x + t * D : y + (t - M) * D;
+        const float *pt = src + t * D;
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             if (d < D) {
@@ -179,8 +183,8 @@ __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float 
     if ((threadIdx.x & 31) == 0) {
         for (int d = 0; d < D; ++d) {
             if (lo[d] <= hi[d]) {
-                atomicMin(geo + d, f2ord(lo[d]));
-                atomicMax(geo + 8 + d, f2ord(hi[d]));
+                atomicMin(geo + off + d, f2ord(lo[d]));
+                atomicMax(geo + off + 8 + d, f2ord(hi[d]));
             }
         }
     }
@@ -188,18 +192,21 @@ __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float 
 
 cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, int D, uint32_t *geo,
                         cudaStream_t st) {
-    cudaError_t e = cudaMemsetAsync(geo, 0xff, 8 * sizeof(uint32_t), st);      // minima: max code
-    if (e == cudaSuccess) e = cudaMemsetAsync(geo + 8, 0x00, 8 * sizeof(uint32_t), st);
+    cudaError_t e = cudaSuccess;
+    for (int half = 0; half < 2 && e == cudaSuccess; ++half) {
+        e = cudaMemsetAsync(geo + 16 * half, 0xff, 8 * sizeof(uint32_t), st);     // minima: max code
+        if (e == cudaSuccess) e = cudaMemsetAsync(geo + 16 * half + 8, 0x00, 8 * sizeof(uint32_t), st);
+    }
     if (e != cudaSuccess) return e;
-    int64_t blocks = (M + N + 255) / 256;
-    if (blocks > 148 * 4) blocks = 148 * 4;
+    int64_t blocks = (std::max(M, N) + 255) / 256;
+    if (blocks > 148 * 2) blocks = 148 * 2;
     if (blocks < 1) blocks = 1;
-    bbox_kernel<<<(unsigned)blocks, 256, 0, st>>>(x, M, y, N, D, geo);
+    bbox_kernel<<<dim3((unsigned)blocks, 2), 256, 0, st>>>(x, M, y, N, D, geo);
     return cudaGetLastError();
 }
 
 bool geo_expanded_host(const uint32_t *geo_dev, int D, float s) {
-    uint32_t h[16];
+    uint32_t h[32];
     if (cudaMemcpy(h, geo_dev, sizeof(h), cudaMemcpyDeviceToHost) != cudaSuccess) {
         cudaGetLastError();
         return false;
@@ -213,10 +220,10 @@ bool geo_expanded_host(const uint32_t *geo_dev, int D, float s) {
     float r2 = 0.0f;
     bool ok = true;
     for (int d = 0; d < D; ++d) {
-        const float lo = dec(h[d]), hi = dec(h[8 + d]);
-        ok = ok && std::isfinite(lo) && std::isfinite(hi);
+        const float lo = dec(h[d]), hi = dec(h[8 + d]), xlo = dec(h[16 + d]), xhi = dec(h[24 + d]);
+        ok = ok && std::isfinite(lo) && std::isfinite(hi) && std::isfinite(xlo) && std::isfinite(xhi);
         const float c = 0.5f * lo + 0.5f * hi;
-        const float hh = fmaxf(hi - c, c - lo) * 1.0001f;
+        const float hh = fmaxf(fmaxf(hi - c, c - lo), fmaxf(xhi - c, c - xlo)) * 1.0001f;
         const float sh = s * hh;
         r2 = fmaf(sh, sh, r2);
     }

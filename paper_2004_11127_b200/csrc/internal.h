@@ -29,7 +29,7 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
                         float s, double hscale, int64_t npairs, float *J, cudaStream_t st,
                         const uint32_t *geo = nullptr);
-// Per-coordinate bounding box of x (M x D) and y (N x D) into geo[16] (encoded, geo.cuh).
+// Per-coordinate bounding boxes of y (N x D) and x (M x D) into geo[32] (encoded, geo.cuh).
 cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, int D, uint32_t *geo,
                         cudaStream_t st);
 // Host mirror of the device path decision (reads geo back; synchronises; introspection only).
