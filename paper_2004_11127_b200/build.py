@@ -44,6 +44,8 @@ def _compile(src: str, verbose: bool) -> str:
     obj = os.path.join(BUILD, f"{name}.{_deps_hash(src)}.o")
     if os.path.exists(obj):
         return obj
+    for stale in glob.glob(os.path.join(BUILD, f"{name}.*.o")):   # objects of older sources
+        os.remove(stale)
     cmd = [NVCC] + ARCH + FLAGS + ["-c", src, "-o", obj + ".tmp"]
     if verbose:
         print(" ".join(cmd), flush=True)
