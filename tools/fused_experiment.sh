@@ -1,0 +1,13 @@
+for lib in build/variants/grad_*.so; do
+GENRED_LIB=$lib python - <<'PY'
+import os, torch, synth
+from paper_2004_11127_b200 import genred
+M = 100_000
+x = torch.from_numpy(synth.uniform3(M, 1)).cuda(); y = torch.from_numpy(synth.uniform3(M, 2)).cuda(); b = torch.from_numpy(synth.signal(M, 3)).cuda()
+for _ in range(3): genred.eval("gauss_sum_gradx", "sum", x, y, b, scale=0.5)
+genred.profile(True)
+for _ in range(5): genred.eval("gauss_sum_gradx", "sum", x, y, b, scale=0.5)
+ms = genred.profile_read()
+print("lib", os.environ["GENRED_LIB"], "ms", round(min(ms), 3), "pairs/clk/SM", round(M*M/(min(ms)*1e-3)/(148*1.965e9), 2), genred.last_plan())
+PY
+done
