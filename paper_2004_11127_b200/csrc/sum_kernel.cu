@@ -311,7 +311,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 
 template <int MODE, int D, int E, int R>
 __global__ void __launch_bounds__(kThreads, (((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ||
-                                            ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && R == 2)) ? 3 : 2)
+                                            ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && E == 1 && R == 2)) ? 3 : 2)
 sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
