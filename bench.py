@@ -241,6 +241,9 @@ def main() -> None:
     ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (cpu_baseline); 0 = auto")
     ap.add_argument("--ref-pairs", type=float, default=0, help="oracle pairs per reference step (0 = auto)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="testing only: gloo lets several ranks share one GPU (--one-device)")
+    ap.add_argument("--one-device", action="store_true", help="testing only: every rank uses cuda:0")
     ap.add_argument("--no-cpu", action="store_true")
     args = ap.parse_args()
 
@@ -255,9 +258,14 @@ def main() -> None:
     import torch.distributed as dist
     from paper_2004_11127_b200 import genred
 
+    if args.one_device:
+        local = 0
     torch.cuda.set_device(local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group("gloo")
     w = workload(args.config)
     c = w["cfg"]
     M, N = c.M, c.N

@@ -61,6 +61,14 @@ static inline double sqdist(const double *x, const double *y, int D) {
 
 static inline int64_t row_of(const int64_t *rows, int64_t r) { return rows ? rows[r] : r; }
 
+void oracle_set_num_threads(int n) {
+#ifdef _OPENMP
+    if (n > 0) omp_set_num_threads(n);
+#else
+    (void)n;
+#endif
+}
+
 int oracle_num_threads(void) {
 #ifdef _OPENMP
     return omp_get_max_threads();

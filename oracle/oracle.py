@@ -61,6 +61,14 @@ def num_threads() -> int:
     return int(_load().oracle_num_threads())
 
 
+def set_num_threads(n: int) -> None:
+    """OpenMP threads for the oracle (torchrun sets OMP_NUM_THREADS=1 per rank)."""
+    lib = _load()
+    lib.oracle_set_num_threads.argtypes = [ctypes.c_int]
+    lib.oracle_set_num_threads.restype = None
+    lib.oracle_set_num_threads(int(n))
+
+
 def _f64(a, ncols=None):
     if a is None:
         return None
