@@ -187,6 +187,7 @@ def run_reference(args, rank: int, world: int) -> None:
     if rank != 0:
         return
     import oracle
+    oracle.set_num_threads(os.cpu_count() or 1)     # the other ranks exit: all host cores are ours
     w = workload(args.config)
     c = w["cfg"]
     x, y, b = make_inputs(w, args.dist)
@@ -414,6 +415,8 @@ def main() -> None:
     # ---------------- fp64 oracle on the host cores (rank 0, N=1 only) ----------------
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu:
+        import oracle
+        oracle.set_num_threads(os.cpu_count() or 1)
         nrows = args.cpu_rows or max(16, min(M, int(1e10 // (N * (c.D if argk else 1)))))
         rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
         gpu_rows = (out_idx if argk else out).cpu().numpy()[rows]
