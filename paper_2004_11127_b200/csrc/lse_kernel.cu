@@ -28,7 +28,7 @@ namespace genred {
 // check costs one FMNMX + FSETP per row and sub-chunk instead of a max per pair.
 constexpr float kSumMax = 65536.0f;
 #ifndef GENRED_LSE_SUB
-#define GENRED_LSE_SUB 8
+#define GENRED_LSE_SUB 16
 #endif
 #ifndef GENRED_LSE_MINB
 #define GENRED_LSE_MINB 2
