@@ -162,19 +162,13 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
             for (int e = 0; e < E; ++e) bv[e] = make_float2(f[BOFF + 2 * e], f[BOFF + 2 * e + 1]);
             if constexpr (XP) {
                 const float2 w = make_float2(f[2 * D], f[2 * D + 1]);              // -|y'|^2
-                // coordinate-major over the rows: consecutive FFMA2s share the y'_d operand
-                // (register reuse cache), so each reads two register pairs instead of three
-                float2 uu[R];
-#pragma unroll
-                for (int r = 0; r < R; ++r) uu[r] = fma2(dup2(xr[r][0]), ny[0], w);
-#pragma unroll
-                for (int d = 1; d < D; ++d) {
-#pragma unroll
-                    for (int r = 0; r < R; ++r) uu[r] = fma2(dup2(xr[r][d]), ny[d], uu[r]);   // 2x'.y' - |y'|^2
-                }
+                // (a coordinate-major order over the rows, meant to share y'_d through the register
+                // reuse cache, measured 0.8% slower: ptxas schedules either way)
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
-                    const float2 u = uu[r];
+                    float2 u = fma2(dup2(xr[r][0]), ny[0], w);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(dup2(xr[r][d]), ny[d], u);   // 2x'.y' - |y'|^2
                     float2 ex;
                     // FP32-pipe exp2 share (kPolyShare, off: see DESIGN.md Sec. 6 measurements)
                     if (POLY && r == R - 1 && hh == 0) ex = ex2_poly2(u);
