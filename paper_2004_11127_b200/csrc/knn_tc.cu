@@ -36,6 +36,14 @@ constexpr int BM = 128;                 // query rows per tile (TMEM lanes)
 constexpr int BN = 256;                 // refs per tile (TMEM columns per accumulator)
 constexpr int BK = 16;                  // fp32/tf32 elements per k-block (64 B rows, 64B swizzle)
 constexpr int STAGES = 4;
+#ifndef GENRED_KNN_CLUSTER
+#define GENRED_KNN_CLUSTER 1
+#endif
+// CTAs sharing (multicasting) each ref tile.  CLUSTER = 2 is correct (tests pass) and cuts the
+// data path (1-MMA probe: 3.47 -> 3.10 ms at C4) but measured 3.77 ms against 3.69 ms for the
+// full 3xTF32 kernel: the tensor pipe is then the bound and the pair's lock-step costs more
+// than it saves, so 1 is the default.
+constexpr int CLUSTER = GENRED_KNN_CLUSTER;
 constexpr int A_BYTES = BM * BK * 4;    // 8 KB
 constexpr int B_BYTES = BN * BK * 4;    // 16 KB
 constexpr int STAGE_BYTES = 2 * A_BYTES + 2 * B_BYTES;   // hi + lo of both: 48 KB
@@ -49,6 +57,20 @@ __device__ __forceinline__ void tma_load_2d(void *smem, const CUtensorMap *map, 
     asm volatile(
         "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];"
         ::"r"(smem_u32(smem)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)) : "memory");
+}
+
+// Multicast variant: the same box lands at the same offset in every CTA of `mask` (cluster), each
+// completing the mbarrier at that offset in its own shared memory.
+__device__ __forceinline__ void tma_load_2d_mc(void *smem, const CUtensorMap *map, int c0, int c1,
+                                               uint64_t *bar, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster"
+        " [%0], [%1, {%2, %3}], [%4], %5;"
+        ::"r"(smem_u32(smem)), "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar)), "h"(mask) : "memory");
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 
 __device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
@@ -79,6 +101,12 @@ __device__ __forceinline__ void mma_tf32(uint32_t d_tmem, uint64_t a, uint64_t b
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                  ::"r"(smem_u32(bar)) : "memory");
+}
+
+// Arrive (when the MMAs issued so far complete) on the barrier at this offset in every CTA of mask.
+__device__ __forceinline__ void mma_commit_mc(uint64_t *bar, uint16_t mask) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;"
+                 ::"r"(smem_u32(bar)), "h"(mask) : "memory");
 }
 
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
@@ -127,7 +155,11 @@ __device__ __forceinline__ void kp_insert(float (&d)[KP], int32_t (&j)[KP], floa
     kth = d[KP - 1];
 }
 
-template <int KP>
+// CL = 2: a cluster of two CTAs works on two query row tiles against the same ref tiles; each
+// CTA loads its own A tile and HALF of the B tile, multicast to both (B traffic from L2 halves);
+// a ring stage may be refilled only once both CTAs' MMAs have read it (empty barriers count 2,
+// commits multicast to the pair).
+template <int KP, int CL>
 __global__ void __launch_bounds__(NUM_THREADS, 1)
 knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant__ CUtensorMap map_xlo,
               const __grid_constant__ CUtensorMap map_yhi, const __grid_constant__ CUtensorMap map_ylo,
@@ -147,7 +179,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) {
-        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
+        for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], CL); }
         for (int a = 0; a < 2; ++a) { mbar_init(&tfull[a], 1); mbar_init(&tempty[a], 4); }
         fence_barrier_init();
     }
@@ -158,22 +190,45 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
     }
     fence_before();
     __syncthreads();
+    if (CL > 1) cluster_sync_all();                      // peer barriers initialised before any multicast
     fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    const int n_units = p.n_groups * p.n_rtiles;
+    const int n_rgroups = (p.n_rtiles + CL - 1) / CL;    // row tiles per cluster unit
+    const int n_units = p.n_groups * n_rgroups;
+    const int crank = CL > 1 ? (int)(blockIdx.x % CL) : 0;   // rank in the cluster
+    const int ubeg = blockIdx.x / CL, ustep = gridDim.x / CL;
+    const uint16_t mc_mask = (uint16_t)((1u << CL) - 1);
 
     if (warp == 0) {
         // ------------------------------ TMA producer ------------------------------
         if (lane == 0) {
             int stage = 0; uint32_t phase = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int g = u / p.n_rtiles, r = u % p.n_rtiles;
+            for (int u = ubeg; u < n_units; u += ustep) {
+                const int g = u / n_rgroups, r = (u % n_rgroups) * CL + crank;
                 const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
                 for (int t = t0; t < t1; ++t) {
                     for (int kb = 0; kb < p.nk; ++kb) {
                         mbar_wait(&empty[stage], phase ^ 1);
                         unsigned char *sb = base + stage * STAGE_BYTES;
-                        if (p.dbg & 2) {
+                        if (CL > 1) {
+                            constexpr int HB = B_BYTES / CL;     // this CTA's share of B
+                            mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                            tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
+                            tma_load_2d(sb + A_BYTES, &map_xlo, kb * BK, r * BM, &full[stage]);
+                            if (p.dbg & 4) {                         // experiment: no multicast
+                                for (int hq = 0; hq < CL; ++hq) {
+                                    tma_load_2d(sb + 2 * A_BYTES + hq * HB, &map_yhi, kb * BK,
+                                                t * BN + hq * (BN / CL), &full[stage]);
+                                    tma_load_2d(sb + 2 * A_BYTES + B_BYTES + hq * HB, &map_ylo, kb * BK,
+                                                t * BN + hq * (BN / CL), &full[stage]);
+                                }
+                            } else {
+                            tma_load_2d_mc(sb + 2 * A_BYTES + crank * HB, &map_yhi, kb * BK,
+                                           t * BN + crank * (BN / CL), &full[stage], mc_mask);
+                            tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + crank * HB, &map_ylo, kb * BK,
+                                           t * BN + crank * (BN / CL), &full[stage], mc_mask);
+                            }
+                        } else if (p.dbg & 2) {
                             mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
                             tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
                             tma_load_2d(sb + 2 * A_BYTES, &map_yhi, kb * BK, t * BN, &full[stage]);
@@ -194,8 +249,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
         if (lane == 0) {
             int stage = 0; uint32_t phase = 0;
             int acc = 0; uint32_t aphase = 0;
-            for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-                const int g = u / p.n_rtiles;
+            for (int u = ubeg; u < n_units; u += ustep) {
+                const int g = u / n_rgroups;
                 const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
                 for (int t = t0; t < t1; ++t) {
                     mbar_wait(&tempty[acc], aphase ^ 1);
@@ -219,7 +274,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
                             mma_tf32(d_tmem, ahi + off, bhi + off, 1);
                             }
                         }
-                        mma_commit(&empty[stage]);
+                        if (CL > 1) mma_commit_mc(&empty[stage], mc_mask);
+                        else mma_commit(&empty[stage]);
                         if (++stage == STAGES) { stage = 0; phase ^= 1; }
                     }
                     mma_commit(&tfull[acc]);
@@ -239,8 +295,8 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
         float *cbd = cand_d + et;                    // column et of a [CB][128] array
         int32_t *cbj = cand_j + et;
         int acc = 0; uint32_t aphase = 0;
-        for (int u = blockIdx.x; u < n_units; u += gridDim.x) {
-            const int g = u / p.n_rtiles, r = u % p.n_rtiles;
+        for (int u = ubeg; u < n_units; u += ustep) {
+            const int g = u / n_rgroups, r = (u % n_rgroups) * CL + crank;
             const int t0 = g * p.group, t1 = min(t0 + p.group, p.n_ttiles);
             const int64_t i = (int64_t)r * BM + row_in_tile;
             const float xn = i < p.M ? __ldg(p.xn + i) : 0.0f;
@@ -315,6 +371,7 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
         }
     }
     __syncthreads();
+    if (CL > 1) cluster_sync_all();                      // no multicast may still target this CTA
     if (warp == 1) {
         fence_after();
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem_base) : "memory");
@@ -679,17 +736,28 @@ size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K) {
            al((size_t)tc::FB_CAP * tc::FB_GRID * tc::FB_LIST * 12) + al((size_t)tc::FB_CAP * 4) + 2048;
 }
 
-template <int KP>
+template <int KP, int CL>
 static cudaError_t launch_main(const CUtensorMap *maps, const tc::Params &p, int grid, cudaStream_t st) {
-    auto kern = tc::knn_tc_kernel<KP>;
+    auto kern = tc::knn_tc_kernel<KP, CL>;
     static bool attr = false;
     if (!attr) {
         cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
         if (e != cudaSuccess) return e;
         attr = true;
     }
-    kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(tc::NUM_THREADS);
+    cfg.dynamicSmemBytes = tc::SMEM_BYTES;
+    cfg.stream = st;
+    cudaLaunchAttribute attrs[1];
+    attrs[0].id = cudaLaunchAttributeClusterDimension;
+    attrs[0].val.clusterDim.x = CL;
+    attrs[0].val.clusterDim.y = 1;
+    attrs[0].val.clusterDim.z = 1;
+    cfg.attrs = attrs;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, maps[0], maps[1], maps[2], maps[3], p);
 }
 
 cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info) {
@@ -731,18 +799,19 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     CUtensorMap maps[4];
     if ((e = make_map(&maps[0], xhi, M, Dp, tc::BM)) != cudaSuccess) return e;
     if ((e = make_map(&maps[1], xlo, M, Dp, tc::BM)) != cudaSuccess) return e;
-    if ((e = make_map(&maps[2], yhi, N, Dp, tc::BN)) != cudaSuccess) return e;
-    if ((e = make_map(&maps[3], ylo, N, Dp, tc::BN)) != cudaSuccess) return e;
+    const int CL = tc::CLUSTER;                          // B box = the CTA's share of the ref tile
+    if ((e = make_map(&maps[2], yhi, N, Dp, tc::BN / CL)) != cudaSuccess) return e;
+    if ((e = make_map(&maps[3], ylo, N, Dp, tc::BN / CL)) != cudaSuccess) return e;
     tc::Params p;
     p.M = M; p.N = N; p.Dp = Dp; p.nk = Dp / tc::BK; p.n_rtiles = n_rtiles; p.n_ttiles = n_ttiles;
     p.n_groups = n_groups; p.group = group; p.xn = xn; p.yn = yn; p.pd = pd; p.pj = pj;
     p.dbg = getenv("GENRED_KNN_DBG") ? atoi(getenv("GENRED_KNN_DBG")) : 0;
     p.row_thr = row_thr;
     if ((e = cudaMemsetAsync(row_thr, 0x7f, (size_t)M * 4, st)) != cudaSuccess) return e;   // 3.4e38
-    const int n_units = n_groups * n_rtiles;
-    const int grid = std::min(n_units, a.num_sms);
+    const int n_units = n_groups * ((n_rtiles + CL - 1) / CL);
+    const int grid = std::min(n_units, a.num_sms / CL) * CL;
     if (a.ev_start) cudaEventRecord(a.ev_start, st);
-    e = KP == 16 ? launch_main<16>(maps, p, grid, st) : launch_main<32>(maps, p, grid, st);
+    e = KP == 16 ? launch_main<16, tc::CLUSTER>(maps, p, grid, st) : launch_main<32, tc::CLUSTER>(maps, p, grid, st);
     if (a.ev_stop) cudaEventRecord(a.ev_stop, st);
     if (e != cudaSuccess) return e;
     kernels += 1;
