@@ -745,6 +745,10 @@ static cudaError_t launch_main(const CUtensorMap *maps, const tc::Params &p, int
         if (e != cudaSuccess) return e;
         attr = true;
     }
+    if (CL == 1) {                                        // plain launch (no cluster scheduling)
+        kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], p);
+        return cudaGetLastError();
+    }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(grid);
     cfg.blockDim = dim3(tc::NUM_THREADS);
