@@ -106,6 +106,7 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                                    const uint32_t *geo_enc) {
     const Geo geo = kind == PACK_GAUSS_AUTO ? geo_decode(geo_enc, D, s) : Geo{};
     const int boff = kind == PACK_GAUSS_AUTO ? 2 * (D + 1) : 2 * D;
+    const bool lse = kind == PACK_LSE_HZ || kind == PACK_LSE_H;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
          p += (int64_t)gridDim.x * blockDim.x) {
         int lo = 0, hi = ncopies - 1;                          // last copy with dst <= p
@@ -115,6 +116,21 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
         }
         const RangeCopy c = copies[lo];
         float *rec = J + p * RS;
+        if (lse) {          // LSE records: (-y) pairs [+ h' hi/lo pairs]; invalid: y = +inf, h = -inf
+            for (int h = 0; h < 2; ++h) {
+                const int64_t j = c.js + 2 * (p - c.dst) + h;
+                const bool valid = j < c.je && j < N;
+                for (int d = 0; d < D; ++d) rec[2 * d + h] = valid ? -y[j * D + d] : -INFINITY;
+                if (kind == PACK_LSE_H) {
+                    const double hv = valid ? 1.4426950408889634074 * (double)b[j] : 0.0;
+                    const float hi = valid ? (float)hv : -INFINITY;
+                    rec[2 * D + h] = hi;
+                    rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
+                }
+            }
+            for (int k = 2 * D + (kind == PACK_LSE_H ? 4 : 0); k < RS; ++k) rec[k] = 0.0f;
+            continue;
+        }
         for (int h = 0; h < 2; ++h) {
             const int64_t j = c.js + 2 * (p - c.dst) + h;
             const bool valid = j < c.je && j < N;

@@ -96,7 +96,7 @@ genred_status validate(const genred_args *a, std::string &msg) {
     }
     if (a->n_ranges < 0) { msg = "n_ranges must be >= 0"; return GENRED_E_SHAPE; }
     if (a->n_ranges > 0) {
-        if (!(sum_pair)) { msg = "block-sparse ranges are supported for the Sum reductions"; return GENRED_E_UNSUPPORTED; }
+        if (!(sum_pair || lse_pair)) { msg = "block-sparse ranges are supported for Sum and LSE"; return GENRED_E_UNSUPPORTED; }
         if (!a->ranges_i || !a->slices || !a->ranges_j) { msg = "ranges_i / slices / ranges_j is NULL"; return GENRED_E_INVALID; }
         int64_t prev_ie = 0, prev_slice = 0;
         for (int64_t c = 0; c < a->n_ranges; ++c) {
@@ -248,6 +248,7 @@ genred_status cuda_fail(genred_ctx *ctx, cudaError_t e, const char *where) {
 
 // Block-sparse ranges (Sum family): gather every cluster's j-intervals into a contiguous,
 // tile-padded "range-packed" J, then one CTA per (cluster, row tile) streams only its tiles.
+// mode: 0..3 the Sum modes of sum_kernel, 4 = LSE
 genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st, int mode, int rmax) {
     const int64_t M = a->M, N = a->N;
     const int D = a->D, E = a->E;
@@ -277,7 +278,8 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         for (int64_t r = is; r < ie; r += RT) units.push_back({r, std::min(r + RT, ie), tile0, ntiles});
     }
     copies.push_back({cursor, 0, 0});
-    const int pk = mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
+    const int pk = mode == 4 ? (a->b ? PACK_LSE_H : PACK_LSE_HZ)
+                 : mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
     const int RS = pack_record_stride(pk, D, E);
     const size_t jbytes = al256((size_t)std::max<int64_t>(cursor, 1) * RS * 4);
     const size_t cbytes = al256(copies.size() * sizeof(RangeCopy));
@@ -295,14 +297,14 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         e = cudaMemcpyAsync(dunits, units.data(), units.size() * sizeof(RangeUnit), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "range table copy");
     // neutral outputs for every row first; cluster rows are overwritten by the kernel
-    const int fill_kind = mode == 2 ? 1 : 0;
+    const int fill_kind = mode == 4 ? 2 : (mode == 2 ? 1 : 0);
     const int fill_C = mode == 1 ? D : E;
-    e = launch_fill(fill_kind, M, fill_C, D, a->out, out_f64, a->out_grad, nullptr, nullptr, st);
+    e = launch_fill(fill_kind, M, fill_C, D, a->out, out_f64, a->out_grad, nullptr, a->lse_state, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fill kernel");
     int kernels = 1;
     float sc = 1.0f;
     double scale_grad = 0.0;
-    if (mode != 3) {
+    if (mode != 3 && mode != 4) {
         sc = (float)(sqrt(kLog2e) / a->scale);
         scale_grad = -2.0 / (a->scale * a->scale * (double)sc);
         e = launch_bbox(a->x, M, a->y, N, D, geo, st);
@@ -312,6 +314,26 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     e = launch_pack_ranges(pk, a->y, a->b, N, D, E, sc, dcopies, (int)copies.size(), cursor, J, st, geo);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "range pack kernel");
     kernels++;
+    if (mode == 4) {
+        LseLaunch L;
+        L.D = D; L.R = R; L.x = a->x; L.J = J; L.M = M; L.split = 1; L.tiles_per_split = 0;
+        L.ntiles = 0; L.negc = (float)(-kLog2e / a->scale); L.h_zero = a->b == nullptr;
+        L.out = a->out; L.out_f64 = out_f64; L.state = a->lse_state;
+        L.units = dunits; L.n_units = (int64_t)units.size();
+        int ctas = 0;
+        if (!units.empty()) {
+            prof_event(ctx, true, st);
+            e = launch_lse(L, st, &ctas);
+            prof_event(ctx, false, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "lse kernel (ranges)");
+            kernels++;
+        }
+        ctx->launches += kernels;
+        ctx->plan.split_j = 1; ctx->plan.rows_per_cta = (int32_t)RT; ctx->plan.ctas = ctas;
+        ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        return GENRED_OK;
+    }
     SumLaunch L;
     L.mode = mode; L.D = D; L.E = E; L.R = R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
     L.split = 1; L.tiles_per_split = 0; L.ntiles = 0; L.s = sc;
@@ -461,6 +483,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     }
 
     if (red == GENRED_LSE) {
+        if (a->n_ranges > 0) return eval_ranges(ctx, a, st, 4, lse_rows_per_thread_max(D));
         Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0);
         const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
         const int RS = pack_record_stride(pk, D, 1);

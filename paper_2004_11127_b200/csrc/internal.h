@@ -81,6 +81,8 @@ struct LseLaunch {
     int h_zero;               // h == 0 everywhere (skips a per-pair FADD)
     void *out; int out_f64;   // split == 1: a_i
     double *state;            // split == 1: optional M x 2 state; split > 1: split x M x 2 partials
+    const RangeUnit *units = nullptr;   // block-sparse ranges (device), or nullptr
+    int64_t n_units = 0;
 };
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
 int lse_occupancy(int D, int R);

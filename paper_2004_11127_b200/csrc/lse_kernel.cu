@@ -55,6 +55,7 @@ struct LseParams {
     void *out;
     int out_f64;
     double *state;
+    const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
 };
 
 struct LseRescale {
@@ -110,17 +111,25 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
-    const int64_t itile = blockIdx.x / p.split;
-    const int sp = (int)(blockIdx.x % p.split);
-    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
-    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-    const int nt = (int)(t1 - t0);
+    int64_t row0, row_end, t0;
+    int sp, nt;
+    if (p.units) {                                     // block-sparse: rows of one cluster
+        const RangeUnit u = p.units[blockIdx.x];
+        row0 = u.row0; row_end = u.row_end; t0 = u.tile0; nt = (int)u.ntiles; sp = 0;
+    } else {
+        const int64_t itile = blockIdx.x / p.split;
+        sp = (int)(blockIdx.x % p.split);
+        t0 = (int64_t)sp * p.tiles_per_split;
+        const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
+        nt = (int)(t1 - t0);
+        row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+        row_end = p.M;
+    }
 
     JRing<kStages> ring;
     ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
 
     const int ct = threadIdx.x;
-    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
     const float negc = p.negc;
     const float2 negc2 = dup2(negc);
     float xr[R][D];
@@ -130,7 +139,7 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        const bool ok = i < p.M;
+        const bool ok = i < row_end;
 #pragma unroll
         for (int d = 0; d < D; ++d) xr[r][d] = ok ? __ldg(p.x + i * D + d) : 0.0f;
         m[r] = kLseSentinel;
@@ -204,7 +213,7 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        if (i >= p.M) continue;
+        if (i >= row_end) continue;
         const double stot = s64[r] + (double)s32[r].x + (double)s32[r].y;
         if (p.split > 1) {
             p.state[((int64_t)sp * p.M + i) * 2 + 0] = (double)m[r];
@@ -237,9 +246,11 @@ static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
     LseParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.tiles_per_split = a.tiles_per_split;
     p.ntiles = a.ntiles; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
+    p.units = a.units;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
-    const int64_t grid = ((a.M + rows - 1) / rows) * a.split;
+    const int64_t grid = a.units ? a.n_units : ((a.M + rows - 1) / rows) * a.split;
     *ctas = (int)grid;
+    if (grid == 0) return cudaSuccess;
     kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
     return cudaGetLastError();
 }

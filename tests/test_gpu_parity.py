@@ -654,3 +654,29 @@ def test_ishard_rows_bitwise_equal_to_single_gpu(G):
     lf = host(G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
     lp = host(G.eval("sqdist", "lse", dev(x[1000:2000]), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
     np.testing.assert_array_equal(lp, lf[1000:2000])
+
+
+@pytest.mark.parametrize("with_h", [False, True])
+def test_block_sparse_ranges_lse(G, with_h):
+    x, bx, cx = _clustered(20, 150, 151)
+    y, by, cy = _clustered(25, 130, 152)
+    h = (np.random.default_rng(153).standard_normal(len(y)) * 2).astype(np.float32) if with_h else None
+    ri, sl, rj = _ranges(bx, cx, by, cy, 0.3)
+    # drop the first cluster (its rows must come out -inf); slices stay cumulative from 0
+    rj = rj[sl[0]:]; sl = sl[1:] - sl[0]; ri = ri[1:]
+    st = torch.empty((len(x), 2), dtype=torch.float64, device="cuda")
+    a = host(G.eval("sqdist", "lse", dev(x), dev(y), None if h is None else dev(h), scale=0.01,
+                    out_dtype="float64", lse_state=st, ranges=(ri, sl, rj)))
+    assert np.all(np.isneginf(a[:bx[1]]))
+    prev = 0
+    for c in range(len(ri)):
+        rows = np.arange(ri[c, 0], ri[c, 1])
+        idx = np.concatenate([np.arange(js, je) for js, je in rj[prev:sl[c]]]) if sl[c] > prev else np.zeros(0, int)
+        prev = sl[c]
+        if len(idx) == 0:
+            assert np.all(np.isneginf(a[rows])); continue
+        o, _ = oracle.lse(x[rows], y[idx], None if h is None else h[idx], eps=0.01)
+        assert_lse_parity(a[rows], o, rel=True, what=f"lse ranges c={c}")
+    s = host(st)
+    ok = ~np.isneginf(a)
+    np.testing.assert_allclose(math.log(2) * (s[ok, 0] + np.log2(s[ok, 1])), a[ok], rtol=0, atol=1e-12)
