@@ -19,9 +19,10 @@ __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *
                             int64_t N, int D, int E, float s, double hscale, int64_t npairs, int RS,
                             float *__restrict__ J, const uint32_t *geo_enc) {
     const float NEG_INF = -INFINITY;
-    if (kind == PACK_GAUSS_AUTO) {
+    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) {
         // Gaussian Sum records: [2D coords][w pair][2E signal]; expanded or direct per geo
         const Geo geo = geo_decode(geo_enc, D, s);
+        if (kind == PACK_GAUSS_DIRECT && geo.expanded) return;   // gauss_tc.cu takes this call
         for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
              p += (int64_t)gridDim.x * blockDim.x) {
             float *rec = J + p * RS;
@@ -80,7 +81,7 @@ __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *
 }
 
 int pack_record_stride(int kind, int D, int E) {
-    if (kind == PACK_GAUSS_AUTO) return record_stride(D + 1, E);
+    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) return record_stride(D + 1, E);
     if (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) return record_stride(D, 0);
     if (kind == PACK_LSE_H) return record_stride(D, 2);
     return record_stride(D, E);

@@ -23,6 +23,24 @@ __device__ __forceinline__ float2 mul2(float2 a, float2 b) { return __fmul2_rn(a
 __device__ __forceinline__ float2 fma2(float2 a, float2 b, float2 c) { return __ffma2_rn(a, b, c); }
 __device__ __forceinline__ float2 dup2(float a) { return make_float2(a, a); }
 
+// 2^u for u in [-24, 6] (the expanded path's range, geo.cuh) on the FP32 pipe: u = n + f with
+// n = rint(u) from the 1.5*2^23 shifter, f in [-1/2, 1/2], a degree-5 near-minimax polynomial
+// (max relative error 7.5e-8; 2.3e-7 through fp32 Horner, on par with MUFU.EX2), and n added
+// to the exponent field with one integer LEA.  Two values per packed FADD2/FFMA2.
+__device__ __forceinline__ float2 ex2_poly2(float2 u) {
+    const float2 shifter = dup2(12582912.0f);
+    const float2 t = add2(u, shifter);
+    const float2 n = add2(t, dup2(-12582912.0f));
+    const float2 f = fma2(n, dup2(-1.0f), u);                       // u - n, exact
+    float2 q = fma2(dup2(1.327647129073739e-03f), f, dup2(9.675541892647743e-03f));
+    q = fma2(q, f, dup2(5.550713092088699e-02f));
+    q = fma2(q, f, dup2(2.402212023735046e-01f));
+    q = fma2(q, f, dup2(6.931469440460205e-01f));
+    q = fma2(q, f, dup2(1.000000119209290e+00f));
+    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
+                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
+}
+
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }

@@ -6,6 +6,7 @@
 // genred_create fails with GENRED_E_CUDA.
 #include <math.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
@@ -32,6 +33,8 @@ struct genred_ctx {
     std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
     int *fallback_dev = nullptr;                               // k-NN rows rescanned exactly
     const uint32_t *geo_dev = nullptr;                         // Gaussian Sum bounding box
+    bool geo_tc = false;                                       // ... evaluated by gauss_tc.cu
+    bool gauss_tc = false;                                     // GENRED_GAUSS_TC=1 enables (opt-in)
     int geo_D = 0;
     float geo_s = 0.f;
     bool profiling = false;
@@ -428,17 +431,34 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         const int rmax = sum_rows_per_thread_max(mode, D, E);
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, mode, rmax);
         Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
-        const int pk = mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
+        // Gaussian Sum, one signal column, D <= 3: the tensor-core kernel (gauss_tc.cu) takes
+        // the expanded case; the FP32 kernel behind it only the direct one.  Both use the same
+        // j-split (in 512-j tiles), chosen for 128-row units on one CTA per SM.
+        // Opt-in (GENRED_GAUSS_TC=1): the north star keeps small D on the FP32/MUFU pipes (its
+        // row (c)); this path measured +6% over them, not enough to deviate.
+        const char *tcv = getenv("GENRED_GAUSS_TC");
+        const bool tc = mode == 0 && E == 1 && D <= 3 && (tcv ? atoi(tcv) != 0 : ctx->gauss_tc);
+        if (tc) {
+            const int64_t units_i = (M + gauss_tc_rows_per_unit() - 1) / gauss_tc_rows_per_unit();
+            int S = a->split_j > 0 ? (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, pl.ntiles))
+                                   : choose_split(units_i, pl.ntiles, ctx->num_sms, nullptr);
+            pl.R = rmax;
+            pl.tiles_per_split = (pl.ntiles + S - 1) / S;
+            pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
+        }
+        const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
-        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256);
+        const size_t tbytes = tc ? al256(gauss_tc_scratch_bytes(M, N)) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256 + tbytes);
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
         uint32_t *geo = (uint32_t *)((char *)ctx->scratch + jbytes + pbytes);
+        void *tscratch = (char *)ctx->scratch + jbytes + pbytes + 256;
         // parameter folding in fp64, rounded once to fp32 (R15, R18)
         float sc = 1.0f;
         double scale_grad = 0.0;
@@ -453,6 +473,20 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
         }
+        int ctas = 0;
+        if (tc) {
+            GaussTcLaunch T;
+            T.x = a->x; T.y = a->y; T.b = a->b; T.geo = geo; T.M = M; T.N = N; T.D = D; T.s = sc;
+            T.split = pl.split; T.tiles_per_split = 2 * pl.tiles_per_split; T.scale_sum = 1.0;
+            T.out = a->out; T.out_f64 = out_f64; T.part = part; T.scratch = tscratch;
+            T.num_sms = ctx->num_sms;
+            T.ev_start = prof_event(ctx, true, nullptr, true);
+            T.ev_stop = prof_event(ctx, false, nullptr, true);
+            int tk = 0;
+            e = launch_gauss_tc(T, st, &ctas, &tk);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "tensor-core Gaussian sum");
+            kernels += tk;
+        }
         e = launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         SumLaunch L;
@@ -460,10 +494,12 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
-        int ctas = 0;
-        prof_event(ctx, true, st);
-        e = launch_sum(L, st, &ctas);
-        prof_event(ctx, false, st);
+        L.direct_only = tc ? 1 : 0;
+        int sctas = 0;
+        if (!tc) prof_event(ctx, true, st);
+        e = launch_sum(L, st, &sctas);
+        if (!tc) prof_event(ctx, false, st);
+        if (!tc) ctas = sctas;
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
         if (pl.split > 1) {
             const int cols_sum = (mode == 1) ? 0 : E;
@@ -477,6 +513,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
         ctx->geo_dev = mode != 3 ? geo : nullptr;
+        ctx->geo_tc = tc;
         ctx->geo_D = D;
         ctx->geo_s = sc;
         return GENRED_OK;
@@ -640,6 +677,7 @@ genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
     cudaSetDevice(cuda_device);
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (const char *v = getenv("GENRED_GAUSS_TC")) ctx->gauss_tc = atoi(v) != 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
     cudaSetDevice(prev);
@@ -766,7 +804,7 @@ genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
     *plan = ctx->plan;
     plan->fallback_rows = -1;
     if (ctx->plan.path == 0 && ctx->geo_dev && geo_expanded_host(ctx->geo_dev, ctx->geo_D, ctx->geo_s))
-        plan->path = 2;                                        // expanded form + FMA-pipe exp2
+        plan->path = ctx->geo_tc ? 3 : 2;                      // expanded form (tensor cores / FP32)
     if (ctx->plan.path == 1 && ctx->fallback_dev) {
         int n = -1;
         if (cudaMemcpy(&n, ctx->fallback_dev, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {

@@ -16,7 +16,7 @@ constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
 
 enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4,
-                PACK_GAUSS_AUTO = 5 };
+                PACK_GAUSS_AUTO = 5, PACK_GAUSS_DIRECT = 6 };
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
 // kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
@@ -26,6 +26,8 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 // which contribute nothing.
 // PACK_GAUSS_AUTO (Gaussian Sum): decodes the bounding box `geo` (geo.cuh) and writes either the
 // expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-s y, 0, b).
+// PACK_GAUSS_DIRECT: the direct records when the box rules the expanded form out, else nothing
+// (the tensor-core kernel, gauss_tc.cu, takes the expanded case).
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
                         float s, double hscale, int64_t npairs, float *J, cudaStream_t st,
                         const uint32_t *geo = nullptr);
@@ -66,6 +68,7 @@ struct SumLaunch {
     double *part;             // split > 1: split x M x C fp64 partials
     const RangeUnit *units;   // block-sparse ranges (device), or nullptr
     int64_t n_units;
+    int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
 int sum_occupancy(int mode, int D, int E, int R);
@@ -142,6 +145,28 @@ struct KnnTcInfo {
 int knn_tc_group();
 size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K);
 cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info);
+
+// Gaussian Sum (MODE 0, E = 1, D <= 3) with the exponent contraction on the tensor cores
+// (gauss_tc.cu).  Runs when the box allows the expanded form (device-side decision, geo.cuh),
+// else exits; j-splits of tiles_per_split 512-j tiles, partials in the sum_finalize layout.
+struct GaussTcLaunch {
+    const float *x, *y, *b;
+    const uint32_t *geo;
+    int64_t M, N;
+    int D;
+    float s;
+    int split;
+    int64_t tiles_per_split;           // in 256-j tiles (= 2 x the 512-j tiles of the FP32 plan)
+    double scale_sum;
+    void *out; int out_f64;
+    double *part;
+    void *scratch;                     // gauss_tc_scratch_bytes(M, N) bytes
+    int num_sms;
+    cudaEvent_t ev_start, ev_stop;     // optional: recorded around the tcgen05 kernel
+};
+size_t gauss_tc_scratch_bytes(int64_t M, int64_t N);
+int gauss_tc_rows_per_unit();
+cudaError_t launch_gauss_tc(const GaussTcLaunch &a, cudaStream_t st, int *ctas, int *kernels);
 
 // Deterministic (fixed-order) merges of split-j partials.
 cudaError_t launch_sum_finalize(const double *part, int split, int64_t M, int C, int cols_sum,

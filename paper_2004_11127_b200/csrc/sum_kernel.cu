@@ -60,25 +60,8 @@ struct SumParams {
     float *out_grad;
     double *part;
     const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
+    int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
 };
-
-// 2^u for u in [-24, 6] (the expanded path's range, geo.cuh) on the FP32 pipe: u = n + f with
-// n = rint(u) from the 1.5*2^23 shifter, f in [-1/2, 1/2], a degree-5 near-minimax polynomial
-// (max relative error 7.5e-8; 2.3e-7 through fp32 Horner, on par with MUFU.EX2), and n added
-// to the exponent field with one integer LEA.  Two values per packed FADD2/FFMA2.
-__device__ __forceinline__ float2 ex2_poly2(float2 u) {
-    const float2 shifter = dup2(12582912.0f);
-    const float2 t = add2(u, shifter);
-    const float2 n = add2(t, dup2(-12582912.0f));
-    const float2 f = fma2(n, dup2(-1.0f), u);                       // u - n, exact
-    float2 q = fma2(dup2(1.327647129073739e-03f), f, dup2(9.675541892647743e-03f));
-    q = fma2(q, f, dup2(5.550713092088699e-02f));
-    q = fma2(q, f, dup2(2.402212023735046e-01f));
-    q = fma2(q, f, dup2(6.931469440460205e-01f));
-    q = fma2(q, f, dup2(1.000000119209290e+00f));
-    return make_float2(__int_as_float(__float_as_int(q.x) + (__float_as_int(t.x) << 23)),
-                       __int_as_float(__float_as_int(q.y) + (__float_as_int(t.y) << 23)));
-}
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
 // 14.90 with every exp on MUFU (M = N = 1e6, B200): the packed FFMA2s of the expanded form read
@@ -326,12 +309,14 @@ sum_kernel(const SumParams p) {
     }
 
     JRing<kStages> ring;
-    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
+        if (MODE == 0 && p.direct_only && geo.expanded) return;   // gauss_tc.cu took this call
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
         if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, row_end, sp, geo);
         else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
     } else {
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
         Geo geo{};
         sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
     }
@@ -354,6 +339,7 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.s = a.s;
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = a.units;
+    p.direct_only = a.direct_only;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
     const int64_t grid = a.units ? a.n_units : itiles * a.split;

@@ -445,6 +445,32 @@ def test_gauss_sum_expanded_and_direct_paths(G, case):
     assert_sum_parity(host(a), o, den, what=f"gauss {case}")
 
 
+@pytest.mark.parametrize("M,N,D,signed,split", [
+    (1000, 777, 3, False, 0),        # ragged row tile and j tile
+    (128, 256, 3, True, 1),          # exactly one tile
+    (1, 1, 3, False, 0),             # degenerate
+    (5, 100000, 3, True, 0),         # one row tile, long j axis (split)
+    (40000, 3000, 2, True, 0),
+    (3000, 4100, 1, False, 7),       # forced split, D = 1
+    (20000, 20000, 3, True, 3),
+])
+def test_gauss_tc_path(G, monkeypatch, M, N, D, signed, split):
+    """Opt-in Gaussian Sum with the exponent on the tensor cores (gauss_tc.cu, path 3) against the
+    oracle, and the default FP32 expanded kernel (path 2) on the same inputs."""
+    x = synth.uniform3(M, 91)[:, :D].copy(); y = synth.uniform3(N, 92)[:, :D].copy()
+    b = synth.signal(N, 93, signed=signed)
+    monkeypatch.setenv("GENRED_GAUSS_TC", "1")                 # opt-in path
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split, out_dtype="float64")
+    plan = G.last_plan()
+    assert plan["path"] == 3, plan
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+    assert_sum_parity(host(a), o, den, what=f"gauss tc {M}x{N} D{D}")
+    monkeypatch.setenv("GENRED_GAUSS_TC", "0")
+    a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split, out_dtype="float64")
+    assert G.last_plan()["path"] == 2
+    assert_sum_parity(host(a2), o, den, what="gauss fp32 expanded")
+
+
 @pytest.mark.parametrize("formula", ["gauss_gradx", "gauss_sum_gradx"])
 @pytest.mark.parametrize("case", ["expanded", "far_offset", "direct", "E2_g"])
 def test_gradient_expanded_and_direct_paths(G, formula, case):
