@@ -66,6 +66,9 @@ def workload(cid: int) -> dict:
                     out_dtype="float32")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
+    if cid == 6:   # Cedge: N tiny -> 12 B of x read + 4 B of a written per row (HBM-bound)
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=None, mufu=None, out_dtype="float32",
+                    hbm=True)
     if cid == 4:   # k-NN, D=784: 3xTF32 tcgen05 contraction (tensor-bound)
         return dict(cfg=c, formula="sqdist", reduction="argkmin", fp32=None, mufu=None,
                     out_dtype="float32")
@@ -246,7 +249,14 @@ def main() -> None:
                     help="testing only: gloo lets several ranks share one GPU (--one-device)")
     ap.add_argument("--one-device", action="store_true", help="testing only: every rank uses cuda:0")
     ap.add_argument("--no-cpu", action="store_true")
+    ap.add_argument("--edge-n", type=int, default=0, help="config 6 (Cedge): N (default 8)")
     args = ap.parse_args()
+    if args.edge_n:
+        if args.config != 6:
+            raise SystemExit("--edge-n applies to --config 6")
+        import dataclasses
+        synth.CONFIGS[6] = dataclasses.replace(synth.CONFIGS[6], N=args.edge_n,
+                                               name=f"Cedge Gaussian Sum M=2^28 N={args.edge_n} D=3 E=1 sigma=0.5 (HBM-bound)")
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -362,6 +372,18 @@ def main() -> None:
                     "share_of_step": kmean / ms_step if world == 1 else None,
                     "peak_basis": f"bf16_tflops {bf16:.1f} (MEASURED_PEAKS.json, burst) x 0.5 (tf32/bf16 nominal)",
                     "flops_per_launch": flops, "exact_fp32_equivalent_flops": 2.0 * Ml * N * c.D}
+    elif w.get("hbm"):
+        # HBM-bound edge: algorithmic bytes = x read (D fp32) + a written (E fp32) per row, plus
+        # the packed j-records once (L2-resident afterwards)
+        hbm = float(peaks.get("hbm_gbs", 6541.0))
+        nbytes = Ml * (c.D + c.E) * 4 + N * (c.D + 1 + c.E) * 4
+        achieved_b = nbytes / (kmean * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "achieved": achieved_b, "peak": hbm, "unit": "GB/s",
+                    "frac": achieved_b / hbm, "traffic": traffic,
+                    "kernel": "gauss/sum pair loop (direct form, tiny N)", "kernel_ms": kmean,
+                    "share_of_step": kmean / ms_step if world == 1 else None,
+                    "peak_basis": "HBM copy bandwidth (MEASURED_PEAKS.json)",
+                    "bytes_per_launch": nbytes}
     else:
         peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
         achieved = Ml * N / (kmean * 1e-3)
@@ -417,7 +439,7 @@ def main() -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         oracle.set_num_threads(os.cpu_count() or 1)
-        nrows = args.cpu_rows or max(16, min(M, int(1e10 // (N * (c.D if argk else 1)))))
+        nrows = args.cpu_rows or max(16, min(M, 4_000_000, int(1e10 // (N * (c.D if argk else 1)))))
         rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
         gpu_rows = (out_idx if argk else out).cpu().numpy()[rows]
         cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=gpu_rows)
@@ -431,7 +453,8 @@ def main() -> None:
                        "dist": args.dist if w["reduction"] != "lse" else f"x {c.x_dist}, y {c.y_dist}",
                        "b": "U[0,1)" if b is not None else None,
                        "parallelism": f"ishard{world}" if world > 1 else "single",
-                       "l2": "inputs larger than L2 (280 MB vs 126 MB); no flush" if c.cid == 5 else
+                       "l2": ("inputs larger than L2 (280 MB vs 126 MB); no flush" if c.cid == 5 else
+                              "x larger than L2 (3.2 GB vs 126 MB); no flush") if c.cid in (5, 6) else
                              "inputs re-read from HBM/L2 each step; no flush",
                        "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"],
                        "ctas": plan["ctas"], "K": c.K if argk else None,

@@ -104,11 +104,15 @@ struct JRing {
     int nt;                    // tiles in the range
     int tile_floats;
     uint32_t bytes;
+    uint32_t last_bytes;       // bytes of the range's last tile (a partial tile when N is small)
+
+    __device__ __forceinline__ uint32_t tile_bytes(int k) const { return k == nt - 1 ? last_bytes : bytes; }
 
     __device__ __forceinline__ void init(unsigned char *smem, int tile_floats_, const float *src_,
-                                         int nt_, int nwarps) {
+                                         int nt_, int nwarps, uint32_t last_bytes_ = 0) {
         tile_floats = tile_floats_;
         bytes = (uint32_t)tile_floats_ * 4u;
+        last_bytes = last_bytes_ ? last_bytes_ : bytes;
         tiles = reinterpret_cast<float *>(smem);
         full = reinterpret_cast<uint64_t *>(smem + (size_t)STAGES * bytes);
         empty = full + STAGES;
@@ -121,8 +125,8 @@ struct JRing {
             }
             fence_barrier_init();
             for (int k = 0; k < STAGES && k < nt; ++k) {
-                mbar_arrive_expect_tx(&full[k], bytes);
-                bulk_g2s(tiles + k * tile_floats, src + (int64_t)k * tile_floats, bytes, &full[k]);
+                mbar_arrive_expect_tx(&full[k], tile_bytes(k));
+                bulk_g2s(tiles + k * tile_floats, src + (int64_t)k * tile_floats, tile_bytes(k), &full[k]);
             }
         }
         __syncthreads();
@@ -138,8 +142,9 @@ struct JRing {
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
         if (threadIdx.x == 0 && k + STAGES < nt) {
             mbar_wait(&empty[s], (k / STAGES) & 1);          // every warp is done with tile k
-            mbar_arrive_expect_tx(&full[s], bytes);
-            bulk_g2s(tiles + s * tile_floats, src + (int64_t)(k + STAGES) * tile_floats, bytes, &full[s]);
+            const uint32_t nb = tile_bytes(k + STAGES);
+            mbar_arrive_expect_tx(&full[s], nb);
+            bulk_g2s(tiles + s * tile_floats, src + (int64_t)(k + STAGES) * tile_floats, nb, &full[s]);
         }
     }
     static constexpr int smem_bytes(int tile_floats_) { return STAGES * tile_floats_ * 4 + 2 * STAGES * 8; }

@@ -1,0 +1,161 @@
+// edge_kernel.cu -- the Gaussian Genred Sum at the HBM-bound edge: N tiny (N <= 64), M huge
+// (SURVEY.md Sec. 8(d) row Cedge; Eq. 1).
+//
+// With a handful of j's the pair loop is a few dozen FP32 operations per row, so the kernel is
+// bound by streaming x in (D floats per row) and a out (one float per row).  The generic pair-loop
+// kernel spends a CTA per 1024 rows and pays its whole set-up latency (mbarrier init, j-tile
+// copy, x loads, store) once per CTA; here instead:
+//   * persistent CTAs (a few per SM) keep the N packed j-records in shared memory for the whole
+//     launch and walk row tiles c, c + grid, ...;
+//   * each 1024-row x tile (contiguous, 1024 * D * 4 bytes) arrives by one cp.async.bulk into a
+//     4-stage shared-memory ring completing on mbarriers, so up to 4 tiles per CTA are in flight
+//     (the bytes in flight per SM, not the thread count, set the achieved HBM bandwidth);
+//   * a thread evaluates its rows from shared memory in the direct form (no bounding-box pass
+//     over x, which would be a second full read) and stores a with coalesced writes.
+// The j-records are the PACK_GAUSS_AUTO direct records (-s y_j pairs, w slot, b_j pairs).
+#include <math.h>
+
+#include <algorithm>
+
+#include "device.cuh"
+#include "internal.h"
+
+namespace genred {
+namespace edge {
+
+constexpr int kRowsPerTile = 1024;
+constexpr int kThreads = 256;
+constexpr int kRows = kRowsPerTile / kThreads;      // rows per thread per tile
+constexpr int kStages = 4;
+constexpr int kMaxPairs = 32;                       // N <= 64
+
+template <int D>
+__global__ void __launch_bounds__(kThreads)
+sum_edge_kernel(const float *__restrict__ x, const float *__restrict__ J, int npairs, int RS,
+                int64_t M, float s, double scale, void *out, int out_f64) {
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    float *xt = reinterpret_cast<float *>(smem_raw);                         // [kStages][1024*D]
+    float *jr = xt + kStages * kRowsPerTile * D;                             // [npairs][RS]
+    uint64_t *full = reinterpret_cast<uint64_t *>(jr + kMaxPairs * 12 + 4);
+    const int64_t ntiles = (M + kRowsPerTile - 1) / kRowsPerTile;
+    const int64_t nfull = M / kRowsPerTile;           // tiles copied whole (16-byte multiple)
+    constexpr uint32_t kTileBytes = kRowsPerTile * D * 4;
+
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kStages; ++k) mbar_init(&full[k], 1);
+        fence_barrier_init();
+    }
+    for (int k = threadIdx.x; k < npairs * RS; k += kThreads) jr[k] = J[k];
+    __syncthreads();
+    // prologue: the first kStages tiles of this CTA (whole tiles only; a partial last tile is
+    // read straight from global memory, never past the end of x)
+    if (threadIdx.x == 0) {
+        for (int k = 0; k < kStages; ++k) {
+            const int64_t t = blockIdx.x + (int64_t)k * gridDim.x;
+            if (t < nfull) {
+                mbar_arrive_expect_tx(&full[k], kTileBytes);
+                bulk_g2s(xt + k * kRowsPerTile * D, x + t * kRowsPerTile * D, kTileBytes, &full[k]);
+            }
+        }
+    }
+    int k = 0;
+    for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x, ++k) {
+        const int st = k % kStages;
+        const int64_t row0 = t * kRowsPerTile;
+        float xr[kRows][D];
+        if (t < nfull) {
+            mbar_wait(&full[st], (k / kStages) & 1);
+            const float *xs = xt + st * kRowsPerTile * D;
+#pragma unroll
+            for (int r = 0; r < kRows; ++r)
+#pragma unroll
+                for (int d = 0; d < D; ++d) xr[r][d] = s * xs[(r * kThreads + threadIdx.x) * D + d];
+        } else {
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                const int64_t i = row0 + r * kThreads + threadIdx.x;
+#pragma unroll
+                for (int d = 0; d < D; ++d) xr[r][d] = i < M ? s * __ldg(x + i * D + d) : 0.0f;
+            }
+        }
+        __syncthreads();                                  // every thread is done with stage st
+        if (threadIdx.x == 0) {
+            const int64_t tn = t + (int64_t)kStages * gridDim.x;
+            if (tn < nfull) {
+                mbar_arrive_expect_tx(&full[st], kTileBytes);
+                bulk_g2s(xt + st * kRowsPerTile * D, x + tn * kRowsPerTile * D, kTileBytes, &full[st]);
+            }
+        }
+        float2 acc[kRows];
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) acc[r] = make_float2(0.f, 0.f);
+#pragma unroll 4
+        for (int p = 0; p < npairs; ++p) {
+            const float *rec = jr + p * RS;
+            float2 ny[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) ny[d] = make_float2(rec[2 * d], rec[2 * d + 1]);
+            const float2 bv = make_float2(rec[2 * D + 2], rec[2 * D + 3]);
+#pragma unroll
+            for (int r = 0; r < kRows; ++r) {
+                float2 dd = add2(dup2(xr[r][0]), ny[0]);
+                float2 q = mul2(dd, dd);
+#pragma unroll
+                for (int d = 1; d < D; ++d) {
+                    dd = add2(dup2(xr[r][d]), ny[d]);
+                    q = fma2(dd, dd, q);                  // |x' - y'|^2 (direct form)
+                }
+                const float2 e = make_float2(ex2(-q.x), ex2(-q.y));
+                acc[r] = fma2(e, bv, acc[r]);
+            }
+        }
+#pragma unroll
+        for (int r = 0; r < kRows; ++r) {
+            const int64_t i = row0 + r * kThreads + threadIdx.x;
+            if (i >= M) continue;
+            const double v = ((double)acc[r].x + (double)acc[r].y) * scale;
+            if (out_f64) ((double *)out)[i] = v;
+            else ((float *)out)[i] = (float)v;
+        }
+    }
+}
+
+template <int D>
+static cudaError_t run(const float *x, const float *J, int npairs, int RS, int64_t M, float s,
+                       double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas) {
+    auto kern = sum_edge_kernel<D>;
+    const int smem = kStages * kRowsPerTile * D * 4 + (kMaxPairs * 12 + 4) * 4 + kStages * 8 + 64;
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    int occ = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);
+    const int64_t ntiles = (M + kRowsPerTile - 1) / kRowsPerTile;
+    const int grid = (int)std::min<int64_t>(ntiles, (int64_t)num_sms * std::max(occ, 1));
+    *ctas = grid;
+    kern<<<grid, kThreads, smem, st>>>(x, J, npairs, RS, M, s, scale, out, out_f64);
+    return cudaGetLastError();
+}
+
+}  // namespace edge
+
+int sum_edge_max_n() { return 2 * edge::kMaxPairs; }
+
+cudaError_t launch_sum_edge(const float *x, const float *J, int64_t N, int D, int RS, int64_t M, float s,
+                            double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas) {
+    if (M == 0) { *ctas = 0; return cudaSuccess; }
+    if (N > 2 * edge::kMaxPairs || RS > 12) return cudaErrorInvalidValue;
+    const int npairs = (int)((N + 1) / 2);
+    switch (D) {
+        case 1: return edge::run<1>(x, J, npairs, RS, M, s, scale, out, out_f64, num_sms, st, ctas);
+        case 2: return edge::run<2>(x, J, npairs, RS, M, s, scale, out, out_f64, num_sms, st, ctas);
+        case 3: return edge::run<3>(x, J, npairs, RS, M, s, scale, out, out_f64, num_sms, st, ctas);
+        case 4: return edge::run<4>(x, J, npairs, RS, M, s, scale, out, out_f64, num_sms, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+
+}  // namespace genred

@@ -152,6 +152,8 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
 }
 
 // Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.
+constexpr int64_t kDirectMaxN = 64;          // Gaussian Sum: N at or below -> direct form, no bbox
+
 int choose_split(int64_t itiles, int64_t ntiles, int64_t slots, double *eff_out) {
     int best = 1;
     double best_score = -1.0, best_eff = 0.0;
@@ -468,7 +470,12 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             scale_grad = -2.0 / (sig * sig * (double)sc);        // (x - y) = (x' - y') / s
         }
         int kernels = 2;
-        if (mode != 3) {
+        // Tiny N (the HBM-bound edge, SURVEY.md 8(d) Cedge): the pair loop is a few FP32 ops per
+        // row, so the direct form is free and the bounding-box pass over x (a second full read
+        // of x) is skipped; geo = nullptr selects the direct form on the device.
+        const bool tiny_n = N <= kDirectMaxN && !tc;
+        if (tiny_n) geo = nullptr;
+        if (mode != 3 && !tiny_n) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
@@ -489,12 +496,28 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         }
         e = launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
+        if (tiny_n && mode == 0 && E == 1 && D <= 4 && N <= sum_edge_max_n() &&
+            ((uintptr_t)a->x & 15) == 0) {
+            // HBM-bound edge: persistent CTAs, bulk-copied x tiles, j-records resident in smem
+            prof_event(ctx, true, st);
+            e = launch_sum_edge(a->x, J, N, D, RS, M, sc, 1.0, a->out, out_f64, ctx->num_sms, st, &ctas);
+            prof_event(ctx, false, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "edge sum kernel");
+            ctx->launches += kernels;
+            ctx->plan.split_j = 1; ctx->plan.rows_per_cta = 1024; ctx->plan.ctas = ctas;
+            ctx->plan.kernels = kernels; ctx->plan.path = 0; ctx->plan.tile_j = (int32_t)N;
+            ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+            ctx->geo_dev = nullptr;
+            ctx->geo_tc = false;
+            return GENRED_OK;
+        }
         SumLaunch L;
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
         L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
         L.direct_only = tc ? 1 : 0;
+        L.npairs_valid = (N + 1) / 2;
         int sctas = 0;
         if (!tc) prof_event(ctx, true, st);
         e = launch_sum(L, st, &sctas);

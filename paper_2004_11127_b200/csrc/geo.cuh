@@ -31,8 +31,15 @@ struct Geo {
 // of x.  The centre comes from y alone, so every i-shard of the same problem (same y, different
 // x rows) gets the same centre and, when its rows fit the same radius, bitwise the same
 // arithmetic as the single-GPU run; the radius test covers both clouds.
+// lohi == nullptr: no box was reduced (tiny N, see genred_abi.cu) -> the direct form.
 __device__ __forceinline__ Geo geo_decode(const uint32_t *lohi, int D, float s) {
     Geo g;
+    if (!lohi) {
+#pragma unroll
+        for (int d = 0; d < 8; ++d) g.c[d] = 0.0f;
+        g.expanded = false;
+        return g;
+    }
     float r2 = 0.0f;
     bool ok = true;
 #pragma unroll

@@ -69,6 +69,7 @@ struct SumLaunch {
     const RangeUnit *units;   // block-sparse ranges (device), or nullptr
     int64_t n_units;
     int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
+    int64_t npairs_valid = (int64_t)1 << 60;   // record pairs holding real j (ceil(N/2))
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
 int sum_occupancy(int mode, int D, int E, int R);
@@ -167,6 +168,12 @@ struct GaussTcLaunch {
 size_t gauss_tc_scratch_bytes(int64_t M, int64_t N);
 int gauss_tc_rows_per_unit();
 cudaError_t launch_gauss_tc(const GaussTcLaunch &a, cudaStream_t st, int *ctas, int *kernels);
+
+// Gaussian Sum at the HBM-bound edge (edge_kernel.cu): N <= sum_edge_max_n(), D <= 4, E = 1,
+// x 16-byte aligned; J = the PACK_GAUSS_AUTO direct records (geo = nullptr).
+int sum_edge_max_n();
+cudaError_t launch_sum_edge(const float *x, const float *J, int64_t N, int D, int RS, int64_t M, float s,
+                            double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas);
 
 // Deterministic (fixed-order) merges of split-j partials.
 cudaError_t launch_sum_finalize(const double *part, int split, int64_t M, int C, int cols_sum,

@@ -61,6 +61,8 @@ struct SumParams {
     double *part;
     const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
     int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
+    int64_t npairs_valid;     // record pairs holding real j (dense launches): the last tile's
+                              // loop stops there (tiny N: HBM-bound edge, SURVEY.md 8(d) Cedge)
 };
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
@@ -74,7 +76,7 @@ constexpr bool kPolyShare = false;
 // leaves the MUFU pipe (16 ex2/clk/SM) as the only bound; the row factor 2^(-|x'|^2) is applied
 // in fp64 at the end.
 template <int MODE, int D, int E, int R, bool XP>
-__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt,
+__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt, int64_t t0,
                                          int64_t row0, int64_t row_end, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
@@ -128,7 +130,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-        for (int pp2 = 0; pp2 < Cfg::PAIRS; pp2 += 2) {
+        // pairs of this tile that hold real j (rounded up to the unroll of 2; the rest is padding)
+        const int64_t left = p.npairs_valid - (t0 + k) * (int64_t)Cfg::PAIRS;
+        const int np = left >= Cfg::PAIRS ? Cfg::PAIRS : (int)((left + 1) & ~int64_t(1));
+        for (int pp2 = 0; pp2 < np; pp2 += 2) {
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
             const int pp = pp2 + hh;
@@ -286,6 +291,17 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     }
 }
 
+// Bytes of the CTA's last j-tile that hold real records (0 = the whole tile): with a tiny N the
+// only tile is mostly padding, and copying it whole would double the data moved per CTA.
+template <class Cfg>
+__device__ __forceinline__ uint32_t last_tile_bytes(const SumParams &p, int64_t t0, int nt) {
+    if (nt <= 0) return 0;
+    const int64_t left = p.npairs_valid - (t0 + nt - 1) * (int64_t)Cfg::PAIRS;
+    if (left >= Cfg::PAIRS) return 0;
+    const int64_t np = left <= 0 ? 2 : ((left + 1) & ~int64_t(1));
+    return (uint32_t)(np * Cfg::RS * 4);
+}
+
 template <int MODE, int D, int E, int R>
 __global__ void __launch_bounds__(kThreads, (((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ||
                                             ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && E == 1 && R == 2)) ? 3 : 2)
@@ -312,13 +328,15 @@ sum_kernel(const SumParams p) {
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
         if (MODE == 0 && p.direct_only && geo.expanded) return;   // gauss_tc.cu took this call
-        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
-        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, row0, row_end, sp, geo);
-        else sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps,
+                  last_tile_bytes<Cfg>(p, t0, nt));
+        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, t0, row0, row_end, sp, geo);
+        else sum_body<MODE, D, E, R, false>(p, ring, nt, t0, row0, row_end, sp, geo);
     } else {
-        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps,
+                  last_tile_bytes<Cfg>(p, t0, nt));
         Geo geo{};
-        sum_body<MODE, D, E, R, false>(p, ring, nt, row0, row_end, sp, geo);
+        sum_body<MODE, D, E, R, false>(p, ring, nt, t0, row0, row_end, sp, geo);
     }
 }
 
@@ -340,6 +358,7 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = a.units;
     p.direct_only = a.direct_only;
+    p.npairs_valid = a.units ? (int64_t)1 << 60 : a.npairs_valid;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
     const int64_t grid = a.units ? a.n_units : itiles * a.split;

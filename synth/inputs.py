@@ -50,6 +50,9 @@ CONFIGS = {
               1.0, K=10, x_dist="MNIST784", y_dist="MNIST784"),
     5: Config(5, "C5 Gaussian Sum M=N=1e7 D=3 E=1 sigma=0.5 (i-sharded 1/2/4/8)", "gauss", "sum",
               10_000_000, 10_000_000, 3, 1, 0.5),
+    # Cedge: the memory-bound low-N, high-M edge; N in {1, 2, 4, 8, 16, 32}
+    6: Config(6, "Cedge Gaussian Sum M=2^28 N=8 D=3 E=1 sigma=0.5 (HBM-bound)", "gauss", "sum",
+              1 << 28, 8, 3, 1, 0.5),
 }
 
 
