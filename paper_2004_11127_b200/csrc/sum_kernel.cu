@@ -30,6 +30,9 @@ namespace genred {
 #ifndef GENRED_GRAD_R
 #define GENRED_GRAD_R 2
 #endif
+#ifndef GENRED_GRAD_HH
+#define GENRED_GRAD_HH 2
+#endif
 
 template <int MODE, int D, int E>
 struct SumCfg {
@@ -81,6 +84,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
     constexpr bool POLY = kPolyShare && XP && R == 4;
+    constexpr int HH = (MODE == 1 || MODE == 2) ? GENRED_GRAD_HH : 2;   // record pairs per iteration
     const int ct = threadIdx.x;
     float xr[R][D];
     float gr[R][E];
@@ -132,10 +136,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         const float *tile = ring.acquire(k);
         // pairs of this tile that hold real j (rounded up to the unroll of 2; the rest is padding)
         const int64_t left = p.npairs_valid - (t0 + k) * (int64_t)Cfg::PAIRS;
-        const int np = left >= Cfg::PAIRS ? Cfg::PAIRS : (int)((left + 1) & ~int64_t(1));
-        for (int pp2 = 0; pp2 < np; pp2 += 2) {
+        const int np = left >= Cfg::PAIRS ? Cfg::PAIRS : (int)((left + HH - 1) / HH * HH);
+        for (int pp2 = 0; pp2 < np; pp2 += HH) {
 #pragma unroll
-        for (int hh = 0; hh < 2; ++hh) {
+        for (int hh = 0; hh < HH; ++hh) {
             const int pp = pp2 + hh;
             float f[RS];
 #pragma unroll
@@ -151,7 +155,8 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
             if constexpr (XP) {
                 const float2 w = make_float2(f[2 * D], f[2 * D + 1]);              // -|y'|^2
                 // (a coordinate-major order over the rows, meant to share y'_d through the register
-                // reuse cache, measured 0.8% slower: ptxas schedules either way)
+                // reuse cache, measured 0.8% slower for the Sum and no change for the fused
+                // gradient: ptxas schedules either way)
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
                     float2 u = fma2(dup2(xr[r][0]), ny[0], w);
@@ -183,6 +188,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                             }
                             s0[r] = add2(s0[r], wt);
                         }
+                        // (two scalar FFMAs instead of this 3-register-pair FFMA2 measured 2% slower)
 #pragma unroll
                         for (int d = 0; d < D; ++d) accg[r][d] = fma2(wt, ny[d], accg[r][d]);   // w y'
                     }
@@ -298,7 +304,7 @@ __device__ __forceinline__ uint32_t last_tile_bytes(const SumParams &p, int64_t 
     if (nt <= 0) return 0;
     const int64_t left = p.npairs_valid - (t0 + nt - 1) * (int64_t)Cfg::PAIRS;
     if (left >= Cfg::PAIRS) return 0;
-    const int64_t np = left <= 0 ? 2 : ((left + 1) & ~int64_t(1));
+    const int64_t np = left <= 0 ? 4 : ((left + 3) & ~int64_t(3));     // covers the HH round-up
     return (uint32_t)(np * Cfg::RS * 4);
 }
 

@@ -61,9 +61,15 @@ def kmeans(x, k: int, iters: int = 10, init=None):
         d, j = genred.eval("sqdist", "argkmin", x, c, K=1)
         labels = j[:, 0]
         hist.append(float(d.double().sum().item()))
-        sums = torch.zeros((k, D), dtype=torch.float64, device=x.device)
-        sums.index_add_(0, labels, x.double())
-        counts = torch.bincount(labels, minlength=k).double()
+        # centroid update: deterministic segment sums (sort by label, fp64 prefix sums) instead of
+        # fp64 atomics into k bins (contended and order-dependent)
+        order = torch.argsort(labels, stable=True)
+        counts = torch.bincount(labels, minlength=k)
+        ends = torch.cumsum(counts, 0)
+        xs = x[order].double().t().contiguous()                 # (D, N): scan along rows
+        pref = torch.cat([torch.zeros((D, 1), dtype=torch.float64, device=x.device),
+                          torch.cumsum(xs, 1)], 1)
+        sums = (pref[:, ends] - pref[:, ends - counts]).t()
         keep = counts > 0
-        c = torch.where(keep[:, None], (sums / counts.clamp_min(1)[:, None]).float(), c).contiguous()
+        c = torch.where(keep[:, None], (sums / counts.clamp_min(1)[:, None].double()).float(), c).contiguous()
     return labels, c, hist

@@ -1,4 +1,4 @@
-for lib in build/variants/grad_*.so; do
+for lib in ${VARS:-build/var/libgenred_*.so}; do
 GENRED_LIB=$lib python - <<'PY'
 import os, torch, synth
 from paper_2004_11127_b200 import genred
