@@ -128,13 +128,15 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
-def ncu_traffic(cid: int):
+def ncu_traffic(cid: int, n: int = 0):
     """dram read+write bytes per launch of the dominant kernel from the committed ncu capture."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if not os.path.exists(p):
         return None
     with open(p) as f:
         d = json.load(f)
+    if cid == 6:
+        return d.get(f"C6_N{n}")
     return d.get(f"C{cid}")
 
 
@@ -358,7 +360,7 @@ def main() -> None:
     mhz_max = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
     if argk:
         plan["fallback_rows"] = genred.last_plan(local)["fallback_rows"]
-    traffic = ncu_traffic(args.config)
+    traffic = ncu_traffic(args.config, N)
     if argk:
         # tensor-bound: 3xTF32 = three tf32 GEMMs of 2*M*N*D flops each, against the measured
         # bf16 dense peak x the nominal tf32/bf16 ratio 1/2 (B200_PROFILING.md)
