@@ -157,6 +157,19 @@ def test_host_mode_matches_device_mode(G):
     ld = host(G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64"))
     lh = G.eval("sqdist", "lse", x, y, None, scale=0.05, out_dtype="float64")
     np.testing.assert_array_equal(ld, lh)
+    dd, jd = G.eval("sqdist", "argkmin", dev(x), dev(y), K=5)
+    dh, jh = G.eval("sqdist", "argkmin", x, y, K=5)
+    np.testing.assert_array_equal(host(dd), dh)
+    np.testing.assert_array_equal(host(jd), jh)
+    g = synth.cotangent(M, 24)
+    sd, gd = G.eval("gauss_sum_gradx", "sum", dev(x), dev(y), dev(b), dev(g), scale=0.5)
+    sh, gh = G.eval("gauss_sum_gradx", "sum", x, y, b, g, scale=0.5)
+    np.testing.assert_array_equal(host(sd), sh)
+    np.testing.assert_array_equal(host(gd), gh)
+    # the HBM-bound edge kernel (tiny N) through host buffers, fp64 output
+    ed = host(G.eval("gauss", "sum", dev(x), dev(y[:5]), dev(b[:5]), scale=0.5, out_dtype="float64"))
+    eh = G.eval("gauss", "sum", x, y[:5], b[:5], scale=0.5, out_dtype="float64")
+    np.testing.assert_array_equal(ed, eh)
 
 
 # ------------------------------------------------------------------------------------------------
@@ -443,6 +456,20 @@ def test_gauss_sum_expanded_and_direct_paths(G, case):
     assert plan["path"] == expect, plan
     o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
     assert_sum_parity(host(a), o, den, what=f"gauss {case}")
+
+
+@pytest.mark.parametrize("D", [1, 2, 4, 5])
+def test_gauss_sum_tiny_n_dims_f64(G, D):
+    """Edge kernel for D = 1, 2, 4 (D = 5: the generic kernel) with fp64 output and a partial
+    last row tile."""
+    M, N = 70_001, 9
+    rng = np.random.default_rng(D)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = synth.signal(N, 98, signed=True)
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.7, out_dtype="float64")
+    rows = np.r_[np.arange(0, M, 331), M - 1]
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.7, rows=rows)
+    assert_sum_parity(host(a)[rows], o, den, what=f"gauss tiny N D={D} f64")
 
 
 @pytest.mark.parametrize("N", [1, 2, 7, 33, 64, 65, 513])
