@@ -441,7 +441,7 @@ def main() -> None:
     if rank == 0 and world == 1 and not args.no_cpu:
         import oracle
         oracle.set_num_threads(os.cpu_count() or 1)
-        nrows = args.cpu_rows or max(16, min(M, 4_000_000, int(1e10 // (N * (c.D if argk else 1)))))
+        nrows = args.cpu_rows or max(16, min(M, 4_000_000, int(3e10 // (N * (c.D if argk else 1)))))
         rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
         gpu_rows = (out_idx if argk else out).cpu().numpy()[rows]
         cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=gpu_rows)
