@@ -151,16 +151,20 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
     return n;
 }
 
-// Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.
 constexpr int64_t kDirectMaxN = 64;          // Gaussian Sum: N at or below -> direct form, no bbox
+constexpr int64_t kMinSplitPairs = 64;       // shortest record-pair j-split (128 j)
 
-int choose_split(int64_t itiles, int64_t ntiles, int64_t slots, double *eff_out) {
+// Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.  The
+// j-axis has `total` units (512-j tiles, or record pairs split in multiples of `grain`); every
+// split keeps at least `min_units`.
+int choose_split(int64_t itiles, int64_t total, int64_t grain, int64_t min_units, int64_t slots,
+                 double *eff_out) {
     int best = 1;
     double best_score = -1.0, best_eff = 0.0;
-    const int smax = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, ntiles / 4));
+    const int smax = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, total / min_units));
     for (int S = 1; S <= smax; ++S) {
-        const int64_t tps = (ntiles + S - 1) / S;
-        const int64_t Seff = (ntiles + tps - 1) / tps;
+        const int64_t per = ((total + S - 1) / S + grain - 1) / grain * grain;
+        const int64_t Seff = (total + per - 1) / per;
         if (Seff != S) continue;
         const int64_t U = itiles * S;
         const int64_t waves = (U + slots - 1) / slots;
@@ -175,12 +179,19 @@ int choose_split(int64_t itiles, int64_t ntiles, int64_t slots, double *eff_out)
 struct Plan {
     int R = 1, split = 1;
     int64_t itiles = 0, ntiles = 0, tiles_per_split = 0;
+    int64_t npv = 0, pairs_per_split = 0;     // record-pair splits (Sum, LSE)
 };
 
+// pair_splits: the Sum and LSE kernels split j at record-pair granularity (kSplitGrain), so small
+// and mid-size problems can spread over all SMs; ArgKMin and LSE_GRAD split whole 512-j tiles.
 Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int occ_kind_a,
-               int occ_kind_b, int occ_kind_c) {
+               int occ_kind_b, int occ_kind_c, bool pair_splits = false) {
     Plan pl;
     pl.ntiles = (a->N + kTileJ - 1) / kTileJ;
+    pl.npv = ((a->N + 1) / 2 + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+    const int64_t total = pair_splits ? pl.npv : pl.ntiles;
+    const int64_t grain = pair_splits ? kSplitGrain : 1;
+    const int64_t min_units = pair_splits ? kMinSplitPairs : 4;
     int rcands[2] = {rmax, 1};
     int ncand = rmax > 1 ? 2 : 1;
     double best = -1.0;
@@ -192,11 +203,11 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
         int S;
         double eff;
         if (a->split_j > 0) {
-            S = (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, pl.ntiles));
+            S = (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, total / grain));
             const int64_t U = itiles * S, waves = (U + slots - 1) / slots;
             eff = (double)U / (double)(waves * slots);
         } else {
-            S = choose_split(itiles, pl.ntiles, slots, &eff);
+            S = choose_split(itiles, total, grain, min_units, slots, &eff);
         }
         const double score = eff * (R == rmax ? 1.0 : 0.9);      // fewer rows/thread costs issue slots
         if (score > best || (a->split_j > 0 && R == rmax)) {
@@ -205,8 +216,13 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
             if (a->split_j > 0) break;                          // forced split: always rmax rows
         }
     }
-    pl.tiles_per_split = (pl.ntiles + pl.split - 1) / pl.split;
-    pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
+    if (pair_splits) {
+        pl.pairs_per_split = ((pl.npv + pl.split - 1) / pl.split + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+        pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+    } else {
+        pl.tiles_per_split = (pl.ntiles + pl.split - 1) / pl.split;
+        pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
+    }
     return pl;
 }
 
@@ -321,8 +337,8 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     kernels++;
     if (mode == 4) {
         LseLaunch L;
-        L.D = D; L.R = R; L.x = a->x; L.J = J; L.M = M; L.split = 1; L.tiles_per_split = 0;
-        L.ntiles = 0; L.negc = (float)(-kLog2e / a->scale); L.h_zero = a->b == nullptr;
+        L.D = D; L.R = R; L.x = a->x; L.J = J; L.M = M; L.split = 1; L.pairs_per_split = 0;
+        L.npv = 0; L.negc = (float)(-kLog2e / a->scale); L.h_zero = a->b == nullptr;
         L.out = a->out; L.out_f64 = out_f64; L.state = a->lse_state;
         L.units = dunits; L.n_units = (int64_t)units.size();
         int ctas = 0;
@@ -341,7 +357,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     }
     SumLaunch L;
     L.mode = mode; L.D = D; L.E = E; L.R = R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
-    L.split = 1; L.tiles_per_split = 0; L.ntiles = 0; L.s = sc;
+    L.split = 1; L.pairs_per_split = 0; L.npv = 0; L.s = sc;
     L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
     L.out_grad = a->out_grad; L.part = nullptr; L.geo = geo;
     L.units = dunits; L.n_units = (int64_t)units.size();
@@ -432,7 +448,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
                        : (f == GENRED_GAUSS_SUM_GRADX) ? 2 : 3;
         const int rmax = sum_rows_per_thread_max(mode, D, E);
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, mode, rmax);
-        Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E);
+        Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E, true);
         // Gaussian Sum, one signal column, D <= 3: the tensor-core kernel (gauss_tc.cu) takes
         // the expanded case; the FP32 kernel behind it only the direct one.  Both use the same
         // j-split (in 512-j tiles), chosen for 128-row units on one CTA per SM.
@@ -442,11 +458,12 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         const bool tc = mode == 0 && E == 1 && D <= 3 && (tcv ? atoi(tcv) != 0 : ctx->gauss_tc);
         if (tc) {
             const int64_t units_i = (M + gauss_tc_rows_per_unit() - 1) / gauss_tc_rows_per_unit();
-            int S = a->split_j > 0 ? (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, pl.ntiles))
-                                   : choose_split(units_i, pl.ntiles, ctx->num_sms, nullptr);
+            const int64_t n256 = 2 * pl.ntiles;                    // 256-j tiles of gauss_tc
+            const int S = a->split_j > 0 ? (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), n256)
+                                         : choose_split(units_i, n256, 1, 4, ctx->num_sms, nullptr);
             pl.R = rmax;
-            pl.tiles_per_split = (pl.ntiles + S - 1) / S;
-            pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
+            pl.split = S;            // both kernels write S partials (empty ranges write zeros)
+            pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
         }
         const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
@@ -484,7 +501,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (tc) {
             GaussTcLaunch T;
             T.x = a->x; T.y = a->y; T.b = a->b; T.geo = geo; T.M = M; T.N = N; T.D = D; T.s = sc;
-            T.split = pl.split; T.tiles_per_split = 2 * pl.tiles_per_split; T.scale_sum = 1.0;
+            T.split = pl.split; T.tiles_per_split = (2 * pl.ntiles + pl.split - 1) / pl.split; T.scale_sum = 1.0;
             T.out = a->out; T.out_f64 = out_f64; T.part = part; T.scratch = tscratch;
             T.num_sms = ctx->num_sms;
             T.ev_start = prof_event(ctx, true, nullptr, true);
@@ -513,11 +530,10 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         }
         SumLaunch L;
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
-        L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles; L.s = sc;
+        L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
         L.direct_only = tc ? 1 : 0;
-        L.npairs_valid = (N + 1) / 2;
         int sctas = 0;
         if (!tc) prof_event(ctx, true, st);
         e = launch_sum(L, st, &sctas);
@@ -544,7 +560,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
 
     if (red == GENRED_LSE) {
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, 4, lse_rows_per_thread_max(D));
-        Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0);
+        Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0, true);
         const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
         const int RS = pack_record_stride(pk, D, 1);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
@@ -558,7 +574,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         LseLaunch L;
         L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
-        L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+        L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv;
         L.negc = (float)(-kLog2e / a->scale);
         L.h_zero = a->b == nullptr;
         L.out = a->out; L.out_f64 = out_f64;

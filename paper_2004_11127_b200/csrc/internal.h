@@ -11,6 +11,9 @@ constexpr int kStages = 4;                  // depth of the bulk-copy ring
 constexpr int kConsumerWarps = 8;           // math warps per CTA
 constexpr int kThreads = kConsumerWarps * 32;         // all math warps; thread 0 also refills the j-ring
 constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference of an empty LSE state
+// j-splits of the Sum and LSE kernels are whole multiples of this many record pairs (32 j): the
+// Sum's record-pair unroll and the LSE's 16-pair rescale sub-chunk both divide it.
+constexpr int kSplitGrain = 16;
 
 // Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
@@ -60,7 +63,8 @@ struct SumLaunch {
     const uint32_t *geo;      // MODE 0: encoded bounding box (geo.cuh)
     int64_t M;
     int split;                // number of j-splits (grid = itiles * split)
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split;  // record pairs per j-split (multiple of kSplitGrain)
+    int64_t npv;              // record pairs reduced: ceil(N/2) rounded up to kSplitGrain
     float s;                  // coordinate pre-scale (sqrt(log2e)/sigma, or 1 for SQDIST)
     double scale_sum, scale_grad;
     void *out; int out_f64;   // sum output (SUM / SUM_GRADX / SQDIST_SUM) or gradient (GRADX)
@@ -69,7 +73,6 @@ struct SumLaunch {
     const RangeUnit *units;   // block-sparse ranges (device), or nullptr
     int64_t n_units;
     int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
-    int64_t npairs_valid = (int64_t)1 << 60;   // record pairs holding real j (ceil(N/2))
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
 int sum_occupancy(int mode, int D, int E, int R);
@@ -80,7 +83,8 @@ struct LseLaunch {
     const float *x, *J;
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split;  // record pairs per j-split (multiple of kSplitGrain)
+    int64_t npv;              // record pairs reduced: ceil(N/2) rounded up to kSplitGrain
     float negc;               // -log2(e)/eps
     int h_zero;               // h == 0 everywhere (skips a per-pair FADD)
     void *out; int out_f64;   // split == 1: a_i

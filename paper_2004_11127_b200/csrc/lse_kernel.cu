@@ -35,6 +35,7 @@ constexpr float kSumMax = 65536.0f;
 #endif
 constexpr int kSub = GENRED_LSE_SUB;  // record pairs per sub-chunk (2 kSub j)
 constexpr int kPromote = 64 / kSub;   // sub-chunks per fp64 promotion (128 j)
+static_assert(kSplitGrain % kSub == 0, "j-splits must hold whole sub-chunks");
 
 template <int D, bool HZ>
 struct LseCfg {
@@ -50,7 +51,7 @@ struct LseParams {
     const float *x, *J;
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split, npv;      // record-pair j-splits (see SumParams)
     float negc;
     void *out;
     int out_f64;
@@ -111,23 +112,26 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
-    int64_t row0, row_end, t0;
-    int sp, nt;
+    // this CTA's j-range: record pairs [q0, q0 + npc), streamed in tiles of PAIRS
+    int64_t row0, row_end, q0, npc;
+    int sp;
     if (p.units) {                                     // block-sparse: rows of one cluster
         const RangeUnit u = p.units[blockIdx.x];
-        row0 = u.row0; row_end = u.row_end; t0 = u.tile0; nt = (int)u.ntiles; sp = 0;
+        row0 = u.row0; row_end = u.row_end; sp = 0;
+        q0 = u.tile0 * Cfg::PAIRS; npc = u.ntiles * Cfg::PAIRS;
     } else {
         const int64_t itile = blockIdx.x / p.split;
         sp = (int)(blockIdx.x % p.split);
-        t0 = (int64_t)sp * p.tiles_per_split;
-        const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-        nt = (int)(t1 - t0);
+        q0 = (int64_t)sp * p.pairs_per_split;
+        npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
         row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
         row_end = p.M;
     }
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
 
     JRing<kStages> ring;
-    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * RS, nt, kConsumerWarps, (uint32_t)last_np * RS * 4u);
 
     const int ct = threadIdx.x;
     const float negc = p.negc;
@@ -149,7 +153,8 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-        for (int sc = 0; sc < Cfg::PAIRS / kSub; ++sc) {
+        const int nsc = (k == nt - 1 ? last_np : Cfg::PAIRS) / kSub;     // sub-chunks in this tile
+        for (int sc = 0; sc < nsc; ++sc) {
             const float *base = tile + sc * kSub * RS;
             float2 cs[R];
 #pragma unroll
@@ -244,8 +249,8 @@ static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
         attr_done = true;
     }
     LseParams p;
-    p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.tiles_per_split = a.tiles_per_split;
-    p.ntiles = a.ntiles; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
+    p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.pairs_per_split = a.pairs_per_split;
+    p.npv = a.npv; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
     p.units = a.units;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t grid = a.units ? a.n_units : ((a.M + rows - 1) / rows) * a.split;

@@ -55,7 +55,8 @@ struct SumParams {
     const uint32_t *geo;      // Gaussian modes: encoded bounding box (geo.cuh)
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split;  // j-split length in record pairs (a multiple of kSplitGrain)
+    int64_t npv;              // record pairs to reduce: ceil(N/2) rounded up to kSplitGrain
     float s;
     double scale_sum, scale_grad;
     void *out;
@@ -64,8 +65,6 @@ struct SumParams {
     double *part;
     const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
     int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
-    int64_t npairs_valid;     // record pairs holding real j (dense launches): the last tile's
-                              // loop stops there (tiny N: HBM-bound edge, SURVEY.md 8(d) Cedge)
 };
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
@@ -79,7 +78,7 @@ constexpr bool kPolyShare = false;
 // leaves the MUFU pipe (16 ex2/clk/SM) as the only bound; the row factor 2^(-|x'|^2) is applied
 // in fp64 at the end.
 template <int MODE, int D, int E, int R, bool XP>
-__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt, int64_t t0,
+__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt, int last_np,
                                          int64_t row0, int64_t row_end, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
@@ -134,9 +133,9 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-        // pairs of this tile that hold real j (rounded up to the unroll of 2; the rest is padding)
-        const int64_t left = p.npairs_valid - (t0 + k) * (int64_t)Cfg::PAIRS;
-        const int np = left >= Cfg::PAIRS ? Cfg::PAIRS : (int)((left + HH - 1) / HH * HH);
+        // record pairs of this tile: whole tiles, except the range's last one (a multiple of
+        // kSplitGrain, so of HH)
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
         for (int pp2 = 0; pp2 < np; pp2 += HH) {
 #pragma unroll
         for (int hh = 0; hh < HH; ++hh) {
@@ -297,17 +296,6 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     }
 }
 
-// Bytes of the CTA's last j-tile that hold real records (0 = the whole tile): with a tiny N the
-// only tile is mostly padding, and copying it whole would double the data moved per CTA.
-template <class Cfg>
-__device__ __forceinline__ uint32_t last_tile_bytes(const SumParams &p, int64_t t0, int nt) {
-    if (nt <= 0) return 0;
-    const int64_t left = p.npairs_valid - (t0 + nt - 1) * (int64_t)Cfg::PAIRS;
-    if (left >= Cfg::PAIRS) return 0;
-    const int64_t np = left <= 0 ? 4 : ((left + 3) & ~int64_t(3));     // covers the HH round-up
-    return (uint32_t)(np * Cfg::RS * 4);
-}
-
 template <int MODE, int D, int E, int R>
 __global__ void __launch_bounds__(kThreads, (((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ||
                                             ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && E == 1 && R == 2)) ? 3 : 2)
@@ -315,34 +303,36 @@ sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
-    int64_t row0, row_end, t0;
-    int sp, nt;
+    // this CTA's j-range: record pairs [q0, q0 + npc), streamed in tiles of PAIRS
+    int64_t row0, row_end, q0, npc;
+    int sp;
     if (p.units) {                                     // block-sparse: rows of one cluster
         const RangeUnit u = p.units[blockIdx.x];
-        row0 = u.row0; row_end = u.row_end; t0 = u.tile0; nt = (int)u.ntiles; sp = 0;
+        row0 = u.row0; row_end = u.row_end; sp = 0;
+        q0 = u.tile0 * Cfg::PAIRS; npc = u.ntiles * Cfg::PAIRS;
     } else {
         const int64_t itile = blockIdx.x / p.split;
         sp = (int)(blockIdx.x % p.split);
-        t0 = (int64_t)sp * p.tiles_per_split;
-        const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-        nt = (int)(t1 - t0);
+        q0 = (int64_t)sp * p.pairs_per_split;
+        npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);   // empty: zero partial
         row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
         row_end = p.M;
     }
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
+    const uint32_t last_bytes = (uint32_t)last_np * Cfg::RS * 4u;   // a partial last tile is copied partially
 
     JRing<kStages> ring;
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
         if (MODE == 0 && p.direct_only && geo.expanded) return;   // gauss_tc.cu took this call
-        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps,
-                  last_tile_bytes<Cfg>(p, t0, nt));
-        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, t0, row0, row_end, sp, geo);
-        else sum_body<MODE, D, E, R, false>(p, ring, nt, t0, row0, row_end, sp, geo);
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
+        if (geo.expanded) sum_body<MODE, D, E, R, true>(p, ring, nt, last_np, row0, row_end, sp, geo);
+        else sum_body<MODE, D, E, R, false>(p, ring, nt, last_np, row0, row_end, sp, geo);
     } else {
-        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps,
-                  last_tile_bytes<Cfg>(p, t0, nt));
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
         Geo geo{};
-        sum_body<MODE, D, E, R, false>(p, ring, nt, t0, row0, row_end, sp, geo);
+        sum_body<MODE, D, E, R, false>(p, ring, nt, last_np, row0, row_end, sp, geo);
     }
 }
 
@@ -360,11 +350,10 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     }
     SumParams p;
     p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;
-    p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.s = a.s;
+    p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.s = a.s;
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = a.units;
     p.direct_only = a.direct_only;
-    p.npairs_valid = a.units ? (int64_t)1 << 60 : a.npairs_valid;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
     const int64_t grid = a.units ? a.n_units : itiles * a.split;

@@ -140,8 +140,9 @@ def test_split_invariance_and_determinism(G, split):
     M, N = 3000, 9000
     x = synth.gmm3(M, 11); y = synth.gmm3(N, 12); b = synth.signal(N, 13, signed=True)
     a1 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
-    ntiles = -(-N // 512)
-    assert G.last_plan()["split_j"] == -(-ntiles // -(-ntiles // split))   # j-tiles per split rounded up
+    npv = -(-(-(-N // 2)) // 16) * 16                       # record pairs, in 16-pair grains
+    pps = -(-(-(-npv // split)) // 16) * 16                 # pairs per split, rounded up
+    assert G.last_plan()["split_j"] == -(-npv // pps)
     a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split)
     assert torch.equal(a1, a2)
     o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
