@@ -22,11 +22,17 @@ def gauss_matvec(p, v, sigma: float, ranges=None):
 
 
 def gauss_cg(p, b, sigma: float, alpha: float, tol: float = 1e-6, max_iter: int = 500, x0=None,
-             ranges=None):
+             ranges=None, graph: bool = False, check_every: int = 8):
     """Solve (K + alpha I) x = b by conjugate gradients (K is SPD for distinct points, alpha > 0).
 
     p: (N, D) fp32 CUDA points, b: (N,) or (N, E) right-hand side.  Residual norms are tracked in
-    fp64; matvecs run in libgenred (fp32 data, fp64 tile accumulation).  Returns (x, info)."""
+    fp64; matvecs run in libgenred (fp32 data, fp64 tile accumulation).  Returns (x, info).
+
+    graph=True captures one CG iteration (the Genred matvec launches + the vector updates) in a
+    CUDA graph and replays it, testing convergence every ``check_every`` iterations (one host
+    sync per check instead of one per iteration); the arithmetic is identical."""
+    if graph:
+        return _gauss_cg_graph(p, b, sigma, alpha, tol, max_iter, x0, ranges, check_every)
     squeeze = b.dim() == 1
     B = (b[:, None] if squeeze else b).to(torch.float32).contiguous()
     X = torch.zeros_like(B) if x0 is None else (x0[:, None] if squeeze else x0).clone().float()
@@ -47,6 +53,54 @@ def gauss_cg(p, b, sigma: float, alpha: float, tol: float = 1e-6, max_iter: int 
         d = r + (rr_new / rr).float() * d
         rr = rr_new
     info = {"iterations": it, "rel_residual": (torch.sqrt(rr) / bnorm).max().item()}
+    return (X[:, 0] if squeeze else X), info
+
+
+def _gauss_cg_graph(p, b, sigma, alpha, tol, max_iter, x0, ranges, check_every):
+    squeeze = b.dim() == 1
+    B = (b[:, None] if squeeze else b).to(torch.float32).contiguous()
+    X = torch.zeros_like(B) if x0 is None else (x0[:, None] if squeeze else x0).clone().float().contiguous()
+    r = B - (gauss_matvec(p, X, sigma, ranges) + alpha * X) if x0 is not None else B.clone()
+    d = r.clone()
+    rr = (r.double() * r.double()).sum(0)
+    bnorm = torch.sqrt((B.double() * B.double()).sum(0))
+    done = torch.zeros((), dtype=torch.bool, device=B.device)
+
+    def iteration():
+        # once converged, the step and the direction update are frozen (masked), so replays
+        # past convergence leave X unchanged: same result as stopping at the first hit
+        Ad = gauss_matvec(p, d, sigma, ranges) + alpha * d
+        step = torch.where(done, torch.zeros_like(rr), rr / (d.double() * Ad.double()).sum(0))
+        X.add_(step.float() * d)
+        r.sub_(step.float() * Ad)
+        rr_new = (r.double() * r.double()).sum(0)
+        hit = torch.all(torch.sqrt(rr_new) <= tol * bnorm)
+        beta = torch.where(done | hit, torch.zeros_like(rr), rr_new / rr)
+        d.mul_(beta.float()).add_(r)
+        rr.copy_(torch.where(done, rr, rr_new))
+        done.logical_or_(hit)
+
+    side = torch.cuda.Stream(device=B.device)
+    side.wait_stream(torch.cuda.current_stream(B.device))
+    with torch.cuda.stream(side):                       # warm-up outside the capture
+        state = [t.clone() for t in (X, r, d, rr, done)]
+        iteration()
+        for t, v in zip((X, r, d, rr, done), state):
+            t.copy_(v)
+    torch.cuda.current_stream(B.device).wait_stream(side)
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(g):
+        iteration()
+    it = 0
+    while it < max_iter:
+        n = min(check_every, max_iter - it)
+        for _ in range(n):
+            g.replay()
+        it += n
+        if bool(done.item()):
+            break
+    info = {"iterations": it, "rel_residual": (torch.sqrt(rr) / bnorm).max().item(), "graph": True,
+            "converged": bool(done.item())}
     return (X[:, 0] if squeeze else X), info
 
 

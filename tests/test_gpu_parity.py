@@ -706,6 +706,19 @@ def test_gauss_cg_solves_kernel_system(G):
     assert np.linalg.norm(res) <= 5e-5 * np.linalg.norm(rhs)
 
 
+def test_gauss_cg_cuda_graph_matches_eager(G):
+    """One CG iteration (Genred matvec + vector updates) captured in a CUDA graph and replayed
+    gives bitwise the eager solution (updates freeze after convergence)."""
+    from paper_2004_11127_b200.solvers import gauss_cg
+    N, sigma, alpha = 5000, 0.08, 0.1
+    p = synth.uniform3(N, 125); rhs = synth.signal(N, 126, signed=True)[:, 0]
+    xe, ie = gauss_cg(dev(p), dev(rhs), sigma, alpha, tol=1e-6, max_iter=300)
+    xg, ig = gauss_cg(dev(p), dev(rhs), sigma, alpha, tol=1e-6, max_iter=300, graph=True, check_every=8)
+    assert ig["converged"] and ig["iterations"] >= ie["iterations"]
+    np.testing.assert_array_equal(host(xg), host(xe))
+    assert ig["rel_residual"] == ie["rel_residual"]
+
+
 def test_kmeans_assignment_and_monotone_objective(G):
     from paper_2004_11127_b200.solvers import kmeans
     x = synth.gmm3(20000, 131)

@@ -97,6 +97,16 @@ def main():
     lines.append({"item": "8(f)4 CG (K + 0.1 I) x = b, Gaussian sigma=0.05", "N": N, "ms": ms,
                   "iterations": info["iterations"], "rel_residual": info["rel_residual"],
                   "ms_per_iteration": ms / max(info["iterations"], 1)})
+    solvers.gauss_cg(p, rhs, 0.05, 0.1, tol=1e-6, max_iter=16, graph=True)      # capture warm-up
+    torch.cuda.synchronize()
+    e0.record()
+    xg, ginfo = solvers.gauss_cg(p, rhs, 0.05, 0.1, tol=1e-6, max_iter=1000, graph=True)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    lines.append({"item": "8(f)4 CG as above, one iteration captured in a CUDA graph", "N": N, "ms": ms,
+                  "iterations": ginfo["iterations"], "rel_residual": ginfo["rel_residual"],
+                  "ms_per_iteration": ms / max(ginfo["iterations"], 1),
+                  "bitwise_equal_to_eager": bool(torch.equal(xg, xs))})
     # 5. k-means
     N, k = 1_000_000, 1000
     xk = dev(synth.gmm3(N, 13))
