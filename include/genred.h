@@ -26,6 +26,10 @@
  *     faults surface at the caller's next synchronisation.
  *   - NaN / Inf inputs propagate under IEEE semantics and are not checked.
  *   - A context is used by one host thread at a time; distinct contexts are independent.
+ *   - CUDA graphs: once a context's scratch arena has grown to the largest problem (one warm-up
+ *     call), device-mode genred_eval neither synchronises nor allocates, so it can be captured
+ *     on `stream`.  Captured launches use that arena: while the graph lives, calls on the same
+ *     context must not need a larger arena nor run concurrently on another stream.
  */
 #ifndef GENRED_H
 #define GENRED_H
