@@ -15,23 +15,44 @@
 
 namespace genred {
 
-__global__ void pack_kernel(int kind, const float *__restrict__ y, const float *__restrict__ b,
-                            int64_t N, int D, int E, float s, double hscale, int64_t npairs, int RS,
-                            float *__restrict__ J, const uint32_t *geo_enc) {
+// One block = one 512-j tile = 256 record pairs: the tile's y (and b / h) rows are staged into
+// shared memory with coalesced loads, each thread builds its record pair there, and the block
+// writes the tile's records (contiguous in J) with coalesced 16-byte stores.
+__global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__restrict__ y,
+                                                   const float *__restrict__ b, int64_t N, int D, int E,
+                                                   float s, double hscale, int64_t npairs, int RS,
+                                                   float *__restrict__ J, const uint32_t *geo_enc) {
+    extern __shared__ float4 pack_smem4[];
+    float *sm = reinterpret_cast<float *>(pack_smem4);
     const float NEG_INF = -INFINITY;
-    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) {
-        // Gaussian Sum records: [2D coords][w pair][2E signal]; expanded or direct per geo
-        const Geo geo = geo_decode(geo_enc, D, s);
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT;
+    const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
+    const int EB = (gauss || sumk) ? (b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);   // staged b / h columns
+    float *ys = sm;                           // [512][D]
+    float *bs = ys + kTileJ * D;              // [512][EB]
+    float *outs = bs + kTileJ * EB;           // [256][RS]  (16-byte aligned: 512 (D + EB) floats)
+    Geo geo{};
+    if (gauss) {
+        geo = geo_decode(geo_enc, D, s);      // expanded or direct per the bounding box
         if (kind == PACK_GAUSS_DIRECT && geo.expanded) return;   // gauss_tc.cu takes this call
-        for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
-             p += (int64_t)gridDim.x * blockDim.x) {
-            float *rec = J + p * RS;
-            for (int h = 0; h < 2; ++h) {
-                const int64_t j = 2 * p + h;
-                const bool valid = j < N;
+    }
+    const int t = threadIdx.x;
+    for (int64_t blk = blockIdx.x; blk * 256 < npairs; blk += gridDim.x) {
+        const int64_t j0 = blk * kTileJ;
+        const int nj = (int)max((int64_t)0, min((int64_t)kTileJ, N - j0));
+        for (int k = t; k < nj * D; k += 256) ys[k] = __ldg(y + j0 * D + k);
+        for (int k = t; k < nj * EB; k += 256) bs[k] = __ldg(b + j0 * EB + k);
+        __syncthreads();
+        float *rec = outs + t * RS;
+        for (int k = 0; k < RS; ++k) rec[k] = 0.0f;
+        for (int h = 0; h < 2; ++h) {
+            const int jj = 2 * t + h;
+            const bool valid = jj < nj;
+            if (gauss) {
+                // [2D coords][w pair][2E signal]; padding: y = 0, w = 0, b = 0
                 double w = 0.0;
                 for (int d = 0; d < D; ++d) {
-                    const float v = valid ? y[j * D + d] : 0.0f;
+                    const float v = valid ? ys[jj * D + d] : 0.0f;
                     float r;
                     if (geo.expanded) {
                         r = valid ? s * (v - geo.c[d]) : 0.0f;        // y' = s (y - c)
@@ -42,42 +63,41 @@ __global__ void pack_kernel(int kind, const float *__restrict__ y, const float *
                     rec[2 * d + h] = r;
                 }
                 rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;   // w = -|y'|^2
-                for (int e = 0; e < E; ++e)                           // padding: b = 0
-                    rec[2 * D + 2 + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
-            }
-            for (int k = 2 * (D + 1 + E); k < RS; ++k) rec[k] = 0.0f;
-        }
-        return;
-    }
-    for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
-         p += (int64_t)gridDim.x * blockDim.x) {
-        float *rec = J + p * RS;
-        for (int h = 0; h < 2; ++h) {
-            const int64_t j = 2 * p + h;
-            const bool valid = j < N;
-            for (int d = 0; d < D; ++d) {
-                float v = valid ? y[j * D + d] : 0.0f;
-                float r;
-                if (kind == PACK_GAUSS || kind == PACK_SQDIST_SUM) r = valid ? -(s * v) : 0.0f;
-                else r = valid ? -v : NEG_INF;          // LSE / ARGKMIN: padded y at +inf distance
-                rec[2 * d + h] = r;
-            }
-            if (kind == PACK_GAUSS || kind == PACK_SQDIST_SUM) {
                 for (int e = 0; e < E; ++e)
-                    rec[2 * D + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
+                    rec[2 * D + 2 + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
+                continue;
+            }
+            for (int d = 0; d < D; ++d) {
+                const float v = valid ? ys[jj * D + d] : 0.0f;
+                // Sum kinds: -s y (padding 0, b = 0); LSE / ArgKMin: -y (padding at +inf distance)
+                rec[2 * d + h] = sumk ? (valid ? -(s * v) : 0.0f) : (valid ? -v : NEG_INF);
+            }
+            if (sumk) {
+                for (int e = 0; e < E; ++e)
+                    rec[2 * D + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
             } else if (kind == PACK_LSE_H) {
                 // h' = log2(e) h as an fp32 hi + lo pair (fp64 product), so that
                 // (h'_hi - m) + h'_lo keeps |h| ~ 1e4 biases exact to fp32 rounding of t.
-                const double hv = valid ? hscale * (double)b[j] : 0.0;
+                const double hv = valid ? hscale * (double)bs[jj] : 0.0;
                 const float hi = valid ? (float)hv : NEG_INF;
                 rec[2 * D + h] = hi;
                 rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
             }
         }
-        const int used = (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) ? 2 * D
-                       : (kind == PACK_LSE_H ? 2 * D + 4 : 2 * (D + E));
-        for (int k = used; k < RS; ++k) rec[k] = 0.0f;
+        __syncthreads();
+        const int nrec = (int)min((int64_t)256, npairs - blk * 256);
+        float4 *dst = reinterpret_cast<float4 *>(J + blk * 256 * RS);
+        const float4 *src4 = reinterpret_cast<const float4 *>(outs);
+        for (int k = t; k < nrec * RS / 4; k += 256) dst[k] = src4[k];
+        __syncthreads();
     }
+}
+
+static int pack_smem_bytes(int kind, int D, int E, int RS, bool has_b) {
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT;
+    const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
+    const int EB = (gauss || sumk) ? (has_b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);
+    return (kTileJ * (D + EB) + 256 * RS) * 4;
 }
 
 int pack_record_stride(int kind, int D, int E) {
@@ -90,10 +110,17 @@ int pack_record_stride(int kind, int D, int E) {
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E, float s,
                         double hscale, int64_t npairs, float *J, cudaStream_t st, const uint32_t *geo) {
     const int RS = pack_record_stride(kind, D, E);
+    const int smem = pack_smem_bytes(kind, D, E, RS, b != nullptr);
+    static int attr_set = 0;
+    if (smem > 48 * 1024 && smem > attr_set) {
+        cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        if (e != cudaSuccess) return e;
+        attr_set = smem;
+    }
     int64_t blocks = (npairs + 255) / 256;
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
-    pack_kernel<<<(unsigned)blocks, 256, 0, st>>>(kind, y, b, N, D, E, s, hscale, npairs, RS, J, geo);
+    pack_kernel<<<(unsigned)blocks, 256, smem, st>>>(kind, y, b, N, D, E, s, hscale, npairs, RS, J, geo);
     return cudaGetLastError();
 }
 
@@ -169,6 +196,8 @@ cudaError_t launch_pack_ranges(int kind, const float *y, const float *b, int64_t
 
 // ---- per-coordinate bounding box of x and y (order-preserving uint encodings, geo.cuh) -------
 // blockIdx.y = 0: y into geo[0..15]; blockIdx.y = 1: x into geo[16..31]
+// Row-wise pass over y (blockIdx.y == 0) or x (1): a warp reads 32 consecutive rows per load
+// instruction (coalesced); four rows per thread per iteration keep 4 D loads in flight.
 __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float *__restrict__ y,
                             int64_t N, int D, uint32_t *geo) {
     float lo[8], hi[8];
@@ -177,13 +206,25 @@ __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float 
     const float *src = blockIdx.y == 0 ? y : x;
     const int64_t rows = blockIdx.y == 0 ? N : M;
     const int off = blockIdx.y == 0 ? 0 : 16;
-    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < rows;
-         t += (int64_t)gridDim.x * blockDim.x) {
-        const float *pt = src + t * D;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    for (; t + 3 * stride < rows; t += 4 * stride) {
+        float v[4][8];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int d = 0; d < 8; ++d) v[q][d] = d < D ? __ldg(src + (t + q * stride) * D + d) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+                if (d < D) { lo[d] = fminf(lo[d], v[q][d]); hi[d] = fmaxf(hi[d], v[q][d]); }
+    }
+    for (; t < rows; t += stride) {
 #pragma unroll
         for (int d = 0; d < 8; ++d) {
             if (d < D) {
-                const float v = pt[d];
+                const float v = __ldg(src + t * D + d);
                 lo[d] = fminf(lo[d], v);
                 hi[d] = fmaxf(hi[d], v);
             }
@@ -197,12 +238,22 @@ __global__ void bbox_kernel(const float *__restrict__ x, int64_t M, const float 
             hi[d] = fmaxf(hi[d], __shfl_xor_sync(0xffffffffu, hi[d], o));
         }
     }
+    // block reduction through shared memory, then one atomic per coordinate and block (per-warp
+    // atomics on the same 2D words serialise at L2)
+    __shared__ float slo[8][8], shi[8][8];
+    const int warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        for (int d = 0; d < D; ++d) {
-            if (lo[d] <= hi[d]) {
-                atomicMin(geo + off + d, f2ord(lo[d]));
-                atomicMax(geo + off + 8 + d, f2ord(hi[d]));
-            }
+#pragma unroll
+        for (int dd = 0; dd < 8; ++dd) { slo[warp][dd] = lo[dd]; shi[warp][dd] = hi[dd]; }
+    }
+    __syncthreads();
+    if (threadIdx.x < D) {
+        const int dd = threadIdx.x;
+        float l = slo[0][dd], h = shi[0][dd];
+        for (int w = 1; w < nw; ++w) { l = fminf(l, slo[w][dd]); h = fmaxf(h, shi[w][dd]); }
+        if (l <= h) {
+            atomicMin(geo + off + dd, f2ord(l));
+            atomicMax(geo + off + 8 + dd, f2ord(h));
         }
     }
 }
@@ -215,8 +266,8 @@ cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, in
         if (e == cudaSuccess) e = cudaMemsetAsync(geo + 16 * half + 8, 0x00, 8 * sizeof(uint32_t), st);
     }
     if (e != cudaSuccess) return e;
-    int64_t blocks = (std::max(M, N) + 255) / 256;
-    if (blocks > 148 * 2) blocks = 148 * 2;
+    int64_t blocks = (std::max(M, N) + 1023) / 1024;
+    if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
     bbox_kernel<<<dim3((unsigned)blocks, 2), 256, 0, st>>>(x, M, y, N, D, geo);
     return cudaGetLastError();
@@ -248,6 +299,31 @@ bool geo_expanded_host(const uint32_t *geo_dev, int D, float s) {
 }
 
 // ---- Sum / gradient: out = scale * sum_{split} part[split] in split order ----------------------
+__device__ __forceinline__ void sum_finalize_store(double acc, int64_t i, int C, int c, int cols_sum,
+                                                   const float *__restrict__ g, int E, double scale_sum,
+                                                   double scale_grad, int mode, void *out, int out_f64,
+                                                   float *out_grad);
+
+// Many splits (small-M mode): one warp per output, lanes sum strided partials in a fixed order
+// and a fixed butterfly finishes (deterministic), instead of one thread walking all S partials.
+__global__ void sum_finalize_warp_kernel(const double *__restrict__ part, int split, int64_t M, int C,
+                                         int cols_sum, const float *__restrict__ g, int E,
+                                         double scale_sum, double scale_grad, int mode, void *out,
+                                         int out_f64, float *out_grad) {
+    const int64_t total = M * C;
+    const int lane = threadIdx.x & 31;
+    for (int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; t < total;
+         t += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        const int64_t i = t / C;
+        const int c = (int)(t % C);
+        double acc = 0.0;
+        for (int q = lane; q < split; q += 32) acc += part[((int64_t)q * M + i) * C + c];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) sum_finalize_store(acc, i, C, c, cols_sum, g, E, scale_sum, scale_grad, mode, out, out_f64, out_grad);
+    }
+}
+
 __global__ void sum_finalize_kernel(const double *__restrict__ part, int split, int64_t M, int C,
                                     int cols_sum, const float *__restrict__ g, int E,
                                     double scale_sum, double scale_grad, int mode, void *out,
@@ -259,6 +335,15 @@ __global__ void sum_finalize_kernel(const double *__restrict__ part, int split, 
         const int c = (int)(t % C);
         double acc = 0.0;
         for (int q = 0; q < split; ++q) acc += part[((int64_t)q * M + i) * C + c];
+        sum_finalize_store(acc, i, C, c, cols_sum, g, E, scale_sum, scale_grad, mode, out, out_f64, out_grad);
+    }
+}
+
+__device__ __forceinline__ void sum_finalize_store(double acc, int64_t i, int C, int c, int cols_sum,
+                                                   const float *__restrict__ g, int E, double scale_sum,
+                                                   double scale_grad, int mode, void *out, int out_f64,
+                                                   float *out_grad) {
+    {
         if (c < cols_sum) {
             double v = acc * scale_sum;
             if (out_f64) ((double *)out)[i * cols_sum + c] = v;
@@ -279,6 +364,15 @@ __global__ void sum_finalize_kernel(const double *__restrict__ part, int split, 
 cudaError_t launch_sum_finalize(const double *part, int split, int64_t M, int C, int cols_sum,
                                 const float *g, int E, double scale_sum, double scale_grad,
                                 int mode, void *out, int out_f64, float *out_grad, cudaStream_t st) {
+    if (split > 32) {
+        int64_t blocks = (M * C * 32 + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        if (blocks < 1) blocks = 1;
+        sum_finalize_warp_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, split, M, C, cols_sum, g, E,
+                                                                   scale_sum, scale_grad, mode, out,
+                                                                   out_f64, out_grad);
+        return cudaGetLastError();
+    }
     int64_t blocks = (M * C + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;

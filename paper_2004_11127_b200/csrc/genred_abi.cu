@@ -152,16 +152,19 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
 }
 
 constexpr int64_t kDirectMaxN = 64;          // Gaussian Sum: N at or below -> direct form, no bbox
+constexpr int64_t kDirectMaxM = 16;          // Gaussian Sum: M at or below -> direct form, no bbox
 constexpr int64_t kMinSplitPairs = 64;       // shortest record-pair j-split (128 j)
+constexpr int64_t kMaxSplitSmm = 2048;       // small-M mode: j-splits (CTAs of a few rows each)
+constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
 
 // Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.  The
 // j-axis has `total` units (512-j tiles, or record pairs split in multiples of `grain`); every
 // split keeps at least `min_units`.
 int choose_split(int64_t itiles, int64_t total, int64_t grain, int64_t min_units, int64_t slots,
-                 double *eff_out) {
+                 double *eff_out, int64_t cap = kMaxSplit) {
     int best = 1;
     double best_score = -1.0, best_eff = 0.0;
-    const int smax = (int)std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, total / min_units));
+    const int smax = (int)std::min<int64_t>(cap, std::max<int64_t>(1, total / min_units));
     for (int S = 1; S <= smax; ++S) {
         const int64_t per = ((total + S - 1) / S + grain - 1) / grain * grain;
         const int64_t Seff = (total + per - 1) / per;
@@ -465,6 +468,27 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             pl.split = S;            // both kernels write S partials (empty ranges write zeros)
             pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
         }
+        // Small M (north star (a), the warp-shuffle finish): when even one-row-per-thread tiles
+        // split as far as j allows cannot fill the GPU, CTAs of a few rows whose 256 threads
+        // share the rows and split j take over (sum_smm.cu).  Not for tiny N (edge kernel).
+        bool smm = false;
+        // (A forced split_j keeps the row-tile kernels, so i-shards of one problem with the same
+        // split compute their rows bitwise as the unsharded call does.)
+        if (!tc && a->split_j <= 0 && N > kDirectMaxN && sum_smm_supported(mode, D, E)) {
+            const int64_t it1 = (M + kConsumerWarps * 32 - 1) / (kConsumerWarps * 32);
+            const int64_t smax = std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, pl.npv / kMinSplitPairs));
+            const int64_t slots1 = (int64_t)ctx->num_sms * occupancy(ctx, 0, mode, D, E, 1);
+            smm = it1 * smax < slots1;
+        }
+        if (smm) {
+            const int Rs = sum_smm_rows(mode);
+            const int64_t groups = (M + Rs - 1) / Rs;
+            const int64_t slots = (int64_t)ctx->num_sms * sum_smm_occupancy(mode, D);
+            const int S = choose_split(groups, pl.npv, kSplitGrain, kMinSmmPairs, slots, nullptr, kMaxSplitSmm);
+            pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+            pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+            pl.R = Rs;
+        }
         const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
@@ -491,8 +515,11 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // row, so the direct form is free and the bounding-box pass over x (a second full read
         // of x) is skipped; geo = nullptr selects the direct form on the device.
         const bool tiny_n = N <= kDirectMaxN && !tc;
-        if (tiny_n) geo = nullptr;
-        if (mode != 3 && !tiny_n) {
+        // Few rows (M <= kDirectMaxM): the pair loop is bound by streaming the j-records, so the
+        // direct form costs nothing and the bounding-box pass over y (a full read of y) is skipped.
+        const bool no_box = tiny_n || (M <= kDirectMaxM && !tc);
+        if (no_box) geo = nullptr;
+        if (mode != 3 && !no_box) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
@@ -536,7 +563,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.direct_only = tc ? 1 : 0;
         int sctas = 0;
         if (!tc) prof_event(ctx, true, st);
-        e = launch_sum(L, st, &sctas);
+        e = smm ? launch_sum_smm(L, st, &sctas) : launch_sum(L, st, &sctas);
         if (!tc) prof_event(ctx, false, st);
         if (!tc) ctas = sctas;
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
@@ -548,7 +575,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             kernels++;
         }
         ctx->launches += kernels;
-        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? pl.R : kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
         ctx->geo_dev = mode != 3 ? geo : nullptr;

@@ -75,6 +75,12 @@ struct SumLaunch {
     int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
+// Small-M mode (sum_smm.cu): CTAs of R = sum_smm_rows(mode) rows whose threads split j; grid =
+// ceil(M / R) * split, split-major.  E = 1, D <= 4 only (sum_smm_supported).
+bool sum_smm_supported(int mode, int D, int E);
+int sum_smm_rows(int mode);
+int sum_smm_occupancy(int mode, int D);
+cudaError_t launch_sum_smm(const SumLaunch &a, cudaStream_t st, int *ctas);
 int sum_occupancy(int mode, int D, int E, int R);
 int sum_rows_per_thread_max(int mode, int D, int E);
 

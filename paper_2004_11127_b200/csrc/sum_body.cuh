@@ -1,0 +1,369 @@
+// sum_body.cuh -- the Genred Sum pair loop, shared by sum_kernel.cu (row tiles: one thread per
+// row, R rows per thread) and sum_smm.cu (small M: the CTA's threads share R rows).  See
+// sum_kernel.cu for the design notes.
+#pragma once
+#include <math.h>
+#include <stdlib.h>
+
+#include "device.cuh"
+#include "geo.cuh"
+#include "internal.h"
+
+namespace genred {
+
+// Rows per thread of the gradient modes for D + E <= 4: 2 rows at 3 CTAs/SM measured 10.74
+// pairs/clk/SM against 10.48 for 4 rows at 2 CTAs/SM (fused Sum+grad, M = N = 1e5).
+#ifndef GENRED_GRAD_R
+#define GENRED_GRAD_R 2
+#endif
+#ifndef GENRED_GRAD_HH
+#define GENRED_GRAD_HH 2
+#endif
+
+template <int MODE, int D, int E>
+struct SumCfg {
+    // record pair: 2D coordinates, then (MODE 0 only) the pair slot of w = -|y'|^2 used by the
+    // expanded form, then 2E signal values; padded to a multiple of 16 bytes
+    static constexpr int BOFF = (MODE != 3) ? 2 * (D + 1) : 2 * D;
+    static constexpr int RS = ((BOFF + 2 * E) + 3) / 4 * 4;       // floats per record pair
+    static constexpr int PAIRS = kTileJ / 2;
+    static constexpr int TILE_FLOATS = PAIRS * RS;
+    static constexpr int NS = (MODE == 1) ? 0 : E;                // sum columns
+    static constexpr int NG = (MODE == 1 || MODE == 2) ? D : 0;   // gradient columns
+    static constexpr int C = NS + NG;
+    static constexpr bool GRAD = NG > 0;
+    static constexpr bool EXP = MODE != 3;
+    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
+};
+
+struct SumParams {
+    const float *x, *J, *g;
+    const uint32_t *geo;      // Gaussian modes: encoded bounding box (geo.cuh)
+    int64_t M;
+    int split;
+    int64_t pairs_per_split;  // j-split length in record pairs (a multiple of kSplitGrain)
+    int64_t npv;              // record pairs to reduce: ceil(N/2) rounded up to kSplitGrain
+    float s;
+    double scale_sum, scale_grad;
+    void *out;
+    int out_f64;
+    float *out_grad;
+    double *part;
+    const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
+    int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
+};
+
+// Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
+// 14.90 with every exp on MUFU (M = N = 1e6, B200): the packed FFMA2s of the expanded form read
+// three register pairs and already load the FP32 pipe close to the MUFU time, so the share is off.
+constexpr bool kPolyShare = false;
+
+// The pair loop + epilogue.  XP selects the expanded form of the Gaussian Sum (MODE 0 only):
+//   exp(-|x-y|^2/sigma^2) = 2^(-|x'|^2) * 2^(u),  u = 2 x'.y' - |y'|^2,  x' = s (x - c)
+// so a pair costs 3 FFMA (u, packed over two j's) + exp + 1 FFMA instead of 7 FP32 ops, which
+// leaves the MUFU pipe (16 ex2/clk/SM) as the only bound; the row factor 2^(-|x'|^2) is applied
+// in fp64 at the end.
+// SMM (small-M mode, north star (a) "a warp-shuffle finish runs when several threads share one
+// i"): all 256 threads of the CTA share the same R rows and split each tile's record pairs among
+// themselves (thread t takes pairs t, t + 256, ...); at the end the CTA reduces its fp64 partials
+// with warp shuffles (fixed butterfly order) and a fixed-order sum over the 8 warps, and thread 0
+// runs the epilogue for the R rows.  Used when M is too small to fill the GPU with row tiles.
+template <int MODE, int D, int E, int R, bool XP, bool SMM>
+__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt, int last_np,
+                                         int64_t row0, int64_t row_end, int sp, const Geo &geo) {
+    using Cfg = SumCfg<MODE, D, E>;
+    constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
+    constexpr bool POLY = kPolyShare && XP && R == 4;
+    constexpr int HH = SMM ? 1 : (MODE == 1 || MODE == 2) ? GENRED_GRAD_HH : 2;   // record pairs per iteration
+    const int ct = threadIdx.x;
+    float xr[R][D];
+    float gr[R][E];
+    double xsq[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = SMM ? row0 + r : row0 + r * (kConsumerWarps * 32) + ct;
+        const bool ok = i < row_end;
+        xsq[r] = 0.0;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const float v = ok ? __ldg(p.x + i * D + d) : 0.0f;
+            if constexpr (XP) {
+                const float xs = ok ? p.s * (v - geo.c[d]) : 0.0f;        // x' = s (x - c)
+                xsq[r] += (double)xs * (double)xs;
+                xr[r][d] = 2.0f * xs;                                      // exact doubling
+            } else {
+                xr[r][d] = p.s * v;
+            }
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+            gr[r][e] = (Cfg::GRAD && E > 1 && ok && p.g) ? __ldg(p.g + i * E + e) : 1.0f;
+    }
+    float2 acc[R][NS > 0 ? NS : 1];
+    float2 accg[R][NG > 0 ? NG : 1];
+    double acc64[R][C];
+    // expanded gradient: G_i ~ x'_i S0_i - S_i with S0 = sum_j w_ij, S = sum_j w_ij y'_j; S0 is the
+    // Sum itself when MODE == 2 and E == 1 (w = e b), else it has its own accumulator
+    constexpr bool OWN_S0 = XP && NG > 0 && !(MODE == 2 && E == 1);
+    float2 s0[R];
+    double s064[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        s0[r] = make_float2(0.f, 0.f);
+        s064[r] = 0.0;
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc64[r][c] = 0.0;
+#pragma unroll
+        for (int c = 0; c < (NS > 0 ? NS : 1); ++c) acc[r][c] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < (NG > 0 ? NG : 1); ++c) accg[r][c] = make_float2(0.f, 0.f);
+    }
+
+    for (int k = 0; k < nt; ++k) {
+        const float *tile = ring.acquire(k);
+        // record pairs of this tile: whole tiles, except the range's last one (a multiple of
+        // kSplitGrain, so of HH)
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
+        for (int pp2 = SMM ? ct : 0; pp2 < np; pp2 += SMM ? kThreads : HH) {
+#pragma unroll
+        for (int hh = 0; hh < HH; ++hh) {
+            const int pp = pp2 + hh;
+            float f[RS];
+#pragma unroll
+            for (int q = 0; q < RS / 4; ++q) {
+                const float4 v = lds128(tile + pp * RS + 4 * q);
+                f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+            }
+            float2 ny[D], bv[E];
+#pragma unroll
+            for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
+#pragma unroll
+            for (int e = 0; e < E; ++e) bv[e] = make_float2(f[BOFF + 2 * e], f[BOFF + 2 * e + 1]);
+            if constexpr (XP) {
+                const float2 w = make_float2(f[2 * D], f[2 * D + 1]);              // -|y'|^2
+                // (a coordinate-major order over the rows, meant to share y'_d through the register
+                // reuse cache, measured 0.8% slower for the Sum and no change for the fused
+                // gradient: ptxas schedules either way)
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 u = fma2(dup2(xr[r][0]), ny[0], w);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(dup2(xr[r][d]), ny[d], u);   // 2x'.y' - |y'|^2
+                    float2 ex;
+                    // FP32-pipe exp2 share (kPolyShare, off: see DESIGN.md Sec. 6 measurements)
+                    if (POLY && r == R - 1 && hh == 0) ex = ex2_poly2(u);
+                    else ex = make_float2(ex2(u.x), ex2(u.y));
+                    if constexpr (NG == 0) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                    } else {
+                        float2 wt;
+                        if constexpr (E == 1) {
+                            wt = mul2(ex, bv[0]);                       // e b (g_i applied later)
+                        } else {
+                            float2 bg = mul2(bv[0], dup2(gr[r][0]));
+#pragma unroll
+                            for (int e = 1; e < E; ++e) bg = fma2(bv[e], dup2(gr[r][e]), bg);
+                            wt = mul2(ex, bg);                          // e <b, g_i>
+                        }
+                        if constexpr (MODE == 2 && E == 1) {
+                            acc[r][0] = add2(acc[r][0], wt);           // Sum == S0
+                        } else {
+                            if constexpr (MODE == 2) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                            }
+                            s0[r] = add2(s0[r], wt);
+                        }
+                        // (two scalar FFMAs instead of this 3-register-pair FFMA2 measured 2% slower)
+#pragma unroll
+                        for (int d = 0; d < D; ++d) accg[r][d] = fma2(wt, ny[d], accg[r][d]);   // w y'
+                    }
+                }
+            } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 dd[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) dd[d] = add2(dup2(xr[r][d]), ny[d]);   // x' - y'
+                float2 q = mul2(dd[0], dd[0]);
+#pragma unroll
+                for (int d = 1; d < D; ++d) q = fma2(dd[d], dd[d], q);             // |x'-y'|^2
+                if constexpr (!Cfg::EXP) {
+#pragma unroll
+                    for (int e = 0; e < E; ++e) acc[r][e] = fma2(q, bv[e], acc[r][e]);
+                } else {
+                    const float2 ex = make_float2(ex2(-q.x), ex2(-q.y));   // e^{-|x-y|^2/sigma^2}
+                    if constexpr (MODE == 0) {
+#pragma unroll
+                        for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                    } else {
+                        float2 w;
+                        if constexpr (E == 1) {
+                            w = mul2(ex, bv[0]);                   // e_ij b_j (g_i applied later)
+                            if constexpr (MODE == 2) acc[r][0] = add2(acc[r][0], w);
+                        } else {
+                            float2 bg = mul2(bv[0], dup2(gr[r][0]));
+#pragma unroll
+                            for (int e = 1; e < E; ++e) bg = fma2(bv[e], dup2(gr[r][e]), bg);
+                            w = mul2(ex, bg);                      // e_ij <b_j, g_i>
+                            if constexpr (MODE == 2) {
+#pragma unroll
+                                for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
+                            }
+                        }
+#pragma unroll
+                        for (int d = 0; d < D; ++d) accg[r][d] = fma2(w, dd[d], accg[r][d]);
+                    }
+                }
+            }
+            }
+        }
+        }
+        ring.release(k);
+        // promote the tile's fp32 partials to fp64 (every 512 j)
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int c = 0; c < NS; ++c) {
+                acc64[r][c] += (double)acc[r][c].x + (double)acc[r][c].y;
+                acc[r][c] = make_float2(0.f, 0.f);
+            }
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                acc64[r][NS + c] += (double)accg[r][c].x + (double)accg[r][c].y;
+                accg[r][c] = make_float2(0.f, 0.f);
+            }
+            if constexpr (OWN_S0) {
+                s064[r] += (double)s0[r].x + (double)s0[r].y;
+                s0[r] = make_float2(0.f, 0.f);
+            }
+        }
+    }
+
+    if constexpr (SMM) {
+        // CTA reduction of the per-thread fp64 partials (deterministic), result in thread 0
+        constexpr int CO = C + (OWN_S0 ? 1 : 0);
+        __shared__ double red[kConsumerWarps][R * CO];
+        const int lane = ct & 31, warp = ct >> 5;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int c = 0; c < CO; ++c) {
+                double v = c < C ? acc64[r][c] : s064[r];
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) red[warp][r * CO + c] = v;
+            }
+        }
+        __syncthreads();
+        if (ct != 0) return;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+#pragma unroll
+            for (int c = 0; c < CO; ++c) {
+                double v = red[0][r * CO + c];
+#pragma unroll
+                for (int w = 1; w < kConsumerWarps; ++w) v += red[w][r * CO + c];
+                if (c < C) acc64[r][c] = v;
+                else s064[r] = v;
+            }
+        }
+    }
+
+    // ---- epilogue --------------------------------------------------------------------------
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = SMM ? row0 + r : row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= row_end) continue;
+        if constexpr (XP) {
+            const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
+            if constexpr (NG > 0) {
+                // sum_j w_ij (x'_i - y'_j) = x'_i S0_i - S_i  (the kernel's d' convention)
+                const double S0 = OWN_S0 ? s064[r] : acc64[r][0];
+#pragma unroll
+                for (int c = 0; c < NG; ++c)
+                    acc64[r][NS + c] = 0.5 * (double)xr[r][c] * S0 - acc64[r][NS + c];
+            }
+#pragma unroll
+            for (int c = 0; c < C; ++c) acc64[r][c] *= fac;
+        }
+        if (p.split > 1) {
+            double *dst = p.part + ((int64_t)sp * p.M + i) * C;
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst[c] = acc64[r][c];
+            continue;
+        }
+#pragma unroll
+        for (int c = 0; c < NS; ++c) {
+            const double v = acc64[r][c] * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i * NS + c] = v;
+            else ((float *)p.out)[i * NS + c] = (float)v;
+        }
+        if constexpr (NG > 0) {
+            double gs = p.scale_grad;
+            if (E == 1 && p.g) gs *= (double)__ldg(p.g + i);
+#pragma unroll
+            for (int c = 0; c < NG; ++c) {
+                const double v = acc64[r][NS + c] * gs;
+                if (MODE == 2) p.out_grad[i * D + c] = (float)v;
+                else if (p.out_f64) ((double *)p.out)[i * D + c] = v;
+                else ((float *)p.out)[i * D + c] = (float)v;
+            }
+        }
+    }
+}
+
+template <int MODE, int D, int E, int R, bool SMM = false>
+__global__ void __launch_bounds__(kThreads, (!SMM && (((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ||
+                                            ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && E == 1 && R == 2))) ? 3 : 2)
+sum_kernel(const SumParams p) {
+    using Cfg = SumCfg<MODE, D, E>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+
+    // this CTA's j-range: record pairs [q0, q0 + npc), streamed in tiles of PAIRS
+    int64_t row0, row_end, q0, npc;
+    int sp;
+    if (p.units) {                                     // block-sparse: rows of one cluster
+        const RangeUnit u = p.units[blockIdx.x];
+        row0 = u.row0; row_end = u.row_end; sp = 0;
+        q0 = u.tile0 * Cfg::PAIRS; npc = u.ntiles * Cfg::PAIRS;
+    } else if (SMM) {
+        // split-major: concurrently running CTAs share a j-range (L2 reuse across row groups)
+        const int64_t ngroups = (p.M + R - 1) / R;
+        sp = (int)(blockIdx.x / ngroups);
+        row0 = (int64_t)(blockIdx.x % ngroups) * R;
+        row_end = p.M;
+        q0 = (int64_t)sp * p.pairs_per_split;
+        npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    } else {
+        const int64_t itile = blockIdx.x / p.split;
+        sp = (int)(blockIdx.x % p.split);
+        q0 = (int64_t)sp * p.pairs_per_split;
+        npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);   // empty: zero partial
+        row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+        row_end = p.M;
+    }
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
+    const uint32_t last_bytes = (uint32_t)last_np * Cfg::RS * 4u;   // a partial last tile is copied partially
+
+    JRing<kStages> ring;
+    if constexpr (MODE != 3) {
+        const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
+        if (MODE == 0 && p.direct_only && geo.expanded) return;   // gauss_tc.cu took this call
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
+        if (geo.expanded) sum_body<MODE, D, E, R, true, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+        else sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+    } else {
+        ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
+        Geo geo{};
+        sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+    }
+}
+
+
+}  // namespace genred

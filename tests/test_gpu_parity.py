@@ -459,6 +459,35 @@ def test_gauss_sum_expanded_and_direct_paths(G, case):
     assert_sum_parity(host(a), o, den, what=f"gauss {case}")
 
 
+@pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
+@pytest.mark.parametrize("M,N,D", [(1, 200_000, 3), (5, 70_001, 2), (37, 150_000, 4), (300, 100_000, 1)])
+def test_small_m_mode(G, formula, M, N, D):
+    """Small M (north star (a)): CTAs of a few rows whose threads split j and finish with warp
+    shuffles; many j-splits merged by the warp finalize.  Against the oracle, and bitwise
+    reproducible run to run."""
+    rng = np.random.default_rng(M + N + D)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = synth.signal(N, 161, signed=True); g = synth.cotangent(M, 162)
+    sigma = 0.5 if formula != "sqdist" else 1.0
+    args = (dev(x), dev(y), dev(b)) + ((dev(g),) if "grad" in formula else ())
+    res = G.eval(formula, "sum", *args, scale=sigma)
+    plan = G.last_plan()
+    assert plan["rows_per_cta"] <= 8 and plan["split_j"] > 1, plan          # small-M mode taken
+    res2 = G.eval(formula, "sum", *args, scale=sigma)
+    for r1, r2 in zip(res if isinstance(res, tuple) else (res,), res2 if isinstance(res2, tuple) else (res2,)):
+        np.testing.assert_array_equal(host(r1), host(r2))
+    if formula == "sqdist":
+        o, den = oracle.sqdist_sum(x, y, b)
+        assert_sum_parity(host(res), o, den, what=f"smm sqdist M={M}")
+        return
+    if formula in ("gauss", "gauss_sum_gradx"):
+        o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+        assert_sum_parity(host(res[0] if isinstance(res, tuple) else res), o, den, what=f"smm sum M={M}")
+    if "grad" in formula:
+        og, deng = oracle.gauss_gradx(x, y, b, g, sigma=sigma)
+        assert_sum_parity(host(res[1] if isinstance(res, tuple) else res), og, deng, what=f"smm grad M={M}")
+
+
 @pytest.mark.parametrize("D", [1, 2, 4, 5])
 def test_gauss_sum_tiny_n_dims_f64(G, D):
     """Edge kernel for D = 1, 2, 4 (D = 5: the generic kernel) with fp64 output and a partial
@@ -516,7 +545,7 @@ def test_gauss_tc_path(G, monkeypatch, M, N, D, signed, split):
     assert_sum_parity(host(a), o, den, what=f"gauss tc {M}x{N} D{D}")
     monkeypatch.setenv("GENRED_GAUSS_TC", "0")
     a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split, out_dtype="float64")
-    assert G.last_plan()["path"] == (2 if N > 64 else 0)          # tiny N: direct form, no bbox
+    assert G.last_plan()["path"] == (2 if N > 64 and M > 16 else 0)   # tiny N or M: direct form, no bbox
     assert_sum_parity(host(a2), o, den, what="gauss fp32 expanded")
 
 
