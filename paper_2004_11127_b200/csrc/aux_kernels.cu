@@ -413,8 +413,53 @@ __global__ void lse_finalize_kernel(const double *__restrict__ part, int split, 
     }
 }
 
+// Many splits: one warp per row; the max and the rescaled sum run lane-strided in a fixed order
+// and finish with fixed butterflies (deterministic).
+__global__ void lse_finalize_warp_kernel(const double *__restrict__ part, int split, int64_t M, void *out,
+                                         int out_f64, double *state_out) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t i = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5; i < M;
+         i += ((int64_t)gridDim.x * blockDim.x) >> 5) {
+        double mstar = -INFINITY;
+        for (int q = lane; q < split; q += 32) {
+            const double s = part[((int64_t)q * M + i) * 2 + 1];
+            const double m = part[((int64_t)q * M + i) * 2 + 0];
+            if (s > 0.0 && m > mstar) mstar = m;
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mstar = fmax(mstar, __shfl_xor_sync(0xffffffffu, mstar, o));
+        double S = 0.0;
+        if (mstar > -INFINITY) {
+            for (int q = lane; q < split; q += 32) {
+                const double m = part[((int64_t)q * M + i) * 2 + 0];
+                const double s = part[((int64_t)q * M + i) * 2 + 1];
+                if (s > 0.0) S += s * exp2(m - mstar);
+            }
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+        if (lane != 0) continue;
+        const double a = (S > 0.0) ? 0.69314718055994530942 * (mstar + log2(S)) : -INFINITY;
+        if (out) {
+            if (out_f64) ((double *)out)[i] = a;
+            else ((float *)out)[i] = (float)a;
+        }
+        if (state_out) {
+            state_out[2 * i + 0] = (S > 0.0) ? mstar : (double)kLseSentinel;
+            state_out[2 * i + 1] = S;
+        }
+    }
+}
+
 cudaError_t launch_lse_finalize(const double *part, int split, int64_t M, void *out, int out_f64,
                                 double *state_out, cudaStream_t st) {
+    if (split > 32) {
+        int64_t blocks = (M * 32 + 255) / 256;
+        if (blocks > 148 * 8) blocks = 148 * 8;
+        if (blocks < 1) blocks = 1;
+        lse_finalize_warp_kernel<<<(unsigned)blocks, 256, 0, st>>>(part, split, M, out, out_f64, state_out);
+        return cudaGetLastError();
+    }
     int64_t blocks = (M + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;

@@ -45,7 +45,8 @@ struct genred_ctx {
 namespace {
 
 constexpr double kLog2e = 1.4426950408889634074;
-constexpr int kMaxSplit = 64;
+constexpr int kMaxSplit = 64;                // 512-j tile splits (ArgKMin, LSE_GRAD)
+constexpr int kMaxSplitPairs = 1024;         // record-pair splits (Sum, LSE): merged by warp finalizes
 
 genred_status fail(genred_ctx *ctx, genred_status st, const std::string &msg) {
     if (ctx) ctx->err = msg;
@@ -155,13 +156,14 @@ constexpr int64_t kDirectMaxN = 64;          // Gaussian Sum: N at or below -> d
 constexpr int64_t kDirectMaxM = 16;          // Gaussian Sum: M at or below -> direct form, no bbox
 constexpr int64_t kMinSplitPairs = 64;       // shortest record-pair j-split (128 j)
 constexpr int64_t kMaxSplitSmm = 2048;       // small-M mode: j-splits (CTAs of a few rows each)
+constexpr int64_t kSmmMaxM = 64;             // small-M mode for M at or below
 constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
 
 // Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.  The
 // j-axis has `total` units (512-j tiles, or record pairs split in multiples of `grain`); every
 // split keeps at least `min_units`.
 int choose_split(int64_t itiles, int64_t total, int64_t grain, int64_t min_units, int64_t slots,
-                 double *eff_out, int64_t cap = kMaxSplit) {
+                 double *eff_out, int64_t cap = kMaxSplit, double penalty = 0.002) {
     int best = 1;
     double best_score = -1.0, best_eff = 0.0;
     const int smax = (int)std::min<int64_t>(cap, std::max<int64_t>(1, total / min_units));
@@ -172,7 +174,7 @@ int choose_split(int64_t itiles, int64_t total, int64_t grain, int64_t min_units
         const int64_t U = itiles * S;
         const int64_t waves = (U + slots - 1) / slots;
         const double eff = (double)U / (double)(waves * slots);
-        const double score = eff - 0.002 * S;
+        const double score = eff - penalty * S;
         if (score > best_score + 1e-12) { best_score = score; best = S; best_eff = eff; }
     }
     if (eff_out) *eff_out = best_eff;
@@ -205,14 +207,18 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
         const int64_t slots = (int64_t)ctx->num_sms * occupancy(ctx, kind, occ_kind_a, occ_kind_b, occ_kind_c, R);
         int S;
         double eff;
+        const int64_t cap = pair_splits ? kMaxSplitPairs : kMaxSplit;
         if (a->split_j > 0) {
-            S = (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), std::max<int64_t>(1, total / grain));
+            S = (int)std::min<int64_t>(std::min<int64_t>(a->split_j, cap), std::max<int64_t>(1, total / grain));
             const int64_t U = itiles * S, waves = (U + slots - 1) / slots;
             eff = (double)U / (double)(waves * slots);
         } else {
-            S = choose_split(itiles, total, grain, min_units, slots, &eff);
+            // (pair splits: a smaller per-split penalty lets small M spread over many splits)
+            S = choose_split(itiles, total, grain, min_units, slots, &eff, cap, pair_splits ? 2e-4 : 0.002);
         }
-        const double score = eff * (R == rmax ? 1.0 : 0.9);      // fewer rows/thread costs issue slots
+        // fewer rows/thread costs issue slots; rows past M in the last row tile are wasted work
+        const double util = (double)a->M / (double)(itiles * rows);
+        const double score = eff * util * (R == rmax ? 1.0 : 0.9);
         if (score > best || (a->split_j > 0 && R == rmax)) {
             best = score;
             pl.R = R; pl.split = S; pl.itiles = itiles;
@@ -474,12 +480,10 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         bool smm = false;
         // (A forced split_j keeps the row-tile kernels, so i-shards of one problem with the same
         // split compute their rows bitwise as the unsharded call does.)
-        if (!tc && a->split_j <= 0 && N > kDirectMaxN && sum_smm_supported(mode, D, E)) {
-            const int64_t it1 = (M + kConsumerWarps * 32 - 1) / (kConsumerWarps * 32);
-            const int64_t smax = std::min<int64_t>(kMaxSplit, std::max<int64_t>(1, pl.npv / kMinSplitPairs));
-            const int64_t slots1 = (int64_t)ctx->num_sms * occupancy(ctx, 0, mode, D, E, 1);
-            smm = it1 * smax < slots1;
-        }
+        // (Measured at N = 1e7: the small-M CTAs re-stream the j-records per R = 8 rows, so they
+        // pay off only while most threads of a one-row-per-thread tile would idle, M <= 64.)
+        if (!tc && a->split_j <= 0 && N > kDirectMaxN && M <= kSmmMaxM && sum_smm_supported(mode, D, E))
+            smm = true;
         if (smm) {
             const int Rs = sum_smm_rows(mode);
             const int64_t groups = (M + Rs - 1) / Rs;

@@ -5,7 +5,7 @@ import torch, synth
 from paper_2004_11127_b200 import genred
 N = int(sys.argv[1]) if len(sys.argv) > 1 else 10_000_000
 y = torch.from_numpy(synth.uniform3(N, 2)).cuda(); b = torch.from_numpy(synth.signal(N, 3)).cuda()
-for M in (1, 16, 256, 2048, 16384):
+for M in (1, 16, 64, 65, 256, 1024, 2048, 16384):
     x = torch.from_numpy(synth.uniform3(M, 1)).cuda()
     for red in ("sum", "lse"):
         f = (lambda: genred.eval("gauss", "sum", x, y, b, scale=0.5)) if red == "sum" else \
