@@ -174,7 +174,7 @@ typedef struct {
     int32_t kernels;         /* kernels launched by the last call */
     int32_t path;            /* 0 = FP32/MUFU small-D path, 1 = tcgen05 tensor path, 2 = Gaussian
                                 Sum expanded form with the FP32-pipe exp2 share (synchronises) */
-    int64_t scratch_bytes;   /* device scratch currently held by the context */
+    int64_t scratch_bytes;   /* device scratch the last call used (the context may hold more) */
     int64_t fallback_rows;   /* tensor path: rows whose 3xTF32 screening failed the margin
                                 certificate and were rescanned exactly (synchronises; else -1) */
 } genred_plan;

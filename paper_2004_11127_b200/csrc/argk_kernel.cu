@@ -29,7 +29,7 @@ struct ArgkParams {
     int64_t M;
     int K;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split, npv;      // record-pair j-splits (see SumParams)
     float *dist;
     int64_t *idx;
     int64_t j_offset;
@@ -66,12 +66,13 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 
     const int64_t itile = blockIdx.x / p.split;
     const int sp = (int)(blockIdx.x % p.split);
-    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
-    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-    const int nt = (int)(t1 - t0);
+    const int64_t q0 = (int64_t)sp * p.pairs_per_split;                   // record pairs [q0, q0 + npc)
+    const int64_t npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
 
     JRing<kStages> ring;
-    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * RS, nt, kConsumerWarps, (uint32_t)last_np * RS * 4u);
 
     const int ct = threadIdx.x;
     const int K = p.K;
@@ -93,9 +94,10 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-        const int32_t jbase = (int32_t)((t0 + k) * kTileJ);
+        const int32_t jbase = (int32_t)(2 * (q0 + (int64_t)k * Cfg::PAIRS));
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
 #pragma unroll 2
-        for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
+        for (int pp = 0; pp < np; ++pp) {
             float f[RS];
 #pragma unroll
             for (int u = 0; u < RS / 4; ++u) {
@@ -157,7 +159,7 @@ static cudaError_t run_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
     }
     ArgkParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.K = a.K; p.split = a.split;
-    p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.dist = a.dist; p.idx = a.idx;
+    p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.dist = a.dist; p.idx = a.idx;
     p.j_offset = a.j_offset; p.pdist = a.pdist; p.pidx = a.pidx;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t grid = ((a.M + rows - 1) / rows) * a.split;

@@ -509,6 +509,46 @@ cudaError_t launch_topk_merge_i32(const float *pd, const int32_t *pi, int split,
     return cudaGetLastError();
 }
 
+// Merge lists [64 g, 64 g + 64) of row i into list g (lexicographic (d, j), as topk_merge).
+__global__ void topk_merge_groups_kernel(const float *__restrict__ pd, const int32_t *__restrict__ pi,
+                                         int split, int64_t M, int K, float *gd, int32_t *gi) {
+    const int G1 = (split + 63) / 64;
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < M * G1;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int g = (int)(t / M);
+        const int64_t i = t % M;
+        const int q0 = 64 * g, nq = min(64, split - q0);
+        int head[64];
+        for (int q = 0; q < nq; ++q) head[q] = 0;
+        for (int k = 0; k < K; ++k) {
+            int best = -1;
+            float bd = INFINITY;
+            int32_t bj = -1;
+            for (int q = 0; q < nq; ++q) {
+                if (head[q] >= K) continue;
+                const int64_t off = ((int64_t)(q0 + q) * M + i) * K + head[q];
+                const int32_t j = pi[off];
+                if (j < 0) continue;
+                const float d = pd[off];
+                if (best < 0 || d < bd || (d == bd && (uint32_t)j < (uint32_t)bj)) { best = q; bd = d; bj = j; }
+            }
+            const int64_t o = ((int64_t)g * M + i) * K + k;
+            if (best >= 0) { head[best]++; gd[o] = bd; gi[o] = bj; }
+            else { gd[o] = INFINITY; gi[o] = -1; }
+        }
+    }
+}
+
+cudaError_t launch_topk_merge_groups(const float *pd, const int32_t *pi, int split, int64_t M, int K,
+                                     float *gd, int32_t *gi, cudaStream_t st) {
+    const int64_t work = M * ((split + 63) / 64);
+    int64_t blocks = (work + 127) / 128;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    topk_merge_groups_kernel<<<(unsigned)blocks, 128, 0, st>>>(pd, pi, split, M, K, gd, gi);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_topk_merge_i64(const float *pd, const int64_t *pi, int G, int64_t M, int K,
                                   float *dist, int64_t *idx, cudaStream_t st) {
     int64_t blocks = (M + 127) / 128;

@@ -26,6 +26,7 @@ struct genred_ctx {
     std::string err;
     void *scratch = nullptr;
     size_t scratch_cap = 0;
+    size_t scratch_need = 0;                                   // bytes the last call used
     void *stage = nullptr;
     size_t stage_cap = 0;
     genred_plan plan{};
@@ -174,7 +175,9 @@ int choose_split(int64_t itiles, int64_t total, int64_t grain, int64_t min_units
         const int64_t U = itiles * S;
         const int64_t waves = (U + slots - 1) / slots;
         const double eff = (double)U / (double)(waves * slots);
-        const double score = eff - penalty * S;
+        // relative penalty: prefer fewer splits at equal efficiency, but never trade a fuller GPU
+        // for fewer splits (an absolute penalty made tiny-M launches pick S = 1: one CTA)
+        const double score = eff * (1.0 - penalty * S);
         if (score > best_score + 1e-12) { best_score = score; best = S; best_eff = eff; }
     }
     if (eff_out) *eff_out = best_eff;
@@ -236,6 +239,7 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
 }
 
 genred_status ensure(genred_ctx *ctx, void **buf, size_t *cap, size_t need) {
+    if (buf == &ctx->scratch) ctx->scratch_need = need;
     if (need <= *cap) return GENRED_OK;
     size_t n = std::max(need, *cap + *cap / 2);
     n = (n + 255) & ~size_t(255);
@@ -361,7 +365,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->launches += kernels;
         ctx->plan.split_j = 1; ctx->plan.rows_per_cta = (int32_t)RT; ctx->plan.ctas = ctas;
         ctx->plan.kernels = kernels; ctx->plan.path = 0;
-        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;
     }
     SumLaunch L;
@@ -381,7 +385,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     ctx->launches += kernels;
     ctx->plan.split_j = 1; ctx->plan.rows_per_cta = (int32_t)RT; ctx->plan.ctas = ctas;
     ctx->plan.kernels = kernels; ctx->plan.path = 0;
-    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
     ctx->geo_dev = mode != 3 ? geo : nullptr;
     ctx->geo_D = D;
     ctx->geo_s = sc;
@@ -448,7 +452,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
-        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;
     }
 
@@ -554,7 +558,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             ctx->launches += kernels;
             ctx->plan.split_j = 1; ctx->plan.rows_per_cta = 1024; ctx->plan.ctas = ctas;
             ctx->plan.kernels = kernels; ctx->plan.path = 0; ctx->plan.tile_j = (int32_t)N;
-            ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+            ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
             ctx->geo_dev = nullptr;
             ctx->geo_tc = false;
             return GENRED_OK;
@@ -581,7 +585,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? pl.R : kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
-        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         ctx->geo_dev = mode != 3 ? geo : nullptr;
         ctx->geo_tc = tc;
         ctx->geo_D = D;
@@ -624,7 +628,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
-        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;
     }
 
@@ -647,28 +651,32 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->fallback_dev = info.fallback_count;
         ctx->plan.split_j = 1; ctx->plan.rows_per_cta = 128; ctx->plan.ctas = info.ctas;
         ctx->plan.kernels = info.kernels; ctx->plan.path = 1; ctx->plan.tile_j = 256;
-        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;
     }
 
     // ArgKMin, small D, FP32 path
     const int K = a->K;
     const int R = argk_rows_per_thread(K);
-    Plan pl = make_plan(ctx, a, 2, R, D, K, 0);
+    Plan pl = make_plan(ctx, a, 2, R, D, K, 0, true);
     const int RS = pack_record_stride(PACK_ARGKMIN, D, 0);
     const int64_t npairs = pl.ntiles * (kTileJ / 2);
     const size_t jbytes = al256((size_t)npairs * RS * 4);
     const size_t pdb = pl.split > 1 ? al256((size_t)pl.split * M * K * 4) : 0;
-    genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + 2 * pdb);
+    const int G1 = pl.split > 64 ? (pl.split + 63) / 64 : 0;        // two-level merge above 64 lists
+    const size_t gdb = G1 ? al256((size_t)G1 * M * K * 4) : 0;
+    genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + 2 * pdb + 2 * gdb);
     if (s != GENRED_OK) return s;
     float *J = (float *)ctx->scratch;
     float *pdist = pl.split > 1 ? (float *)((char *)ctx->scratch + jbytes) : nullptr;
     int32_t *pidx = pl.split > 1 ? (int32_t *)((char *)ctx->scratch + jbytes + pdb) : nullptr;
+    float *gdist = G1 ? (float *)((char *)ctx->scratch + jbytes + 2 * pdb) : nullptr;
+    int32_t *gidx = G1 ? (int32_t *)((char *)ctx->scratch + jbytes + 2 * pdb + gdb) : nullptr;
     e = launch_pack(PACK_ARGKMIN, a->y, nullptr, N, D, 0, 1.0f, 0.0, npairs, J, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
     ArgkLaunch L;
     L.D = D; L.K = K; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
-    L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+    L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv;
     L.dist = (float *)a->out; L.idx = a->out_idx; L.j_offset = a->j_offset;
     L.pdist = pdist; L.pidx = pidx;
     int ctas = 0;
@@ -677,7 +685,13 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     prof_event(ctx, false, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "argkmin kernel");
     int kernels = 2;
-    if (pl.split > 1) {
+    if (G1) {
+        e = launch_topk_merge_groups(pdist, pidx, pl.split, M, K, gdist, gidx, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "top-k group merge kernel");
+        e = launch_topk_merge_i32(gdist, gidx, G1, M, K, (float *)a->out, a->out_idx, a->j_offset, st);
+        if (e != cudaSuccess) return cuda_fail(ctx, e, "top-k merge kernel");
+        kernels += 2;
+    } else if (pl.split > 1) {
         e = launch_topk_merge_i32(pdist, pidx, pl.split, M, K, (float *)a->out, a->out_idx,
                                   a->j_offset, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "top-k merge kernel");
@@ -686,7 +700,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     ctx->launches += kernels;
     ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
     ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
-    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_cap;
+    ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
     return GENRED_OK;
 }
 

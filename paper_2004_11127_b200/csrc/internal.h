@@ -107,7 +107,7 @@ struct ArgkLaunch {
     const float *x, *J;
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split, npv;                  // record-pair j-splits (multiple of kSplitGrain)
     float *dist; int64_t *idx; int64_t j_offset;   // split == 1 outputs
     float *pdist; int32_t *pidx;                   // split > 1: split x M x K partials
 };
@@ -193,6 +193,10 @@ cudaError_t launch_lse_finalize(const double *part, int split, int64_t M, void *
                                 double *state_out, cudaStream_t st);
 cudaError_t launch_topk_merge_i32(const float *pd, const int32_t *pi, int split, int64_t M, int K,
                                   float *dist, int64_t *idx, int64_t j_offset, cudaStream_t st);
+// First level of a two-level merge for split > 64: groups of 64 lists -> ceil(split / 64) lists
+// in the same (split-major) partial layout.
+cudaError_t launch_topk_merge_groups(const float *pd, const int32_t *pi, int split, int64_t M, int K,
+                                     float *gd, int32_t *gi, cudaStream_t st);
 cudaError_t launch_topk_merge_i64(const float *pd, const int64_t *pi, int G, int64_t M, int K,
                                   float *dist, int64_t *idx, cudaStream_t st);
 cudaError_t launch_fill(int kind, int64_t M, int C, int K, void *out, int out_f64, float *out_grad,

@@ -285,12 +285,25 @@ def test_argkmin_lattice_ties(G):
     assert host(d)[0].tolist() == [0, 1, 1, 1, 1, 1, 1, 2]
 
 
-@pytest.mark.parametrize("split", [1, 3])
+@pytest.mark.parametrize("split", [1, 3, 100])
 def test_argkmin_duplicates_across_splits(G, split):
     y = np.tile(np.array([[0.5, 0.5, 0.5]], np.float32), (4000, 1))
     x = np.array([[0.5, 0.5, 0.5], [0.4, 0.5, 0.5]], np.float32)
     d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=6, split_j=split)
     assert host(j).tolist() == [[0, 1, 2, 3, 4, 5]] * 2
+
+
+@pytest.mark.parametrize("M,K", [(1, 1), (3, 10), (50, 32)])
+def test_argkmin_small_m_many_splits(G, M, K):
+    """Few query rows against a large N: many record-pair j-splits whose K-lists merge in two
+    levels (groups of 64, then the group lists) under the (d, j) order."""
+    N = 400_000
+    rng = np.random.default_rng(M * 7 + K)
+    x = rng.random((M, 3)).astype(np.float32); y = rng.random((N, 3)).astype(np.float32)
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+    assert G.last_plan()["split_j"] > 64, G.last_plan()
+    od, oj = oracle.argkmin(x, y, K + 1)
+    argk_check(host(d), host(j), od, oj, K, what=f"argk small M={M} K={K}")
 
 
 # ------------------------------------------------------------------------------------------------
