@@ -16,6 +16,9 @@ namespace genred {
 #ifndef GENRED_GRAD_R
 #define GENRED_GRAD_R 2
 #endif
+#ifndef GENRED_GRAD_MINB
+#define GENRED_GRAD_MINB 3
+#endif
 #ifndef GENRED_GRAD_HH
 #define GENRED_GRAD_HH 2
 #endif
@@ -317,9 +320,17 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     }
 }
 
+// CTAs per SM the register allocation must allow (the 16 K registers of each SM sub-partition)
+template <int MODE, int D, int E, int R, bool SMM>
+constexpr int sum_min_blocks() {
+    if (SMM) return 2;
+    if ((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) return 3;
+    if ((MODE == 1 || MODE == 2) && D + E <= 4 && E == 1 && R == GENRED_GRAD_R) return GENRED_GRAD_MINB;
+    return 2;
+}
+
 template <int MODE, int D, int E, int R, bool SMM = false>
-__global__ void __launch_bounds__(kThreads, (!SMM && (((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) ||
-                                            ((MODE == 1 || MODE == 2) && GENRED_GRAD_R == 2 && D + E <= 4 && E == 1 && R == 2))) ? 3 : 2)
+__global__ void __launch_bounds__(kThreads, sum_min_blocks<MODE, D, E, R, SMM>())
 sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
