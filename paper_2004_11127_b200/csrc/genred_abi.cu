@@ -596,6 +596,17 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     if (red == GENRED_LSE) {
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, 4, lse_rows_per_thread_max(D));
         Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0, true);
+        // small M: CTAs of a few rows whose threads split j (see the Sum path)
+        const bool smm = a->split_j <= 0 && M <= kSmmMaxM && N > kDirectMaxN;
+        if (smm) {
+            const int Rs = lse_smm_rows(D);
+            const int64_t groups = (M + Rs - 1) / Rs;
+            const int S = choose_split(groups, pl.npv, kSplitGrain, kMinSmmPairs, (int64_t)ctx->num_sms * 2,
+                                       nullptr, kMaxSplitSmm);
+            pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+            pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+            pl.R = Rs;
+        }
         const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
         const int RS = pack_record_stride(pk, D, 1);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
@@ -616,7 +627,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.state = pl.split > 1 ? part : a->lse_state;
         int ctas = 0;
         prof_event(ctx, true, st);
-        e = launch_lse(L, st, &ctas);
+        e = smm ? launch_lse_smm(L, st, &ctas) : launch_lse(L, st, &ctas);
         prof_event(ctx, false, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "lse kernel");
         int kernels = 2;
@@ -626,7 +637,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             kernels++;
         }
         ctx->launches += kernels;
-        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+        ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? pl.R : kConsumerWarps * 32 * pl.R;
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;

@@ -99,6 +99,10 @@ struct LseLaunch {
     int64_t n_units = 0;
 };
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
+// Small-M mode (lse_kernel.cu): CTAs of lse_smm_rows(D) rows whose threads split j; grid =
+// ceil(M / R) * split, split-major, 2 CTAs per SM.
+int lse_smm_rows(int D);
+cudaError_t launch_lse_smm(const LseLaunch &a, cudaStream_t st, int *ctas);
 int lse_occupancy(int D, int R);
 int lse_rows_per_thread_max(int D);
 

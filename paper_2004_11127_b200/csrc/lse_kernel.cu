@@ -66,11 +66,11 @@ struct LseRescale {
 };
 
 // Out of line so that its registers do not burden the hot loop.
-template <int D, bool HZ, int RS>
+template <int D, bool HZ, int RS, int NSUB = kSub>
 __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&xr)[D], float negc,
                                                float m_old, double s64, float2 s32) {
     float vmax = -INFINITY;
-    for (int q = 0; q < kSub; ++q) {
+    for (int q = 0; q < NSUB; ++q) {
         const float *rec = base + q * RS;
         for (int h = 0; h < 2; ++h) {
             float q1 = 0.f;
@@ -88,7 +88,7 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
     o.m = fmaxf(vmax, m_old);
     o.s64 = (s64 + (double)s32.x + (double)s32.y) * exp2((double)m_old - (double)o.m);
     float c1 = 0.f;
-    for (int q = 0; q < kSub; ++q) {
+    for (int q = 0; q < NSUB; ++q) {
         const float *rec = base + q * RS;
         for (int h = 0; h < 2; ++h) {
             float q1 = 0.f;
@@ -235,6 +235,172 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
             p.state[2 * i + 1] = stot;
         }
     }
+}
+
+// Small-M mode (north star (a), the warp-shuffle finish; see sum_smm.cu): a CTA owns R rows, its
+// 256 threads take the tile's record pairs t, t + 256, ..., each keeping its own streaming
+// (m, s) per row with the same lazy rescale (one pair per check), and the CTA merges the 256
+// states per row with max / rescaled-sum butterflies and a fixed-order sum over warps.
+template <int D, int R, bool HZ>
+__global__ void __launch_bounds__(kThreads, 2) lse_smm_kernel(const LseParams p) {
+    using Cfg = LseCfg<D, HZ>;
+    constexpr int RS = Cfg::RS;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int64_t ngroups = (p.M + R - 1) / R;
+    const int sp = (int)(blockIdx.x / ngroups);                    // split-major (L2 sharing)
+    const int64_t row0 = (int64_t)(blockIdx.x % ngroups) * R;
+    const int64_t q0 = (int64_t)sp * p.pairs_per_split;
+    const int64_t npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * RS, nt, kConsumerWarps, (uint32_t)last_np * RS * 4u);
+
+    const int ct = threadIdx.x;
+    const float negc = p.negc;
+    const float2 negc2 = dup2(negc);
+    float xr[R][D];
+    float m[R];
+    double s64[R];
+    float2 s32[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r;
+        const bool ok = i < p.M;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xr[r][d] = ok ? __ldg(p.x + i * D + d) : 0.0f;
+        m[r] = kLseSentinel;
+        s64[r] = 0.0;
+        s32[r] = make_float2(0.f, 0.f);
+    }
+    for (int k = 0; k < nt; ++k) {
+        const float *tile = ring.acquire(k);
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
+        for (int pp = ct; pp < np; pp += kThreads) {
+            const float *rec = tile + pp * RS;
+            float f[RS];
+#pragma unroll
+            for (int u = 0; u < RS / 4; ++u) {
+                const float4 v = lds128(rec + 4 * u);
+                f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+            }
+            float2 ny[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
+            float2 hhi = make_float2(0.f, 0.f), hlo = make_float2(0.f, 0.f);
+            if constexpr (!HZ) {
+                hhi = make_float2(f[2 * D], f[2 * D + 1]);
+                hlo = make_float2(f[2 * D + 2], f[2 * D + 3]);
+            }
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float2 dd = add2(dup2(xr[r][0]), ny[0]);
+                float2 q2 = mul2(dd, dd);
+#pragma unroll
+                for (int d = 1; d < D; ++d) {
+                    dd = add2(dup2(xr[r][d]), ny[d]);
+                    q2 = fma2(dd, dd, q2);
+                }
+                const float2 hm = HZ ? dup2(-m[r]) : add2(add2(hhi, dup2(-m[r])), hlo);
+                const float2 t = fma2(q2, negc2, hm);
+                const float2 cs = make_float2(ex2(t.x), ex2(t.y));
+                if (!(fmaxf(cs.x, cs.y) <= kSumMax)) {
+                    const LseRescale rs = lse_rescale<D, HZ, RS, 1>(rec, xr[r], negc, m[r], s64[r], s32[r]);
+                    m[r] = rs.m;
+                    s64[r] = rs.s64;
+                    s32[r] = make_float2(rs.c1, 0.f);
+                } else {
+                    s32[r] = add2(s32[r], cs);
+                }
+            }
+        }
+        ring.release(k);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            s64[r] += (double)s32[r].x + (double)s32[r].y;
+            s32[r] = make_float2(0.f, 0.f);
+        }
+    }
+    // CTA merge of the per-thread (m, s) states of each row (deterministic butterflies)
+    __shared__ double red[kConsumerWarps][R];
+    __shared__ double mrow[R];
+    const int lane = ct & 31, warp = ct >> 5;
+    double mt[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        mt[r] = s64[r] > 0.0 ? (double)m[r] : -INFINITY;
+        double v = mt[r];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+        if (lane == 0) red[warp][r] = v;
+    }
+    __syncthreads();
+    if (ct < R) {
+        double v = red[0][ct];
+        for (int w = 1; w < kConsumerWarps; ++w) v = fmax(v, red[w][ct]);
+        mrow[ct] = v;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        double c = (s64[r] > 0.0 && mrow[r] > -INFINITY) ? s64[r] * exp2(mt[r] - mrow[r]) : 0.0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        if (lane == 0) red[warp][r] = c;
+    }
+    __syncthreads();
+    if (ct >= R) return;
+    const int64_t i = row0 + ct;
+    if (i >= p.M) return;
+    double stot = red[0][ct];
+    for (int w = 1; w < kConsumerWarps; ++w) stot += red[w][ct];
+    const double mm = stot > 0.0 ? mrow[ct] : (double)kLseSentinel;
+    if (p.split > 1) {
+        p.state[((int64_t)sp * p.M + i) * 2 + 0] = mm;
+        p.state[((int64_t)sp * p.M + i) * 2 + 1] = stot;
+        return;
+    }
+    const double a = (stot > 0.0) ? 0.69314718055994530942 * (mm + log2(stot)) : -INFINITY;
+    if (p.out) {
+        if (p.out_f64) ((double *)p.out)[i] = a;
+        else ((float *)p.out)[i] = (float)a;
+    }
+    if (p.state) {
+        p.state[2 * i + 0] = mm;
+        p.state[2 * i + 1] = stot;
+    }
+}
+
+template <int D, bool HZ>
+static cudaError_t run_lse_smm(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    using Cfg = LseCfg<D, HZ>;
+    constexpr int R = D <= 4 ? 8 : 4;
+    auto kern = lse_smm_kernel<D, R, HZ>;
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+        attr_done = true;
+    }
+    LseParams p;
+    p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.pairs_per_split = a.pairs_per_split;
+    p.npv = a.npv; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
+    p.units = nullptr;
+    const int64_t grid = (a.M + R - 1) / R * a.split;
+    *ctas = (int)grid;
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
+int lse_smm_rows(int D) { return D <= 4 ? 8 : 4; }
+
+cudaError_t launch_lse_smm(const LseLaunch &a, cudaStream_t st, int *ctas) {
+#define GENRED_SMM(DD) if (a.D == DD) return a.h_zero ? run_lse_smm<DD, true>(a, st, ctas) : run_lse_smm<DD, false>(a, st, ctas);
+    GENRED_SMM(1) GENRED_SMM(2) GENRED_SMM(3) GENRED_SMM(4)
+    GENRED_SMM(5) GENRED_SMM(6) GENRED_SMM(7) GENRED_SMM(8)
+#undef GENRED_SMM
+    return cudaErrorInvalidValue;
 }
 
 template <int D, int R, bool HZ>

@@ -505,6 +505,29 @@ def test_small_m_mode(G, formula, M, N, D):
         assert_sum_parity(host(res[1] if isinstance(res, tuple) else res), og, deng, what=f"smm grad M={M}")
 
 
+@pytest.mark.parametrize("M,N,D,hkind", [(1, 300_000, 3, "zero"), (7, 120_001, 2, "random"),
+                                         (64, 200_000, 5, "random"), (33, 90_000, 3, "far")])
+def test_lse_small_m_mode(G, M, N, D, hkind):
+    """LSE small-M mode: per-thread streaming (m, s) states merged per row by max / rescaled-sum
+    butterflies; against the oracle (1e-6 absolute) and bitwise run to run."""
+    rng = np.random.default_rng(M + N)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    h = None
+    if hkind == "random":
+        h = (rng.standard_normal(N) * 3).astype(np.float32)
+    elif hkind == "far":                       # one far term dominates some rows: rescale path
+        h = np.zeros(N, np.float32); h[::997] = 40.0
+    a1 = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=0.05,
+                out_dtype="float64")
+    plan = G.last_plan()
+    assert plan["rows_per_cta"] <= 8 and plan["split_j"] > 1, plan
+    a2 = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=0.05,
+                out_dtype="float64")
+    np.testing.assert_array_equal(host(a1), host(a2))
+    o, _ = oracle.lse(x, y, h, eps=0.05)
+    assert_lse_parity(host(a1), o, what=f"lse smm M={M}")
+
+
 @pytest.mark.parametrize("D", [1, 2, 4, 5])
 def test_gauss_sum_tiny_n_dims_f64(G, D):
     """Edge kernel for D = 1, 2, 4 (D = 5: the generic kernel) with fp64 output and a partial
