@@ -150,12 +150,9 @@ static cudaError_t run_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
     using Cfg = ArgkCfg<D>;
     constexpr int R = argk_rows<KMAX>();
     auto kern = argk_kernel<D, KMAX, R>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     ArgkParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.K = a.K; p.split = a.split;

@@ -111,11 +111,9 @@ cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int
                         double hscale, int64_t npairs, float *J, cudaStream_t st, const uint32_t *geo) {
     const int RS = pack_record_stride(kind, D, E);
     const int smem = pack_smem_bytes(kind, D, E, RS, b != nullptr);
-    static int attr_set = 0;
-    if (smem > 48 * 1024 && smem > attr_set) {
-        cudaError_t e = cudaFuncSetAttribute(pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (smem > 48 * 1024) {                       // every kind / D / E fits in 96 KB
+        const cudaError_t e = smem_opt_in((const void *)pack_kernel, 96 * 1024);
         if (e != cudaSuccess) return e;
-        attr_set = smem;
     }
     int64_t blocks = (npairs + 255) / 256;
     if (blocks > 148 * 8) blocks = 148 * 8;

@@ -125,11 +125,9 @@ static cudaError_t run(const float *x, const float *J, int npairs, int RS, int64
                        double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas) {
     auto kern = sum_edge_kernel<D>;
     const int smem = kStages * kRowsPerTile * D * 4 + (kMaxPairs * 12 + 4) * 4 + kStages * 8 + 64;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, smem);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     int occ = 1;
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, kThreads, smem);

@@ -496,11 +496,9 @@ static cudaError_t gtc_run(const GaussTcLaunch &a, cudaStream_t st, int *ctas, i
     p.out = a.out; p.out_f64 = a.out_f64; p.part = a.part;
     p.dbg = getenv("GENRED_TC_DBG") ? atoi(getenv("GENRED_TC_DBG")) : 0;
     auto kern = gtc::gauss_tc_kernel<D>;
-    static bool attr = false;
-    if (!attr) {
-        if ((e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, gtc::SMEM_BYTES)) != cudaSuccess)
-            return e;
-        attr = true;
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, gtc::SMEM_BYTES);
+        if (e != cudaSuccess) return e;
     }
     const int grid = std::min(p.n_units, a.num_sms);
     if (a.ev_start) cudaEventRecord(a.ev_start, st);

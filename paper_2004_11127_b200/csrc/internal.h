@@ -4,7 +4,26 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace genred {
+
+// Opt a kernel in to `bytes` of dynamic shared memory on the current device, once per (kernel,
+// device): the attribute is per device, so a process driving several GPUs needs it on each.
+inline cudaError_t smem_opt_in(const void *kernel, int bytes) {
+    static std::mutex mu;
+    static std::set<std::pair<const void *, int>> done;
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    std::lock_guard<std::mutex> lock(mu);
+    if (done.count({kernel, dev})) return cudaSuccess;
+    e = cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+    if (e == cudaSuccess) done.insert({kernel, dev});
+    return e;
+}
 
 constexpr int kTileJ = 512;                 // j-records per shared-memory stage
 constexpr int kStages = 4;                  // depth of the bulk-copy ring

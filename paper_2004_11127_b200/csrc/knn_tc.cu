@@ -739,11 +739,9 @@ size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K) {
 template <int KP, int CL>
 static cudaError_t launch_main(const CUtensorMap *maps, const tc::Params &p, int grid, cudaStream_t st) {
     auto kern = tc::knn_tc_kernel<KP, CL>;
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, tc::SMEM_BYTES);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, tc::SMEM_BYTES);
         if (e != cudaSuccess) return e;
-        attr = true;
     }
     if (CL == 1) {                                        // plain launch (no cluster scheduling)
         kern<<<grid, tc::NUM_THREADS, tc::SMEM_BYTES, st>>>(maps[0], maps[1], maps[2], maps[3], p);

@@ -376,11 +376,9 @@ static cudaError_t run_lse_smm(const LseLaunch &a, cudaStream_t st, int *ctas) {
     using Cfg = LseCfg<D, HZ>;
     constexpr int R = D <= 4 ? 8 : 4;
     auto kern = lse_smm_kernel<D, R, HZ>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     LseParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.pairs_per_split = a.pairs_per_split;
@@ -407,12 +405,9 @@ template <int D, int R, bool HZ>
 static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
     using Cfg = LseCfg<D, HZ>;
     auto kern = lse_kernel<D, R, HZ>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     LseParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.pairs_per_split = a.pairs_per_split;

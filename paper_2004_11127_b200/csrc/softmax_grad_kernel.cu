@@ -147,11 +147,9 @@ template <int D, int R>
 static cudaError_t run_sm(const SmLaunch &a, cudaStream_t st, int *ctas) {
     using Cfg = SmCfg<D>;
     auto kern = softmax_grad_kernel<D, R>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     SmParams p;
     p.x = a.x; p.J = a.J; p.coef = a.coef; p.alpha = a.alpha; p.M = a.M; p.split = a.split;

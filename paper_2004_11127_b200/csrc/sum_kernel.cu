@@ -28,12 +28,9 @@ template <int MODE, int D, int E, int R>
 static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     using Cfg = SumCfg<MODE, D, E>;
     auto kern = sum_kernel<MODE, D, E, R>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     SumParams p;
     p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;

@@ -20,11 +20,9 @@ static cudaError_t run_smm(const SumLaunch &a, cudaStream_t st, int *ctas) {
     constexpr int R = smm_rows<MODE>();
     using Cfg = SumCfg<MODE, D, 1>;
     auto kern = sum_kernel<MODE, D, 1, R, true>;
-    static bool attr_done = false;
-    if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
         if (e != cudaSuccess) return e;
-        attr_done = true;
     }
     SumParams p;
     p.x = a.x; p.J = a.J; p.g = a.g; p.M = a.M; p.split = a.split;
