@@ -88,6 +88,7 @@ def main():
     # 4. kernel CG solve
     N = 100_000
     p = dev(synth.uniform3(N, 11)); rhs = dev(synth.signal(N, 12, signed=True)[:, 0])
+    solvers.gauss_cg(p, rhs, 0.05, 0.1, tol=1e-6, max_iter=3)                 # warm-up (plan, scratch)
     torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record()
@@ -110,6 +111,7 @@ def main():
     # 5. k-means
     N, k = 1_000_000, 1000
     xk = dev(synth.gmm3(N, 13))
+    solvers.kmeans(xk, k, iters=1)                                             # warm-up (plan, scratch)
     torch.cuda.synchronize()
     e0.record()
     labels, c, hist = solvers.kmeans(xk, k, iters=10)
