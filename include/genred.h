@@ -122,12 +122,13 @@ typedef struct {
     const double *col_shift; /* LSE_GRAD: beta (N values) */
     /* Block-sparse ranges ("cluster-wise block-sparsity patterns"; KeOps'
      * ranges_i / slices_i / redranges_j convention).  HOST int64 arrays, used when n_ranges > 0
-     * (Sum reductions of GAUSS, GAUSS_GRADX, GAUSS_SUM_GRADX, SQDIST, and (SQDIST, LSE)):
+     * (Sum reductions of GAUSS, GAUSS_GRADX, GAUSS_SUM_GRADX, SQDIST; (SQDIST, LSE); and
+     * (SQDIST, ARGKMIN) with D <= 16, whose indices are the original j):
      *   ranges_i[2c], ranges_i[2c+1]   rows [is, ie) of cluster c; clusters sorted, disjoint
      *   slices[c]                     end of cluster c's intervals in ranges_j (cumulative)
      *   ranges_j[2k], ranges_j[2k+1]  j-interval [js, je); a cluster's intervals sorted, disjoint
      * a_i reduces over the union of its cluster's j-intervals; rows outside every cluster get the
-     * neutral value (0, or -inf for LSE).  split_j is ignored. */
+     * neutral value (0, -inf for LSE, (+inf, -1) for ArgKMin).  split_j is ignored. */
     int64_t n_ranges;
     const int64_t *ranges_i;
     const int64_t *slices;

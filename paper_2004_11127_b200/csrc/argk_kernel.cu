@@ -17,7 +17,9 @@ namespace genred {
 
 template <int D>
 struct ArgkCfg {
-    static constexpr int RS = ((2 * D) + 3) / 4 * 4;
+    // record pair: (-y_d) pairs, then the pair's two j (int32 bits; -1 = padding), so that the
+    // same kernel serves range-packed J (block-sparse ranges), whose positions are not j
+    static constexpr int RS = ((2 * (D + 1)) + 3) / 4 * 4;
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
     static constexpr int STAGE_BYTES = TILE_FLOATS * 4;
@@ -35,6 +37,7 @@ struct ArgkParams {
     int64_t j_offset;
     float *pdist;
     int32_t *pidx;
+    const RangeUnit *units;            // block-sparse ranges: one CTA per unit, direct output
 };
 
 template <int KMAX>
@@ -64,10 +67,20 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
 
-    const int64_t itile = blockIdx.x / p.split;
-    const int sp = (int)(blockIdx.x % p.split);
-    const int64_t q0 = (int64_t)sp * p.pairs_per_split;                   // record pairs [q0, q0 + npc)
-    const int64_t npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    int64_t row0, row_end, q0, npc;                                       // record pairs [q0, q0 + npc)
+    int sp;
+    if (p.units) {
+        const RangeUnit u = p.units[blockIdx.x];
+        row0 = u.row0; row_end = u.row_end; sp = 0;
+        q0 = u.tile0 * Cfg::PAIRS; npc = u.ntiles * Cfg::PAIRS;
+    } else {
+        const int64_t itile = blockIdx.x / p.split;
+        sp = (int)(blockIdx.x % p.split);
+        q0 = (int64_t)sp * p.pairs_per_split;
+        npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+        row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+        row_end = p.M;
+    }
     const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
     const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
 
@@ -76,7 +89,6 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 
     const int ct = threadIdx.x;
     const int K = p.K;
-    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
     float xr[R][D];
     float dist[R][KMAX];
     int32_t idx[R][KMAX];
@@ -84,7 +96,7 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        const bool ok = i < p.M;
+        const bool ok = i < row_end;
 #pragma unroll
         for (int d = 0; d < D; ++d) xr[r][d] = ok ? __ldg(p.x + i * D + d) : 0.0f;
 #pragma unroll
@@ -94,7 +106,6 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
-        const int32_t jbase = (int32_t)(2 * (q0 + (int64_t)k * Cfg::PAIRS));
         const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
 #pragma unroll 2
         for (int pp = 0; pp < np; ++pp) {
@@ -114,9 +125,9 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
                     q = fma2(dd, dd, q);
                 }
                 if (fminf(q.x, q.y) < kth[r]) {
-                    const int32_t j0 = jbase + 2 * pp;
-                    if (q.x < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.x, j0, kth[r]);
-                    if (q.y < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.y, j0 + 1, kth[r]);
+                    const int32_t jx = __float_as_int(f[2 * D]), jy = __float_as_int(f[2 * D + 1]);
+                    if (q.x < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.x, jx, kth[r]);
+                    if (q.y < kth[r]) topk_insert<KMAX>(dist[r], idx[r], K, q.y, jy, kth[r]);
                 }
             }
         }
@@ -126,7 +137,7 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
-        if (i >= p.M) continue;
+        if (i >= row_end) continue;
 #pragma unroll
         for (int k = 0; k < KMAX; ++k) {
             if (k >= K) break;
@@ -157,9 +168,10 @@ static cudaError_t run_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
     ArgkParams p;
     p.x = a.x; p.J = a.J; p.M = a.M; p.K = a.K; p.split = a.split;
     p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.dist = a.dist; p.idx = a.idx;
-    p.j_offset = a.j_offset; p.pdist = a.pdist; p.pidx = a.pidx;
+    p.j_offset = a.j_offset; p.pdist = a.pdist; p.pidx = a.pidx; p.units = a.units;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
-    const int64_t grid = ((a.M + rows - 1) / rows) * a.split;
+    const int64_t grid = a.units ? a.n_units : ((a.M + rows - 1) / rows) * a.split;
+    if (grid == 0) { *ctas = 0; return cudaSuccess; }
     *ctas = (int)grid;
     kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
     return cudaGetLastError();

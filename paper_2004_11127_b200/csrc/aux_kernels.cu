@@ -72,7 +72,9 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                 // Sum kinds: -s y (padding 0, b = 0); LSE / ArgKMin: -y (padding at +inf distance)
                 rec[2 * d + h] = sumk ? (valid ? -(s * v) : 0.0f) : (valid ? -v : NEG_INF);
             }
-            if (sumk) {
+            if (kind == PACK_ARGKMIN) {            // the j of each half, as int32 bits (-1: padding)
+                rec[2 * D + h] = __int_as_float(valid ? (int)(j0 + jj) : -1);
+            } else if (sumk) {
                 for (int e = 0; e < E; ++e)
                     rec[2 * D + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
             } else if (kind == PACK_LSE_H) {
@@ -102,7 +104,8 @@ static int pack_smem_bytes(int kind, int D, int E, int RS, bool has_b) {
 
 int pack_record_stride(int kind, int D, int E) {
     if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) return record_stride(D + 1, E);
-    if (kind == PACK_ARGKMIN || kind == PACK_LSE_HZ) return record_stride(D, 0);
+    if (kind == PACK_ARGKMIN) return record_stride(D + 1, 0);      // + the j pair
+    if (kind == PACK_LSE_HZ) return record_stride(D, 0);
     if (kind == PACK_LSE_H) return record_stride(D, 2);
     return record_stride(D, E);
 }
@@ -132,7 +135,7 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                                    const uint32_t *geo_enc) {
     const Geo geo = kind == PACK_GAUSS_AUTO ? geo_decode(geo_enc, D, s) : Geo{};
     const int boff = kind == PACK_GAUSS_AUTO ? 2 * (D + 1) : 2 * D;
-    const bool lse = kind == PACK_LSE_HZ || kind == PACK_LSE_H;
+    const bool lse = kind == PACK_LSE_HZ || kind == PACK_LSE_H || kind == PACK_ARGKMIN;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
          p += (int64_t)gridDim.x * blockDim.x) {
         int lo = 0, hi = ncopies - 1;                          // last copy with dst <= p
@@ -143,10 +146,12 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
         const RangeCopy c = copies[lo];
         float *rec = J + p * RS;
         if (lse) {          // LSE records: (-y) pairs [+ h' hi/lo pairs]; invalid: y = +inf, h = -inf
+                            // ArgKMin records: (-y) pairs + the original j pair (int32 bits, -1 invalid)
             for (int h = 0; h < 2; ++h) {
                 const int64_t j = c.js + 2 * (p - c.dst) + h;
                 const bool valid = j < c.je && j < N;
                 for (int d = 0; d < D; ++d) rec[2 * d + h] = valid ? -y[j * D + d] : -INFINITY;
+                if (kind == PACK_ARGKMIN) rec[2 * D + h] = __int_as_float(valid ? (int)j : -1);
                 if (kind == PACK_LSE_H) {
                     const double hv = valid ? 1.4426950408889634074 * (double)b[j] : 0.0;
                     const float hi = valid ? (float)hv : -INFINITY;
@@ -154,7 +159,7 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                     rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
                 }
             }
-            for (int k = 2 * D + (kind == PACK_LSE_H ? 4 : 0); k < RS; ++k) rec[k] = 0.0f;
+            for (int k = 2 * D + (kind == PACK_LSE_H ? 4 : kind == PACK_ARGKMIN ? 2 : 0); k < RS; ++k) rec[k] = 0.0f;
             continue;
         }
         for (int h = 0; h < 2; ++h) {

@@ -101,7 +101,9 @@ genred_status validate(const genred_args *a, std::string &msg) {
     }
     if (a->n_ranges < 0) { msg = "n_ranges must be >= 0"; return GENRED_E_SHAPE; }
     if (a->n_ranges > 0) {
-        if (!(sum_pair || lse_pair)) { msg = "block-sparse ranges are supported for Sum and LSE"; return GENRED_E_UNSUPPORTED; }
+        if (!(sum_pair || lse_pair || (argk_pair && a->D <= 16))) {
+            msg = "block-sparse ranges are supported for Sum, LSE and ArgKMin with D <= 16"; return GENRED_E_UNSUPPORTED;
+        }
         if (!a->ranges_i || !a->slices || !a->ranges_j) { msg = "ranges_i / slices / ranges_j is NULL"; return GENRED_E_INVALID; }
         int64_t prev_ie = 0, prev_slice = 0;
         for (int64_t c = 0; c < a->n_ranges; ++c) {
@@ -312,7 +314,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         for (int64_t r = is; r < ie; r += RT) units.push_back({r, std::min(r + RT, ie), tile0, ntiles});
     }
     copies.push_back({cursor, 0, 0});
-    const int pk = mode == 4 ? (a->b ? PACK_LSE_H : PACK_LSE_HZ)
+    const int pk = mode == 5 ? PACK_ARGKMIN : mode == 4 ? (a->b ? PACK_LSE_H : PACK_LSE_HZ)
                  : mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
     const int RS = pack_record_stride(pk, D, E);
     const size_t jbytes = al256((size_t)std::max<int64_t>(cursor, 1) * RS * 4);
@@ -331,14 +333,15 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         e = cudaMemcpyAsync(dunits, units.data(), units.size() * sizeof(RangeUnit), cudaMemcpyHostToDevice, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "range table copy");
     // neutral outputs for every row first; cluster rows are overwritten by the kernel
-    const int fill_kind = mode == 4 ? 2 : (mode == 2 ? 1 : 0);
+    const int fill_kind = mode == 5 ? 3 : mode == 4 ? 2 : (mode == 2 ? 1 : 0);
     const int fill_C = mode == 1 ? D : E;
-    e = launch_fill(fill_kind, M, fill_C, D, a->out, out_f64, a->out_grad, nullptr, a->lse_state, st);
+    e = launch_fill(fill_kind, M, fill_C, mode == 5 ? a->K : D, a->out, out_f64, a->out_grad, a->out_idx,
+                    a->lse_state, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "fill kernel");
     int kernels = 1;
     float sc = 1.0f;
     double scale_grad = 0.0;
-    if (mode != 3 && mode != 4) {
+    if (mode != 3 && mode != 4 && mode != 5) {
         sc = (float)(sqrt(kLog2e) / a->scale);
         scale_grad = -2.0 / (a->scale * a->scale * (double)sc);
         e = launch_bbox(a->x, M, a->y, N, D, geo, st);
@@ -348,6 +351,27 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     e = launch_pack_ranges(pk, a->y, a->b, N, D, E, sc, dcopies, (int)copies.size(), cursor, J, st, geo);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "range pack kernel");
     kernels++;
+    if (mode == 5) {                                  // ArgKMin: units write their rows' lists directly
+        ArgkLaunch L;
+        L.D = D; L.K = a->K; L.R = R; L.x = a->x; L.J = J; L.M = M; L.split = 1;
+        L.pairs_per_split = 0; L.npv = 0;
+        L.dist = (float *)a->out; L.idx = a->out_idx; L.j_offset = a->j_offset;
+        L.pdist = nullptr; L.pidx = nullptr;
+        L.units = dunits; L.n_units = (int64_t)units.size();
+        int ctas = 0;
+        if (!units.empty()) {
+            prof_event(ctx, true, st);
+            e = launch_argk(L, st, &ctas);
+            prof_event(ctx, false, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "argkmin kernel (ranges)");
+            kernels++;
+        }
+        ctx->launches += kernels;
+        ctx->plan.split_j = 1; ctx->plan.rows_per_cta = (int32_t)RT; ctx->plan.ctas = ctas;
+        ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
+        return GENRED_OK;
+    }
     if (mode == 4) {
         LseLaunch L;
         L.D = D; L.R = R; L.x = a->x; L.J = J; L.M = M; L.split = 1; L.pairs_per_split = 0;
@@ -642,6 +666,9 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         return GENRED_OK;
     }
+
+    // ArgKMin with block-sparse ranges (small D; validated)
+    if (a->n_ranges > 0) return eval_ranges(ctx, a, st, 5, argk_rows_per_thread(a->K));
 
     // ArgKMin, large D: tcgen05 3xTF32 screening + exact re-rank (knn_tc.cu)
     if (D > 16) {

@@ -133,6 +133,8 @@ struct ArgkLaunch {
     int64_t pairs_per_split, npv;                  // record-pair j-splits (multiple of kSplitGrain)
     float *dist; int64_t *idx; int64_t j_offset;   // split == 1 outputs
     float *pdist; int32_t *pidx;                   // split > 1: split x M x K partials
+    const RangeUnit *units = nullptr;              // block-sparse ranges (device), or nullptr
+    int64_t n_units = 0;
 };
 cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas);
 int argk_occupancy(int D, int K, int R);

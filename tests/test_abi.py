@@ -121,6 +121,8 @@ def test_ranges_validation(lib):
     rj2 = np.array([[5, 9], [3, 7]], np.int64); sl2 = np.array([2, 2], np.int64)   # unsorted in cluster
     assert G.validate(args(ri, sl2, np.array([[5, 9], [3, 7]], np.int64)))[0] == G.E_SHAPE
     a = args(ri, sl, rj, formula=2, reduction=2, K=3, out_idx=24576)   # ArgKMin with ranges
+    assert G.validate(a)[0] == G.OK
+    a = args(ri, sl, rj, formula=2, reduction=2, K=3, out_idx=24576, D=17)   # tensor path: no ranges
     assert G.validate(a)[0] == G.E_UNSUPPORTED
     a = args(ri, sl, rj, formula=2, reduction=1)                    # LSE with ranges
     assert G.validate(a)[0] == G.OK

@@ -837,3 +837,27 @@ def test_block_sparse_ranges_lse(G, with_h):
     s = host(st)
     ok = ~np.isneginf(a)
     np.testing.assert_allclose(math.log(2) * (s[ok, 0] + np.log2(s[ok, 1])), a[ok], rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("K", [1, 5, 20])
+def test_block_sparse_ranges_argkmin(G, K):
+    """ArgKMin with block-sparse ranges: each cluster's rows search only its j-intervals; the
+    reported indices are the original j (records carry them), uncovered rows get (+inf, -1)."""
+    x, bx, cx = _clustered(18, 120, 171)
+    y, by, cy = _clustered(22, 140, 172)
+    ri, sl, rj = _ranges(bx, cx, by, cy, 0.35)
+    rj = rj[sl[0]:]; sl = sl[1:] - sl[0]; ri = ri[1:]            # first cluster uncovered
+    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, j_offset=1000, ranges=(ri, sl, rj))
+    d, j = host(d), host(j)
+    assert np.all(np.isinf(d[:bx[1]])) and np.all(j[:bx[1]] == -1)
+    prev = 0
+    for c in range(len(ri)):
+        rows = np.arange(ri[c, 0], ri[c, 1])
+        idx = np.concatenate([np.arange(js, je) for js, je in rj[prev:sl[c]]]) if sl[c] > prev else np.zeros(0, int)
+        prev = sl[c]
+        if len(idx) == 0:
+            assert np.all(j[rows] == -1); continue
+        od, oj = oracle.argkmin(x[rows], y[idx], K + 1)
+        oj_glob = np.where(oj >= 0, idx[np.maximum(oj, 0)], -1)         # back to original j
+        jj = np.where(j[rows] >= 0, j[rows] - 1000, -1)
+        argk_check(d[rows], jj, od, oj_glob, K, what=f"argk ranges c={c}")
