@@ -25,7 +25,8 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
     extern __shared__ float4 pack_smem4[];
     float *sm = reinterpret_cast<float *>(pack_smem4);
     const float NEG_INF = -INFINITY;
-    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT;
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
+    const bool raw = kind == PACK_GAUSS_AUTO_RAW;           // direct records: -y instead of -s y
     const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
     const int EB = (gauss || sumk) ? (b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);   // staged b / h columns
     float *ys = sm;                           // [512][D]
@@ -58,7 +59,7 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                         r = valid ? s * (v - geo.c[d]) : 0.0f;        // y' = s (y - c)
                         w += (double)r * (double)r;
                     } else {
-                        r = valid ? -(s * v) : 0.0f;
+                        r = valid ? (raw ? -v : -(s * v)) : 0.0f;
                     }
                     rec[2 * d + h] = r;
                 }
@@ -96,14 +97,15 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
 }
 
 static int pack_smem_bytes(int kind, int D, int E, int RS, bool has_b) {
-    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT;
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
     const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
     const int EB = (gauss || sumk) ? (has_b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);
     return (kTileJ * (D + EB) + 256 * RS) * 4;
 }
 
 int pack_record_stride(int kind, int D, int E) {
-    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) return record_stride(D + 1, E);
+    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW)
+        return record_stride(D + 1, E);
     if (kind == PACK_ARGKMIN) return record_stride(D + 1, 0);      // + the j pair
     if (kind == PACK_LSE_HZ) return record_stride(D, 0);
     if (kind == PACK_LSE_H) return record_stride(D, 2);
@@ -133,8 +135,9 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                                    int64_t N, int D, int E, float s, const RangeCopy *__restrict__ copies,
                                    int ncopies, int64_t npairs, int RS, float *__restrict__ J,
                                    const uint32_t *geo_enc) {
-    const Geo geo = kind == PACK_GAUSS_AUTO ? geo_decode(geo_enc, D, s) : Geo{};
-    const int boff = kind == PACK_GAUSS_AUTO ? 2 * (D + 1) : 2 * D;
+    const bool gauto = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_AUTO_RAW;
+    const Geo geo = gauto ? geo_decode(geo_enc, D, s) : Geo{};
+    const int boff = gauto ? 2 * (D + 1) : 2 * D;
     const bool lse = kind == PACK_LSE_HZ || kind == PACK_LSE_H || kind == PACK_ARGKMIN;
     for (int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; p < npairs;
          p += (int64_t)gridDim.x * blockDim.x) {
@@ -169,15 +172,15 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
             for (int d = 0; d < D; ++d) {
                 const float v = valid ? y[j * D + d] : 0.0f;
                 float r;
-                if (kind == PACK_GAUSS_AUTO && geo.expanded) {
+                if (gauto && geo.expanded) {
                     r = valid ? s * (v - geo.c[d]) : 0.0f;
                     w += (double)r * (double)r;
                 } else {
-                    r = valid ? -(s * v) : 0.0f;
+                    r = valid ? (kind == PACK_GAUSS_AUTO_RAW ? -v : -(s * v)) : 0.0f;
                 }
                 rec[2 * d + h] = r;
             }
-            if (kind == PACK_GAUSS_AUTO) rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;
+            if (gauto) rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;
             for (int e = 0; e < E; ++e)
                 rec[boff + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
         }

@@ -315,7 +315,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     }
     copies.push_back({cursor, 0, 0});
     const int pk = mode == 5 ? PACK_ARGKMIN : mode == 4 ? (a->b ? PACK_LSE_H : PACK_LSE_HZ)
-                 : mode == 3 ? PACK_SQDIST_SUM : PACK_GAUSS_AUTO;
+                 : mode == 3 ? PACK_SQDIST_SUM : (mode == 1 || mode == 2) ? PACK_GAUSS_AUTO_RAW : PACK_GAUSS_AUTO;
     const int RS = pack_record_stride(pk, D, E);
     const size_t jbytes = al256((size_t)std::max<int64_t>(cursor, 1) * RS * 4);
     const size_t cbytes = al256(copies.size() * sizeof(RangeCopy));
@@ -521,7 +521,8 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
             pl.R = Rs;
         }
-        const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT : PACK_GAUSS_AUTO;
+        const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT
+                     : (mode == 1 || mode == 2) ? PACK_GAUSS_AUTO_RAW : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;

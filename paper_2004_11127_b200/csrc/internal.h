@@ -38,7 +38,7 @@ constexpr int kSplitGrain = 16;
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
 
 enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4,
-                PACK_GAUSS_AUTO = 5, PACK_GAUSS_DIRECT = 6 };
+                PACK_GAUSS_AUTO = 5, PACK_GAUSS_DIRECT = 6, PACK_GAUSS_AUTO_RAW = 7 };
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
 // kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
@@ -48,6 +48,8 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 // which contribute nothing.
 // PACK_GAUSS_AUTO (Gaussian Sum): decodes the bounding box `geo` (geo.cuh) and writes either the
 // expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-s y, 0, b).
+// PACK_GAUSS_AUTO_RAW (gradient modes): as PACK_GAUSS_AUTO, but the direct records hold -y (raw),
+// so the kernel forms raw differences x - y (reading R18d).
 // PACK_GAUSS_DIRECT: the direct records when the box rules the expanded form out, else nothing
 // (the tensor-core kernel, gauss_tc.cu, takes the expanded case).
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,

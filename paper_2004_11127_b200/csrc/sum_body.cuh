@@ -78,6 +78,8 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
     constexpr bool POLY = kPolyShare && XP && R == 4;
     constexpr int HH = SMM ? 1 : (MODE == 1 || MODE == 2) ? GENRED_GRAD_HH : 2;   // record pairs per iteration
+    constexpr bool RAWD = !XP && (MODE == 1 || MODE == 2);   // direct gradient: raw differences
+    const float2 negs2 = dup2(-(p.s * p.s));
     const int ct = threadIdx.x;
     float xr[R][D];
     float gr[R][E];
@@ -95,7 +97,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                 xsq[r] += (double)xs * (double)xs;
                 xr[r][d] = 2.0f * xs;                                      // exact doubling
             } else {
-                xr[r][d] = p.s * v;
+                // direct form: pre-scaled s x for the Sum; RAW x for the gradient modes, whose
+                // linear factor (x - y) must come from a raw fp32 difference (exact for nearby
+                // coordinates, Sterbenz) -- s x - s y loses it when x ~ y (R18d)
+                xr[r][d] = RAWD ? v : p.s * v;
             }
         }
 #pragma unroll
@@ -199,7 +204,13 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
                     for (int e = 0; e < E; ++e) acc[r][e] = fma2(q, bv[e], acc[r][e]);
                 } else {
-                    const float2 ex = make_float2(ex2(-q.x), ex2(-q.y));   // e^{-|x-y|^2/sigma^2}
+                    float2 ex;                                                 // e^{-|x-y|^2/sigma^2}
+                    if constexpr (RAWD) {
+                        const float2 t = mul2(q, negs2);                      // -s^2 |x - y|^2
+                        ex = make_float2(ex2(t.x), ex2(t.y));
+                    } else {
+                        ex = make_float2(ex2(-q.x), ex2(-q.y));
+                    }
                     if constexpr (MODE == 0) {
 #pragma unroll
                         for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
@@ -293,6 +304,10 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) acc64[r][c] *= fac;
+        }
+        if constexpr (RAWD) {                              // raw (x - y): back to the s-scaled convention
+#pragma unroll
+            for (int c = 0; c < NG; ++c) acc64[r][NS + c] *= (double)p.s;
         }
         if (p.split > 1) {
             double *dst = p.part + ((int64_t)sp * p.M + i) * C;

@@ -861,3 +861,54 @@ def test_block_sparse_ranges_argkmin(G, K):
         oj_glob = np.where(oj >= 0, idx[np.maximum(oj, 0)], -1)         # back to original j
         jj = np.where(j[rows] >= 0, j[rows] - 1000, -1)
         argk_check(d[rows], jj, od, oj_glob, K, what=f"argk ranges c={c}")
+
+
+def _random_case(rng):
+    red = rng.choice(["sum", "sum", "lse", "argkmin"])
+    formula = {"sum": rng.choice(["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"]),
+               "lse": "sqdist", "argkmin": "sqdist"}[red]
+    M = int(rng.choice([1, 2, 7, 63, 64, 65, 257, 1000, 2500]))
+    N = int(rng.choice([1, 3, 31, 64, 65, 511, 513, 4000, 20000, 70000]))
+    D = int(rng.integers(1, 9))
+    E = int(rng.integers(1, 5)) if (red == "sum" and formula != "sqdist" or formula == "sqdist" and red == "sum") else 1
+    return red, formula, M, N, D, E
+
+
+@pytest.mark.parametrize("seed", list(range(120)))
+def test_randomized_shapes_against_oracle(G, seed):
+    """Seeded random (reduction, formula, M, N, D, E, split, dtype) cases through every planner
+    branch (row tiles / small-M / tiny-N edge / record-pair splits / warp merges) vs the oracle."""
+    rng = np.random.default_rng(10_000 + seed)
+    red, formula, M, N, D, E = _random_case(rng)
+    split = int(rng.choice([0, 0, 0, 2, 5, 40]))
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    if red == "sum":
+        b = rng.standard_normal((N, E)).astype(np.float32)
+        g = rng.standard_normal((M, E)).astype(np.float32)
+        sigma = float(rng.choice([0.3, 0.7, 2.0])) if formula != "sqdist" else 1.0
+        args = (dev(x), dev(y), dev(b)) + ((dev(g),) if "grad" in formula else ())
+        res = G.eval(formula, "sum", *args, scale=sigma, split_j=split,
+                     out_dtype=str(rng.choice(["float32", "float64"])))
+        res = res if isinstance(res, tuple) else (res,)
+        if formula == "sqdist":
+            o, den = oracle.sqdist_sum(x, y, b)
+            assert_sum_parity(host(res[0]), o, den, what=f"seed {seed} sqdist")
+            return
+        if formula in ("gauss", "gauss_sum_gradx"):
+            o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+            assert_sum_parity(host(res[0]), o, den, what=f"seed {seed} sum")
+        if "grad" in formula:
+            og, deng = oracle.gauss_gradx(x, y, b, g, sigma=sigma)
+            assert_sum_parity(host(res[-1]), og, deng, what=f"seed {seed} grad")
+    elif red == "lse":
+        h = (rng.standard_normal(N) * 2).astype(np.float32) if rng.random() < 0.5 else None
+        eps = float(rng.choice([0.02, 0.1, 1.0]))
+        a = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=eps,
+                   split_j=split, out_dtype="float64")
+        o, _ = oracle.lse(x, y, h, eps=eps)
+        assert_lse_parity(host(a), o, rel=True, what=f"seed {seed} lse")
+    else:
+        K = int(rng.choice([1, 3, 10, 32]))
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)
+        od, oj = oracle.argkmin(x, y, K + 1)
+        argk_check(host(d), host(j), od, oj, K, what=f"seed {seed} argk")
