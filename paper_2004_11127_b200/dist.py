@@ -96,3 +96,14 @@ def jshard_eval(formula: str, reduction: str, x, y_local, b_local=None, g=None, 
             ds, js = [d], [j]
         return fns["merge_topk"](torch.stack(ds), torch.stack(js))
     raise ValueError(reduction)
+
+
+def dist_eval(formula: str, reduction: str, x, y, b=None, g=None, *, mode: str = "ishard", **kw):
+    """SURVEY.md 8(b)'s ``genred.dist_eval``: ``mode="ishard"`` -> ishard_eval (x: this rank's
+    rows, y/b broadcast from ``src``), ``mode="jshard"`` -> jshard_eval (y/b: this rank's j-slice,
+    partial results merged across ranks)."""
+    if mode == "ishard":
+        return ishard_eval(formula, reduction, x, y, b, g, **kw)
+    if mode == "jshard":
+        return jshard_eval(formula, reduction, x, y, b, g, **kw)
+    raise ValueError(f"mode must be 'ishard' or 'jshard', not {mode!r}")

@@ -69,7 +69,7 @@ def _worker(rank, world, port, q):
         import sys
         sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
         import synth
-        from paper_2004_11127_b200.dist import ishard_eval, jshard_eval, shard_range
+        from paper_2004_11127_b200.dist import dist_eval, ishard_eval, jshard_eval, shard_range
         fns = _cpu_fns()
         M, N = 37, 53
         x = torch.from_numpy(synth.uniform3(M, 1)); y = torch.from_numpy(synth.gmm3(N, 2))
@@ -82,7 +82,7 @@ def _worker(rank, world, port, q):
         # j-shard
         jlo, jhi = shard_range(N, world, rank)
         ys, bs = y[jlo:jhi].contiguous(), b[jlo:jhi].contiguous()
-        a_s = jshard_eval("gauss", "sum", x, ys, bs, scale=0.5, fns=fns, out_dtype="float64")
+        a_s = dist_eval("gauss", "sum", x, ys, bs, mode="jshard", scale=0.5, fns=fns, out_dtype="float64")
         a_l = jshard_eval("sqdist", "lse", x, ys, None, scale=0.05, fns=fns)
         d_k, j_k = jshard_eval("sqdist", "argkmin", x, ys, K=4, j_offset=jlo, fns=fns)
         q.put((rank, a_i.numpy(), a_s.numpy(), a_l.numpy(), d_k.numpy(), j_k.numpy()))
