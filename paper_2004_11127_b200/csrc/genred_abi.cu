@@ -393,6 +393,7 @@ genred_status eval_ranges(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         return GENRED_OK;
     }
     SumLaunch L;
+    L.num_sms = ctx->num_sms;
     L.mode = mode; L.D = D; L.E = E; L.R = R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
     L.split = 1; L.pairs_per_split = 0; L.npv = 0; L.s = sc;
     L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
@@ -589,6 +590,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             return GENRED_OK;
         }
         SumLaunch L;
+        L.num_sms = ctx->num_sms;
         L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = J; L.g = a->g; L.M = M;
         L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;

@@ -52,8 +52,9 @@ struct SumParams {
     int out_f64;
     float *out_grad;
     double *part;
-    const RangeUnit *units;   // block-sparse ranges: one CTA per unit (rows of one cluster)
+    const RangeUnit *units;   // block-sparse ranges: one unit per (cluster, row tile)
     int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
+    int64_t n_work;           // work units; the persistent grid walks w = blockIdx.x, + gridDim.x, ...
 };
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
@@ -274,7 +275,6 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
             }
         }
         __syncthreads();
-        if (ct != 0) return;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -288,11 +288,11 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         }
     }
 
-    // ---- epilogue --------------------------------------------------------------------------
+    // ---- epilogue (small-M mode: thread 0 for the CTA's rows) ---------------------------------
 #pragma unroll
     for (int r = 0; r < R; ++r) {
         const int64_t i = SMM ? row0 + r : row0 + r * (kConsumerWarps * 32) + ct;
-        if (i >= row_end) continue;
+        if (i >= row_end || (SMM && ct != 0)) continue;
         if constexpr (XP) {
             const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
             if constexpr (NG > 0) {
@@ -344,30 +344,34 @@ constexpr int sum_min_blocks() {
     return 2;
 }
 
+// The grid walks the work units w = blockIdx.x, blockIdx.x + gridDim.x, ...; a unit is (row
+// tile, j-split), (row group, j-split) in the small-M mode, or one block-sparse range unit.  The
+// launch uses one CTA per unit (measured faster than a persistent grid, see sum_kernel.cu).
 template <int MODE, int D, int E, int R, bool SMM = false>
 __global__ void __launch_bounds__(kThreads, sum_min_blocks<MODE, D, E, R, SMM>())
 sum_kernel(const SumParams p) {
     using Cfg = SumCfg<MODE, D, E>;
     extern __shared__ __align__(128) unsigned char smem_raw[];
-
-    // this CTA's j-range: record pairs [q0, q0 + npc), streamed in tiles of PAIRS
+    for (int64_t w = blockIdx.x; w < p.n_work; w += gridDim.x) {
+    if (w != blockIdx.x) __syncthreads();            // the previous unit is done with shared memory
+    // this unit's j-range: record pairs [q0, q0 + npc), streamed in tiles of PAIRS
     int64_t row0, row_end, q0, npc;
     int sp;
     if (p.units) {                                     // block-sparse: rows of one cluster
-        const RangeUnit u = p.units[blockIdx.x];
+        const RangeUnit u = p.units[w];
         row0 = u.row0; row_end = u.row_end; sp = 0;
         q0 = u.tile0 * Cfg::PAIRS; npc = u.ntiles * Cfg::PAIRS;
     } else if (SMM) {
         // split-major: concurrently running CTAs share a j-range (L2 reuse across row groups)
         const int64_t ngroups = (p.M + R - 1) / R;
-        sp = (int)(blockIdx.x / ngroups);
-        row0 = (int64_t)(blockIdx.x % ngroups) * R;
+        sp = (int)(w / ngroups);
+        row0 = (int64_t)(w % ngroups) * R;
         row_end = p.M;
         q0 = (int64_t)sp * p.pairs_per_split;
         npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
     } else {
-        const int64_t itile = blockIdx.x / p.split;
-        sp = (int)(blockIdx.x % p.split);
+        const int64_t itile = w / p.split;
+        sp = (int)(w % p.split);
         q0 = (int64_t)sp * p.pairs_per_split;
         npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);   // empty: zero partial
         row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
@@ -388,6 +392,7 @@ sum_kernel(const SumParams p) {
         ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
         Geo geo{};
         sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+    }
     }
 }
 

@@ -8,12 +8,27 @@
 // (sum_body.cuh, SMM = true).  j-splits (record-pair grains) then spread the work over the GPU;
 // their partials merge in sum_finalize like the row-tile kernels'.  Instantiated for E = 1 and
 // D <= 4 (the other shapes take the row-tile kernels).
+#include <stdlib.h>
+
+#include <algorithm>
+
 #include "sum_body.cuh"
 
 namespace genred {
 
 template <int MODE>
 constexpr int smm_rows() { return (MODE == 0 || MODE == 3) ? 8 : 2; }
+
+template <int MODE, int D>
+static int occ_smm() {
+    constexpr int R = smm_rows<MODE>();
+    using Cfg = SumCfg<MODE, D, 1>;
+    auto kern = sum_kernel<MODE, D, 1, R, true>;
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
+    int n = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess) return 1;
+    return n > 0 ? n : 1;
+}
 
 template <int MODE, int D>
 static cudaError_t run_smm(const SumLaunch &a, cudaStream_t st, int *ctas) {
@@ -30,23 +45,16 @@ static cudaError_t run_smm(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = nullptr;
     p.direct_only = a.direct_only;
-    const int64_t grid = (a.M + R - 1) / R * a.split;
-    if (grid == 0) { *ctas = 0; return cudaSuccess; }
+    p.n_work = (a.M + R - 1) / R * a.split;
+    if (p.n_work == 0) { *ctas = 0; return cudaSuccess; }
+    static const int occ = occ_smm<MODE, D>();                 // GENRED_PERSIST=1: persistent grid
+    static const int persist = getenv("GENRED_PERSIST") ? atoi(getenv("GENRED_PERSIST")) : 0;
+    const int64_t grid = persist ? std::min<int64_t>(p.n_work, (int64_t)a.num_sms * occ) : p.n_work;
     *ctas = (int)grid;
     kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
     return cudaGetLastError();
 }
 
-template <int MODE, int D>
-static int occ_smm() {
-    constexpr int R = smm_rows<MODE>();
-    using Cfg = SumCfg<MODE, D, 1>;
-    auto kern = sum_kernel<MODE, D, 1, R, true>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
-    int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess) return 1;
-    return n > 0 ? n : 1;
-}
 
 template <int MODE>
 static cudaError_t run_smm_d(const SumLaunch &a, cudaStream_t st, int *ctas) {
