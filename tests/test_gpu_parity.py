@@ -912,3 +912,18 @@ def test_randomized_shapes_against_oracle(G, seed):
         d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)
         od, oj = oracle.argkmin(x, y, K + 1)
         argk_check(host(d), host(j), od, oj, K, what=f"seed {seed} argk")
+
+
+def test_ranges_host_mode_matches_device(G):
+    """Block-sparse ranges through GENRED_MEM_HOST (numpy in, numpy out) equal the device call."""
+    x, bx, cx = _clustered(12, 100, 181)
+    y, by, cy = _clustered(15, 90, 182)
+    b = synth.signal(len(y), 183, signed=True)
+    ranges = _ranges(bx, cx, by, cy, 0.4)
+    ad = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.3, ranges=ranges))
+    ah = G.eval("gauss", "sum", x, y, b, scale=0.3, ranges=ranges)
+    np.testing.assert_array_equal(ad, ah)
+    dd, jd = G.eval("sqdist", "argkmin", dev(x), dev(y), K=4, ranges=ranges)
+    dh, jh = G.eval("sqdist", "argkmin", x, y, K=4, ranges=ranges)
+    np.testing.assert_array_equal(host(dd), dh)
+    np.testing.assert_array_equal(host(jd), jh)
