@@ -27,8 +27,8 @@ struct Geo {
     bool expanded;
 };
 
-// lohi[0..7] / [8..15] = encoded per-coordinate minima / maxima of y, [16..23] / [24..31] those
-// of x.  The centre comes from y alone, so every i-shard of the same problem (same y, different
+// lohi[0..7] / [8..15] = encoded per-coordinate minima / INVERTED maxima (~code, so that one
+// 0xff initialisation and atomicMin serve both) of y, [16..23] / [24..31] those of x.  The centre comes from y alone, so every i-shard of the same problem (same y, different
 // x rows) gets the same centre and, when its rows fit the same radius, bitwise the same
 // arithmetic as the single-GPU run; the radius test covers both clouds.
 // lohi == nullptr: no box was reduced (tiny N, see genred_abi.cu) -> the direct form.
@@ -46,8 +46,8 @@ __device__ __forceinline__ Geo geo_decode(const uint32_t *lohi, int D, float s) 
     for (int d = 0; d < 8; ++d) {
         g.c[d] = 0.0f;
         if (d < D) {
-            const float lo = ord2f(lohi[d]), hi = ord2f(lohi[8 + d]);
-            const float xlo = ord2f(lohi[16 + d]), xhi = ord2f(lohi[24 + d]);
+            const float lo = ord2f(lohi[d]), hi = ord2f(~lohi[8 + d]);       // maxima stored inverted
+            const float xlo = ord2f(lohi[16 + d]), xhi = ord2f(~lohi[24 + d]);
             ok = ok && isfinite(lo) && isfinite(hi) && isfinite(xlo) && isfinite(xhi);
             const float c = 0.5f * lo + 0.5f * hi;
             const float h = fmaxf(fmaxf(hi - c, c - lo), fmaxf(xhi - c, c - xlo)) * 1.0001f;
