@@ -445,7 +445,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
 
     if (f == GENRED_LSE_GRAD) {                                   // LSE backward (8(f) row 2)
         const int rmax = sm_rows_per_thread_max(D);
-        Plan pl = make_plan(ctx, a, 3, rmax, D, 0, 0);
+        Plan pl = make_plan(ctx, a, 3, rmax, D, 0, 0, true);
         const int RS = softmax_record_stride(D);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = 1 + D;
@@ -459,7 +459,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         SmLaunch L;
         L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.coef = a->g; L.alpha = a->row_shift; L.M = M;
-        L.split = pl.split; L.tiles_per_split = pl.tiles_per_split; L.ntiles = pl.ntiles;
+        L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv;
         L.negc = (float)(-kLog2e / a->scale); L.scale_grad = -2.0 / a->scale;
         L.out = a->out; L.out_f64 = out_f64; L.out_grad = a->out_grad; L.part = part;
         int ctas = 0;

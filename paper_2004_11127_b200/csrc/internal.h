@@ -150,7 +150,7 @@ struct SmLaunch {
     const double *alpha;
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split, npv;  // record-pair j-splits (multiple of kSplitGrain)
     float negc;
     double scale_grad;
     void *out; int out_f64;

@@ -31,7 +31,7 @@ struct SmParams {
     const double *alpha;
     int64_t M;
     int split;
-    int64_t tiles_per_split, ntiles;
+    int64_t pairs_per_split, npv;      // record-pair j-splits (see SumParams)
     float negc;               // -log2(e)/eps
     double scale_grad;        // -2/eps
     void *out;
@@ -47,11 +47,12 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
     extern __shared__ __align__(128) unsigned char smem_raw[];
     const int64_t itile = blockIdx.x / p.split;
     const int sp = (int)(blockIdx.x % p.split);
-    const int64_t t0 = (int64_t)sp * p.tiles_per_split;
-    const int64_t t1 = min(t0 + p.tiles_per_split, p.ntiles);
-    const int nt = (int)(t1 - t0);
+    const int64_t q0 = (int64_t)sp * p.pairs_per_split;                 // record pairs [q0, q0 + npc)
+    const int64_t npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
     JRing<kStages> ring;
-    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + t0 * Cfg::TILE_FLOATS, nt, kConsumerWarps);
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * RS, nt, kConsumerWarps, (uint32_t)last_np * RS * 4u);
 
     const int ct = threadIdx.x;
     const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
@@ -80,8 +81,9 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
 
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
 #pragma unroll 2
-        for (int pp = 0; pp < Cfg::PAIRS; ++pp) {
+        for (int pp = 0; pp < np; ++pp) {
             float f[RS];
 #pragma unroll
             for (int q = 0; q < RS / 4; ++q) {
@@ -153,7 +155,7 @@ static cudaError_t run_sm(const SmLaunch &a, cudaStream_t st, int *ctas) {
     }
     SmParams p;
     p.x = a.x; p.J = a.J; p.coef = a.coef; p.alpha = a.alpha; p.M = a.M; p.split = a.split;
-    p.tiles_per_split = a.tiles_per_split; p.ntiles = a.ntiles; p.negc = a.negc;
+    p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.negc = a.negc;
     p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64; p.out_grad = a.out_grad;
     p.part = a.part;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
