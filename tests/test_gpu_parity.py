@@ -927,3 +927,20 @@ def test_ranges_host_mode_matches_device(G):
     dh, jh = G.eval("sqdist", "argkmin", x, y, K=4, ranges=ranges)
     np.testing.assert_array_equal(host(dd), dh)
     np.testing.assert_array_equal(host(jd), jh)
+
+
+@pytest.mark.parametrize("M,N,D", [(1, 50_000, 3), (9, 30_001, 2), (300, 200_000, 3), (4000, 700, 5)])
+def test_lse_grad_shapes(G, M, N, D):
+    """LSE backward across the planner's regimes (few rows / many record-pair splits / many rows,
+    few j) against oracle O6."""
+    rng = np.random.default_rng(M * 31 + N)
+    eps = 0.08
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    h = rng.standard_normal(N).astype(np.float32)
+    g = rng.standard_normal(M).astype(np.float32)
+    a, _ = oracle.lse(x, y, h, eps=eps)
+    S, gx = G.eval("lse_grad", "sum", dev(x), dev(y), None, dev(g), scale=eps, out_dtype="float64",
+                   row_shift=dev(-a), col_shift=dev(h.astype(np.float64)))
+    oS, oG, dS, dG = oracle.softmax_grad(x, y, alpha=-a, beta=h, coef=g, eps=eps)
+    assert_sum_parity(host(S), oS, dS, what=f"softmax sum M={M}")
+    assert_sum_parity(host(gx), oG, dG, what=f"lse grad x M={M}")
