@@ -60,9 +60,10 @@ def workload(cid: int) -> dict:
     c = synth.config(cid)
     if cid in (1, 5):  # expanded form: u = 2x'.y' - |y'|^2 (3 FFMA) + acc (1 FFMA) = 4 lane-ops
         return dict(cfg=c, formula="gauss", reduction="sum", fp32=4, mufu=1, out_dtype="float32")
-    if cid == 2:   # Sum + gradient, one fused pass, expanded form: u (3 FFMA) + w = e b + S0 += w
-        #            + S += w y' (3 FFMA) = 8 lane-ops (the direct form needs 12)
-        return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=8, mufu=1,
+    if cid == 2:   # Sum + gradient, one fused pass, expanded form: u (3 FFMA) + S0 += e b (1 FFMA)
+        #            + S += e (b y') (3 FFMA, b y' packed with the j-records) = 7 lane-ops; the peak
+        #            is the MUFU's either way (min(16/1, 128/7) = 16 pairs/clk/SM)
+        return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=7, mufu=1,
                     out_dtype="float32")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")

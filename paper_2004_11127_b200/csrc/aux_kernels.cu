@@ -66,6 +66,11 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                 rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;   // w = -|y'|^2
                 for (int e = 0; e < E; ++e)
                     rec[2 * D + 2 + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
+                if (raw && E == 1 && kGradBY) {                       // b y' (expanded form only)
+                    const float bj = valid ? (b ? bs[jj] : 1.0f) : 0.0f;
+                    for (int d = 0; d < D; ++d)
+                        rec[2 * D + 4 + 2 * d + h] = geo.expanded ? bj * rec[2 * d + h] : 0.0f;
+                }
                 continue;
             }
             for (int d = 0; d < D; ++d) {
@@ -104,8 +109,8 @@ static int pack_smem_bytes(int kind, int D, int E, int RS, bool has_b) {
 }
 
 int pack_record_stride(int kind, int D, int E) {
-    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW)
-        return record_stride(D + 1, E);
+    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) return record_stride(D + 1, E);
+    if (kind == PACK_GAUSS_AUTO_RAW) return gauss_record_stride(D, E, true);
     if (kind == PACK_ARGKMIN) return record_stride(D + 1, 0);      // + the j pair
     if (kind == PACK_LSE_HZ) return record_stride(D, 0);
     if (kind == PACK_LSE_H) return record_stride(D, 2);
@@ -183,8 +188,14 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
             if (gauto) rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;
             for (int e = 0; e < E; ++e)
                 rec[boff + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
+            if (kind == PACK_GAUSS_AUTO_RAW && E == 1 && kGradBY) {   // b y' (expanded form only)
+                const float bj = valid ? (b ? b[j] : 1.0f) : 0.0f;
+                for (int d = 0; d < D; ++d)
+                    rec[boff + 2 + 2 * d + h] = geo.expanded ? bj * rec[2 * d + h] : 0.0f;
+            }
         }
-        for (int k = boff + 2 * E; k < RS; ++k) rec[k] = 0.0f;
+        const int used = boff + 2 * E + ((kind == PACK_GAUSS_AUTO_RAW && E == 1 && kGradBY) ? 2 * D : 0);
+        for (int k = used; k < RS; ++k) rec[k] = 0.0f;
     }
 }
 

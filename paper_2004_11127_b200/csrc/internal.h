@@ -33,6 +33,18 @@ constexpr float kLseSentinel = -3.0e38f;    // finite "minus infinity" reference
 // j-splits of the Sum and LSE kernels are whole multiples of this many record pairs (32 j): the
 // Sum's record-pair unroll and the LSE's 16-pair rescale sub-chunk both divide it.
 constexpr int kSplitGrain = 16;
+// Gradient modes with E = 1: the j-records also carry b_j y'_j (expanded form), so a pair
+// accumulates S0 += e b and S_d += e (b y')_d with 1 + D FFMA2 instead of FMUL2 + FADD2 + D FFMA2.
+#ifndef GENRED_GRAD_BY
+#define GENRED_GRAD_BY 1
+#endif
+constexpr bool kGradBY = GENRED_GRAD_BY != 0;
+// Record-pair floats of the Gaussian family: [2D coords][w pair][2E signal][2D b y' (gradient
+// modes with E = 1, kGradBY)], padded to 16 bytes.
+inline int gauss_record_stride(int D, int E, bool grad) {
+    const int by = (grad && E == 1 && kGradBY) ? 2 * D : 0;
+    return (2 * (D + 1) + 2 * E + by + 3) / 4 * 4;
+}
 
 // Record stride (floats) of one j-PAIR in the packed layout: 2*(D+E) rounded up to 4.
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }

@@ -11,16 +11,17 @@
 
 namespace genred {
 
-// Rows per thread of the gradient modes for D + E <= 4: 2 rows at 3 CTAs/SM measured 10.74
-// pairs/clk/SM against 10.48 for 4 rows at 2 CTAs/SM (fused Sum+grad, M = N = 1e5).
+// Gradient modes with D + E <= 4 (fused Sum+grad, M = N = 1e5, records carrying b y'): 4 rows per
+// thread, 4 record pairs per iteration, 2 CTAs/SM (128 registers) measured 11.47 pairs/clk/SM;
+// 2 rows / 2 pairs / 3 CTAs 10.78; 4 / 4 / 3 CTAs (80 registers, spilling) 11.23; 4 / 8 11.10.
 #ifndef GENRED_GRAD_R
-#define GENRED_GRAD_R 2
+#define GENRED_GRAD_R 4
 #endif
 #ifndef GENRED_GRAD_MINB
-#define GENRED_GRAD_MINB 3
+#define GENRED_GRAD_MINB 2
 #endif
 #ifndef GENRED_GRAD_HH
-#define GENRED_GRAD_HH 2
+#define GENRED_GRAD_HH 4
 #endif
 
 template <int MODE, int D, int E>
@@ -28,7 +29,10 @@ struct SumCfg {
     // record pair: 2D coordinates, then (MODE 0 only) the pair slot of w = -|y'|^2 used by the
     // expanded form, then 2E signal values; padded to a multiple of 16 bytes
     static constexpr int BOFF = (MODE != 3) ? 2 * (D + 1) : 2 * D;
-    static constexpr int RS = ((BOFF + 2 * E) + 3) / 4 * 4;       // floats per record pair
+    // gradient modes, E = 1: 2D more floats, b_j y'_j (expanded form; zero in direct records)
+    static constexpr bool BY = (MODE == 1 || MODE == 2) && E == 1 && kGradBY;
+    static constexpr int BYOFF = BOFF + 2 * E;
+    static constexpr int RS = ((BOFF + 2 * E + (BY ? 2 * D : 0)) + 3) / 4 * 4;   // floats per record pair
     static constexpr int PAIRS = kTileJ / 2;
     static constexpr int TILE_FLOATS = PAIRS * RS;
     static constexpr int NS = (MODE == 1) ? 0 : E;                // sum columns
@@ -169,8 +173,15 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
                         for (int e = 0; e < E; ++e) acc[r][e] = fma2(ex, bv[e], acc[r][e]);
                     } else {
-                        float2 wt;
-                        if constexpr (E == 1) {
+                        float2 wt = make_float2(0.f, 0.f);
+                        if constexpr (Cfg::BY) {
+                            // S0 += e b, S_d += e (b y')_d: b y' comes with the record
+                            float2 &S0r = (MODE == 2) ? acc[r][0] : s0[r];
+                            S0r = fma2(ex, bv[0], S0r);
+#pragma unroll
+                            for (int d = 0; d < D; ++d)
+                                accg[r][d] = fma2(ex, make_float2(f[Cfg::BYOFF + 2 * d], f[Cfg::BYOFF + 2 * d + 1]), accg[r][d]);
+                        } else if constexpr (E == 1) {
                             wt = mul2(ex, bv[0]);                       // e b (g_i applied later)
                         } else {
                             float2 bg = mul2(bv[0], dup2(gr[r][0]));
@@ -178,6 +189,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                             for (int e = 1; e < E; ++e) bg = fma2(bv[e], dup2(gr[r][e]), bg);
                             wt = mul2(ex, bg);                          // e <b, g_i>
                         }
+                        if constexpr (!Cfg::BY) {
                         if constexpr (MODE == 2 && E == 1) {
                             acc[r][0] = add2(acc[r][0], wt);           // Sum == S0
                         } else {
@@ -190,6 +202,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                         // (two scalar FFMAs instead of this 3-register-pair FFMA2 measured 2% slower)
 #pragma unroll
                         for (int d = 0; d < D; ++d) accg[r][d] = fma2(wt, ny[d], accg[r][d]);   // w y'
+                        }
                     }
                 }
             } else {
