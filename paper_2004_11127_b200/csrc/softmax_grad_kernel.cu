@@ -15,7 +15,13 @@
 #include "device.cuh"
 #include "internal.h"
 
+#ifndef GENRED_SM_UNROLL
+#define GENRED_SM_UNROLL 2
+#endif
+
 namespace genred {
+
+constexpr int kSmUnroll = GENRED_SM_UNROLL;      // record pairs unrolled per pair-loop iteration
 
 template <int D>
 struct SmCfg {
@@ -82,7 +88,7 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
         const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
-#pragma unroll 2
+#pragma unroll kSmUnroll
         for (int pp = 0; pp < np; ++pp) {
             float f[RS];
 #pragma unroll
@@ -94,7 +100,6 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
 #pragma unroll
             for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
             const float2 bhi = make_float2(f[2 * D], f[2 * D + 1]);
-            const float2 blo = make_float2(f[2 * D + 2], f[2 * D + 3]);
             const float2 sig = make_float2(f[2 * D + 4], f[2 * D + 5]);
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -104,8 +109,10 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
                 float2 q = mul2(dd[0], dd[0]);
 #pragma unroll
                 for (int d = 1; d < D; ++d) q = fma2(dd[d], dd[d], q);
-                // alpha' + beta' with hi/lo parts: (beta_hi + alpha_hi) + beta_lo + alpha_lo
-                const float2 z = add2(add2(add2(bhi, dup2(ahi[r])), blo), dup2(alo[r]));
+                // alpha' + beta': only the hi parts enter the exponent (their sum is exact when
+                // they nearly cancel); 2^beta_lo is folded into sig by the pack, 2^alpha_lo is
+                // applied to the row's fp64 sums at the end
+                const float2 z = add2(bhi, dup2(ahi[r]));
                 const float2 t = fma2(q, negc2, z);
                 const float2 w = mul2(make_float2(ex2(t.x), ex2(t.y)), sig);
                 s0[r] = add2(s0[r], w);
@@ -130,6 +137,10 @@ __global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParam
     for (int r = 0; r < R; ++r) {
         const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
         if (i >= p.M) continue;
+        const double flo = exp2((double)alo[r]);                 // the 2^alpha_lo factor
+        s064[r] *= flo;
+#pragma unroll
+        for (int d = 0; d < D; ++d) sg64[r][d] *= flo;
         if (p.split > 1) {
             double *dst = p.part + ((int64_t)sp * p.M + i) * C;
             dst[0] = s064[r];
@@ -176,13 +187,16 @@ static int occ_sm() {
 }
 
 // rows per thread: 2 for D <= 4 (registers: D + 2 shifts + 2 + 2D accumulators + 1 + D fp64), else 1
-int sm_rows_per_thread_max(int D) { return D <= 4 ? 2 : 1; }
+#ifndef GENRED_SM_R
+#define GENRED_SM_R 4
+#endif
+int sm_rows_per_thread_max(int D) { return D <= 4 ? GENRED_SM_R : 1; }
 
 #define GENRED_SM_D(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8)
 
 cudaError_t launch_softmax_grad(const SmLaunch &a, cudaStream_t st, int *ctas) {
 #define GENRED_CASE(DD) \
-    if (a.D == DD) return (a.R == 1 || DD > 4) ? run_sm<DD, 1>(a, st, ctas) : run_sm<DD, (DD <= 4 ? 2 : 1)>(a, st, ctas);
+    if (a.D == DD) return (a.R == 1 || DD > 4) ? run_sm<DD, 1>(a, st, ctas) : run_sm<DD, (DD <= 4 ? GENRED_SM_R : 1)>(a, st, ctas);
     GENRED_SM_D(GENRED_CASE)
 #undef GENRED_CASE
     return cudaErrorInvalidValue;
@@ -190,7 +204,7 @@ cudaError_t launch_softmax_grad(const SmLaunch &a, cudaStream_t st, int *ctas) {
 
 int softmax_grad_occupancy(int D, int R) {
 #define GENRED_CASE(DD) \
-    if (D == DD) return (R == 1 || DD > 4) ? occ_sm<DD, 1>() : occ_sm<DD, (DD <= 4 ? 2 : 1)>();
+    if (D == DD) return (R == 1 || DD > 4) ? occ_sm<DD, 1>() : occ_sm<DD, (DD <= 4 ? GENRED_SM_R : 1)>();
     GENRED_SM_D(GENRED_CASE)
 #undef GENRED_CASE
     return 1;
@@ -215,8 +229,10 @@ __global__ void pack_softmax_kernel(const float *__restrict__ y, const float *__
             const double b2 = (valid && beta) ? 1.4426950408889634074 * beta[j] : 0.0;
             const float hi = valid ? (float)b2 : -INFINITY;
             rec[2 * D + h] = hi;
-            rec[2 * D + 2 + h] = valid ? (float)(b2 - (double)hi) : 0.0f;
-            rec[2 * D + 4 + h] = valid ? (sig ? sig[j] : 1.0f) : 0.0f;
+            rec[2 * D + 2 + h] = 0.0f;                            // (beta_lo: folded into sig)
+            // sig' = sig 2^(beta'_lo) in fp64, rounded once: the kernel's exponent uses beta'_hi
+            const double lo = valid ? b2 - (double)hi : 0.0;
+            rec[2 * D + 4 + h] = valid ? (float)((sig ? (double)sig[j] : 1.0) * exp2(lo)) : 0.0f;
         }
         for (int k = 2 * D + 6; k < RS; ++k) rec[k] = 0.0f;
     }
