@@ -13,7 +13,18 @@
 #include "device.cuh"
 #include "internal.h"
 
+#ifndef GENRED_ARGK_R
+#define GENRED_ARGK_R 2
+#endif
+// record pairs unrolled per iteration: 4 measured 12.88 / 12.52 pairs/clk/SM (K = 1 / 10, M = 1e5,
+// N = 1e7) against 12.72 / 11.82 for 2; 4 rows per thread for K <= 4 measured slower (11.93)
+#ifndef GENRED_ARGK_UNROLL
+#define GENRED_ARGK_UNROLL 4
+#endif
+
 namespace genred {
+
+constexpr int kArgkUnroll = GENRED_ARGK_UNROLL;   // record pairs unrolled per pair-loop iteration
 
 template <int D>
 struct ArgkCfg {
@@ -107,7 +118,7 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
         const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
-#pragma unroll 2
+#pragma unroll kArgkUnroll
         for (int pp = 0; pp < np; ++pp) {
             float f[RS];
 #pragma unroll
@@ -154,7 +165,7 @@ __global__ void __launch_bounds__(kThreads, 2) argk_kernel(const ArgkParams p) {
 }
 
 template <int KMAX>
-constexpr int argk_rows() { return KMAX <= 4 ? 2 : 1; }
+constexpr int argk_rows() { return KMAX <= 4 ? GENRED_ARGK_R : 1; }
 
 template <int D, int KMAX>
 static cudaError_t run_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas) {
@@ -203,7 +214,7 @@ static int occ_argk_k(int K) {
     return occ_argk<D, 32>();
 }
 
-int argk_rows_per_thread(int K) { return K <= 4 ? 2 : 1; }
+int argk_rows_per_thread(int K) { return K <= 4 ? GENRED_ARGK_R : 1; }
 
 #define GENRED_ARGK_D(X) X(1) X(2) X(3) X(4) X(5) X(6) X(7) X(8) X(9) X(10) X(11) X(12) X(13) X(14) X(15) X(16)
 
