@@ -84,12 +84,12 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                 for (int e = 0; e < E; ++e)
                     rec[2 * D + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
             } else if (kind == PACK_LSE_H) {
-                // h' = log2(e) h as an fp32 hi + lo pair (fp64 product), so that
-                // (h'_hi - m) + h'_lo keeps |h| ~ 1e4 biases exact to fp32 rounding of t.
+                // h' = log2(e) h split into an fp32 hi part, which enters the exponent, and the
+                // factor c = 2^(h'_lo) of the term: |h| ~ 1e4 biases stay exact to fp32 rounding.
                 const double hv = valid ? hscale * (double)bs[jj] : 0.0;
                 const float hi = valid ? (float)hv : NEG_INF;
                 rec[2 * D + h] = hi;
-                rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
+                rec[2 * D + 2 + h] = valid ? (float)exp2(hv - (double)hi) : 0.0f;   // c = 2^(h'_lo)
             }
         }
         __syncthreads();
@@ -164,7 +164,7 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                     const double hv = valid ? 1.4426950408889634074 * (double)b[j] : 0.0;
                     const float hi = valid ? (float)hv : -INFINITY;
                     rec[2 * D + h] = hi;
-                    rec[2 * D + 2 + h] = valid ? (float)(hv - (double)hi) : 0.0f;
+                    rec[2 * D + 2 + h] = valid ? (float)exp2(hv - (double)hi) : 0.0f;   // c = 2^(h'_lo)
                 }
             }
             for (int k = 2 * D + (kind == PACK_LSE_H ? 4 : kind == PACK_ARGKMIN ? 2 : 0); k < RS; ++k) rec[k] = 0.0f;

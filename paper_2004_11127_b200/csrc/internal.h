@@ -54,8 +54,8 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
 // kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
-// (Sum kinds), nothing more (ArgKMin, LSE with h = 0), or (h'hi[2p], h'hi[2p+1], h'lo[2p],
-// h'lo[2p+1]) with h' = hscale * h split into fp32 hi + lo (LSE with h).  Records past N
+// (Sum kinds), nothing more (ArgKMin, LSE with h = 0), or (h'hi[2p], h'hi[2p+1], c[2p], c[2p+1])
+// with h' = hscale * h, h'hi its fp32 rounding and c = 2^(h' - h'hi) (LSE with h).  Records past N
 // (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf (LSE, ArgKMin),
 // which contribute nothing.
 // PACK_GAUSS_AUTO (Gaussian Sum): decodes the bounding box `geo` (geo.cuh) and writes either the

@@ -97,9 +97,9 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
                 const float dd = xr[d] + rec[2 * d + h];
                 q1 = fmaf(dd, dd, q1);
             }
-            float hmv = -o.m;
-            if constexpr (!HZ) hmv = (rec[2 * D + h] + (-o.m)) + rec[2 * D + 2 + h];
-            c1 += ex2(fmaf(q1, negc, hmv));
+            float hmv = -o.m, cj = 1.0f;
+            if constexpr (!HZ) { hmv = rec[2 * D + h] + (-o.m); cj = rec[2 * D + 2 + h]; }
+            c1 = fmaf(ex2(fmaf(q1, negc, hmv)), cj, c1);
         }
     }
     o.c1 = c1;
@@ -172,10 +172,11 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
                 float2 ny[D];
 #pragma unroll
                 for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
-                float2 hhi = make_float2(0.f, 0.f), hlo = make_float2(0.f, 0.f);
+                // with h: h'_hi enters the exponent, c = 2^(h'_lo) multiplies the term (R6c)
+                float2 hhi = make_float2(0.f, 0.f), hc = make_float2(1.f, 1.f);
                 if constexpr (!HZ) {
                     hhi = make_float2(f[2 * D], f[2 * D + 1]);
-                    hlo = make_float2(f[2 * D + 2], f[2 * D + 3]);
+                    hc = make_float2(f[2 * D + 2], f[2 * D + 3]);
                 }
 #pragma unroll
                 for (int r = 0; r < R; ++r) {
@@ -186,9 +187,10 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
                         dd = add2(dup2(xr[r][d]), ny[d]);
                         q2 = fma2(dd, dd, q2);
                     }
-                    const float2 hm = HZ ? dup2(-m[r]) : add2(add2(hhi, dup2(-m[r])), hlo);  // (h'-m)
+                    const float2 hm = HZ ? dup2(-m[r]) : add2(hhi, dup2(-m[r]));   // (h'_hi - m)
                     const float2 t = fma2(q2, negc2, hm);          // v - m, log2 units
-                    cs[r] = add2(cs[r], make_float2(ex2(t.x), ex2(t.y)));
+                    const float2 e = make_float2(ex2(t.x), ex2(t.y));
+                    cs[r] = HZ ? add2(cs[r], e) : fma2(e, hc, cs[r]);
                 }
             }
 #pragma unroll
@@ -287,10 +289,10 @@ __global__ void __launch_bounds__(kThreads, 2) lse_smm_kernel(const LseParams p)
             float2 ny[D];
 #pragma unroll
             for (int d = 0; d < D; ++d) ny[d] = make_float2(f[2 * d], f[2 * d + 1]);
-            float2 hhi = make_float2(0.f, 0.f), hlo = make_float2(0.f, 0.f);
+            float2 hhi = make_float2(0.f, 0.f), hc = make_float2(1.f, 1.f);
             if constexpr (!HZ) {
                 hhi = make_float2(f[2 * D], f[2 * D + 1]);
-                hlo = make_float2(f[2 * D + 2], f[2 * D + 3]);
+                hc = make_float2(f[2 * D + 2], f[2 * D + 3]);
             }
 #pragma unroll
             for (int r = 0; r < R; ++r) {
@@ -301,9 +303,10 @@ __global__ void __launch_bounds__(kThreads, 2) lse_smm_kernel(const LseParams p)
                     dd = add2(dup2(xr[r][d]), ny[d]);
                     q2 = fma2(dd, dd, q2);
                 }
-                const float2 hm = HZ ? dup2(-m[r]) : add2(add2(hhi, dup2(-m[r])), hlo);
+                const float2 hm = HZ ? dup2(-m[r]) : add2(hhi, dup2(-m[r]));
                 const float2 t = fma2(q2, negc2, hm);
-                const float2 cs = make_float2(ex2(t.x), ex2(t.y));
+                const float2 e = make_float2(ex2(t.x), ex2(t.y));
+                const float2 cs = HZ ? e : mul2(e, hc);
                 if (!(fmaxf(cs.x, cs.y) <= kSumMax)) {
                     const LseRescale rs = lse_rescale<D, HZ, RS, 1>(rec, xr[r], negc, m[r], s64[r], s32[r]);
                     m[r] = rs.m;

@@ -1,6 +1,8 @@
-for lib in build/variants/lse_*.so; do
+for lib in ${VARS:-build/var/libgenred_*.so}; do
   GENRED_LIB=$lib python - <<'PY'
-import os, torch, synth
+import os, sys, torch
+sys.path.insert(0, os.getcwd())
+import synth
 from paper_2004_11127_b200 import genred
 M = N = 1_000_000
 x = torch.from_numpy(synth.uniform3(M, 1003)).cuda(); y = torch.from_numpy(synth.gmm3(N, 2003)).cuda()
