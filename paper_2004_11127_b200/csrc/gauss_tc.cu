@@ -159,7 +159,6 @@ struct Params {
     int out_f64;
     int split;
     double *part;            // split > 1: split x M fp64 partials (sum_finalize layout, C = 1)
-    int dbg;                 // experiments only (GENRED_TC_DBG): 1 no MMA, 2 no tfull wait, 4 no TMEM load
 };
 
 __device__ __forceinline__ float4 lds128s(uint32_t addr) {     // LDS.128 (broadcast: one address per warp)
@@ -275,10 +274,8 @@ gauss_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
                     fence_after();
                     const uint64_t db = desc32(smem_u32(ring + stage * STAGE_BYTES));
                     const uint32_t d_tmem = tmem_base + acc * BN;
-                    if (!(p.dbg & 1)) {
                     mma_tf32(d_tmem, dlo, db, 0);        // A_lo . [B_hi | B_lo]  (second half 0)
                     mma_tf32(d_tmem, dhi, db, 1);        // + A_hi . [B_hi | B_lo]
-                    }
                     mma_commit(&empty[stage]);
                     mma_commit(&tfull[acc]);
                     if (++stage == STAGES) { stage = 0; phase ^= 1; }
@@ -298,7 +295,7 @@ gauss_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
             const int t0 = sp * p.tiles_per_split, t1 = min(t0 + p.tiles_per_split, p.n_ttiles);
             double a64 = 0.0;
             for (int t = t0; t < t1; ++t) {
-                if (!(p.dbg & 2)) mbar_wait(&tfull[acc], aphase);
+                mbar_wait(&tfull[acc], aphase);
                 mbar_wait(&full[stage], phase);          // b of this tile is visible
                 fence_after();
                 const uint32_t bv = smem_u32(ring + stage * STAGE_BYTES + B_BYTES) + cg * COLS * 4;
@@ -309,16 +306,8 @@ gauss_tc_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant
 #pragma unroll
                     for (int c = 0; c < COLS / 32; c += 2) {
                         uint32_t v0[32], v1[32];
-                        if (!(p.dbg & 4)) {
-                            tmem_ld32_nowait(taddr + c * 32, v0);
-                            tmem_ld32_nowait(taddr + c * 32 + 32, v1);
-                        } else {
-#pragma unroll
-                            for (int k = 0; k < 32; ++k) {
-                                v0[k] = __float_as_uint(-0.01f * (float)((lane + k) & 15));
-                                v1[k] = __float_as_uint(-0.02f * (float)((lane + k) & 15));
-                            }
-                        }
+                        tmem_ld32_nowait(taddr + c * 32, v0);
+                        tmem_ld32_nowait(taddr + c * 32 + 32, v1);
                         tmem_wait32(v0);
                         tmem_wait32(v1);
                         accumulate32(v0, bv + c * 128, s4);
@@ -494,7 +483,6 @@ static cudaError_t gtc_run(const GaussTcLaunch &a, cudaStream_t st, int *ctas, i
     p.n_units = p.n_rtiles * a.split;
     p.x = a.x; p.geo = a.geo; p.s = a.s; p.scale_sum = a.scale_sum;
     p.out = a.out; p.out_f64 = a.out_f64; p.part = a.part;
-    p.dbg = getenv("GENRED_TC_DBG") ? atoi(getenv("GENRED_TC_DBG")) : 0;
     auto kern = gtc::gauss_tc_kernel<D>;
     {
         const cudaError_t e = smem_opt_in((const void *)kern, gtc::SMEM_BYTES);

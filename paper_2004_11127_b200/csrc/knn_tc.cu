@@ -133,7 +133,6 @@ struct Params {
     int nk;                  // Dp / BK
     int n_rtiles, n_ttiles, n_groups, group;
     const float *xn, *yn;    // squared norms (fp32)
-    int dbg;                 // experiments only: bit0 = 1 MMA per k-step, bit1 = skip lo loads
     unsigned int *row_thr;   // M: best known K'-th screened value per row (float bits, >= 0)
     float *pd;               // n_groups x M x KP screened distances
     int32_t *pj;             // n_groups x M x KP indices
@@ -215,23 +214,10 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
                             mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
                             tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
                             tma_load_2d(sb + A_BYTES, &map_xlo, kb * BK, r * BM, &full[stage]);
-                            if (p.dbg & 4) {                         // experiment: no multicast
-                                for (int hq = 0; hq < CL; ++hq) {
-                                    tma_load_2d(sb + 2 * A_BYTES + hq * HB, &map_yhi, kb * BK,
-                                                t * BN + hq * (BN / CL), &full[stage]);
-                                    tma_load_2d(sb + 2 * A_BYTES + B_BYTES + hq * HB, &map_ylo, kb * BK,
-                                                t * BN + hq * (BN / CL), &full[stage]);
-                                }
-                            } else {
                             tma_load_2d_mc(sb + 2 * A_BYTES + crank * HB, &map_yhi, kb * BK,
                                            t * BN + crank * (BN / CL), &full[stage], mc_mask);
                             tma_load_2d_mc(sb + 2 * A_BYTES + B_BYTES + crank * HB, &map_ylo, kb * BK,
                                            t * BN + crank * (BN / CL), &full[stage], mc_mask);
-                            }
-                        } else if (p.dbg & 2) {
-                            mbar_arrive_expect_tx(&full[stage], A_BYTES + B_BYTES);
-                            tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
-                            tma_load_2d(sb + 2 * A_BYTES, &map_yhi, kb * BK, t * BN, &full[stage]);
                         } else {
                         mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
                         tma_load_2d(sb, &map_xhi, kb * BK, r * BM, &full[stage]);
@@ -266,13 +252,9 @@ knn_tc_kernel(const __grid_constant__ CUtensorMap map_xhi, const __grid_constant
 #pragma unroll
                         for (int k = 0; k < BK / 8; ++k) {
                             const uint64_t off = (uint64_t)(k * 32) >> 4;    // 8 tf32 = 32 B
-                            if (p.dbg & 1) {
-                                mma_tf32(d_tmem, ahi + off, bhi + off, (kb | k) != 0);
-                            } else {
                             mma_tf32(d_tmem, alo + off, bhi + off, (kb | k) != 0);
                             mma_tf32(d_tmem, ahi + off, blo + off, 1);
                             mma_tf32(d_tmem, ahi + off, bhi + off, 1);
-                            }
                         }
                         if (CL > 1) mma_commit_mc(&empty[stage], mc_mask);
                         else mma_commit(&empty[stage]);
@@ -807,7 +789,6 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     tc::Params p;
     p.M = M; p.N = N; p.Dp = Dp; p.nk = Dp / tc::BK; p.n_rtiles = n_rtiles; p.n_ttiles = n_ttiles;
     p.n_groups = n_groups; p.group = group; p.xn = xn; p.yn = yn; p.pd = pd; p.pj = pj;
-    p.dbg = getenv("GENRED_KNN_DBG") ? atoi(getenv("GENRED_KNN_DBG")) : 0;
     p.row_thr = row_thr;
     if ((e = cudaMemsetAsync(row_thr, 0x7f, (size_t)M * 4, st)) != cudaSuccess) return e;   // 3.4e38
     const int n_units = n_groups * ((n_rtiles + CL - 1) / CL);

@@ -1,6 +1,6 @@
 # A/B of Gaussian Sum kernel variants on the same box (M = N = 2e6, interleaved runs)
 for rep in 1 2; do
-for lib in build/variants/sum_*.so; do
+for lib in ${VARS:-build/var/libgenred_*.so}; do
 GENRED_LIB=$lib python - <<'PY'
 import os, torch, synth
 from paper_2004_11127_b200 import genred
