@@ -23,10 +23,16 @@
 namespace genred {
 namespace edge {
 
-constexpr int kRowsPerTile = 1024;
+#ifndef GENRED_EDGE_ROWS
+#define GENRED_EDGE_ROWS 1024
+#endif
+constexpr int kRowsPerTile = GENRED_EDGE_ROWS;
 constexpr int kThreads = 256;
 constexpr int kRows = kRowsPerTile / kThreads;      // rows per thread per tile
-constexpr int kStages = 4;
+#ifndef GENRED_EDGE_STAGES
+#define GENRED_EDGE_STAGES 4
+#endif
+constexpr int kStages = GENRED_EDGE_STAGES;
 constexpr int kMaxPairs = 32;                       // N <= 64
 
 template <int D>
