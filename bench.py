@@ -198,7 +198,7 @@ def run_reference(args, rank: int, world: int) -> None:
     c = w["cfg"]
     x, y, b = make_inputs(w, args.dist)
     ref_pairs = args.ref_pairs or (1e9 if w["reduction"] != "argkmin" else 1e9 / c.D)
-    rows_per_step = max(1, int(ref_pairs // c.N))
+    rows_per_step = max(1, min(c.M, int(ref_pairs // c.N)))
     rng = np.random.default_rng(12345)
 
     def step():
