@@ -121,13 +121,18 @@ void oracle_gauss_gradx(int64_t M, int64_t N, int D, int E, double sigma,
         nsum *den = calloc((size_t)D, sizeof(nsum));
         for (int64_t j = 0; j < N; ++j) {
             double k = exp(-sqdist(x + i * D, y + j * D, D) * inv_s2);
-            double bg = 0.0;
-            for (int e = 0; e < E; ++e)
-                bg += (b ? b[j * E + e] : 1.0) * (g ? g[i * E + e] : 1.0);
+            double bg = 0.0, bga = 0.0;
+            for (int e = 0; e < E; ++e) {
+                const double p = (b ? b[j * E + e] : 1.0) * (g ? g[i * E + e] : 1.0);
+                bg += p;
+                bga += fabs(p);
+            }
             for (int d = 0; d < D; ++d) {
-                double t = -2.0 * inv_s2 * (x[i * D + d] - y[j * D + d]) * k * bg;
-                nsum_add(&acc[d], t);
-                nsum_add(&den[d], fabs(t));
+                double t = -2.0 * inv_s2 * (x[i * D + d] - y[j * D + d]) * k;
+                nsum_add(&acc[d], t * bg);
+                /* R4b: the terms are the elementary products t b_je g_ie, so the denominator
+                 * sums |t| sum_e |b_je g_ie| (equal to |t bg| when E = 1) */
+                nsum_add(&den[d], fabs(t) * bga);
             }
         }
         for (int d = 0; d < D; ++d) {
