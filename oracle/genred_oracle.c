@@ -18,6 +18,7 @@
  *   oracle_gauss_sum    O1  F = exp(-|x_i-y_j|^2/sigma^2) * b_j           PAPER.md:166-167, 182 (R1)
  *   oracle_gauss_gradx  O2  G_i = sum_j (-2/sigma^2)(x_i-y_j) e_ij <b_j,g_i>  PAPER.md:141-147, 168 (R10)
  *   oracle_lse          O3  F = -|x_i-y_j|^2/eps + h_j ; a_i = m_i + log sum_j exp(F_ij - m_i)
+ *   oracle_lse_cond         the metric's conditioning of O3 (reading R6b)
  *                                                                          PAPER.md:85, 134 (R5)
  *   oracle_argkmin      O4  K smallest (|x_i-y_j|^2, j) in lexicographic order   PAPER.md:85, 134 (R7-R9)
  *   oracle_sqdist_sum   O5  sum_j |x_i-y_j|^2 b_j  (test combination)
@@ -172,6 +173,28 @@ void oracle_lse(int64_t M, int64_t N, int D, double eps,
         }
         out[r] = a;
         if (mmax) mmax[r] = m;
+    }
+}
+
+/* Conditioning of O3 for the error metric (reading R6b): C_i = sum_j p_ij (|x_i-y_j|^2/eps + |h_j|),
+ * p_ij = exp(F_ij - a_i) the softmax weights.  a_i moves by sum_j p_ij dF_ij when each F_ij is
+ * perturbed by dF_ij, and an fp32 evaluation perturbs F_ij by a few ulps of its two parts. */
+void oracle_lse_cond(int64_t M, int64_t N, int D, double eps,
+                     const double *x, const double *y, const double *h,
+                     const int64_t *rows, int64_t nrows, const double *a, double *cond) {
+    int64_t R = rows ? nrows : M;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t i = row_of(rows, r);
+        nsum c = {0.0, 0.0};
+        if (isfinite(a[r])) {
+            for (int64_t j = 0; j < N; ++j) {
+                const double q = sqdist(x + i * D, y + j * D, D) / eps;
+                const double hj = h ? h[j] : 0.0;
+                nsum_add(&c, exp(-q + hj - a[r]) * (q + fabs(hj)));
+            }
+        }
+        cond[r] = nsum_get(&c);
     }
 }
 

@@ -46,6 +46,8 @@ def _load():
             lib.oracle_gauss_sum.argtypes = [I64, I64, I32, I32, F64, P, P, P, P, I64, P, P]
             lib.oracle_gauss_gradx.argtypes = [I64, I64, I32, I32, F64, P, P, P, P, P, I64, P, P]
             lib.oracle_lse.argtypes = [I64, I64, I32, F64, P, P, P, P, I64, P, P]
+            lib.oracle_lse_cond.argtypes = [I64, I64, I32, F64, P, P, P, P, I64, P, P]
+            lib.oracle_lse_cond.restype = None
             lib.oracle_argkmin.argtypes = [I64, I64, I32, I32, P, P, P, I64, P, P]
             lib.oracle_sqdist_sum.argtypes = [I64, I64, I32, I32, P, P, P, P, I64, P, P]
             lib.oracle_softmax_grad.argtypes = [I64, I64, I32, F64, P, P, P, P, P, P, P, I64, P, P, P, P]
@@ -121,8 +123,9 @@ def gauss_gradx(x, y, b=None, g=None, sigma=1.0, rows=None):
     return out, den
 
 
-def lse(x, y, h=None, eps=1.0, rows=None):
-    """O3.  Returns (a [R], m [R]) in fp64; m_i = max_j F_ij."""
+def lse(x, y, h=None, eps=1.0, rows=None, cond=False):
+    """O3.  Returns (a [R], m [R]) in fp64; m_i = max_j F_ij.  cond=True also returns
+    C_i = sum_j p_ij (|x_i - y_j|^2/eps + |h_j|), the metric's conditioning (reading R6b)."""
     x = _f64(x); y = _f64(y)
     M, D = x.shape; N = y.shape[0]
     h = None if h is None else _f64(h).reshape(-1)
@@ -131,7 +134,12 @@ def lse(x, y, h=None, eps=1.0, rows=None):
     out = np.empty(R); mm = np.empty(R)
     _load().oracle_lse(M, N, D, float(eps), _ptr(x), _ptr(y), _ptr(h), _ptr(r), nr,
                        _ptr(out), _ptr(mm))
-    return out, mm
+    if not cond:
+        return out, mm
+    cc = np.empty(R)
+    _load().oracle_lse_cond(M, N, D, float(eps), _ptr(x), _ptr(y), _ptr(h), _ptr(r), nr,
+                            _ptr(out), _ptr(cc))
+    return out, mm, cc
 
 
 def argkmin(x, y, K, rows=None):

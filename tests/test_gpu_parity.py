@@ -906,8 +906,8 @@ def test_randomized_shapes_against_oracle(G, seed):
         eps = float(rng.choice([0.02, 0.1, 1.0]))
         a = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=eps,
                    split_j=split, out_dtype="float64")
-        o, _ = oracle.lse(x, y, h, eps=eps)
-        assert_lse_parity(host(a), o, rel=True, what=f"seed {seed} lse")
+        o, _, cond = oracle.lse(x, y, h, eps=eps, cond=True)
+        assert_lse_parity(host(a), o, rel=True, cond=cond, D=D, what=f"seed {seed} lse")
     else:
         K = int(rng.choice([1, 3, 10, 32]))
         d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)

@@ -360,3 +360,15 @@ def test_softmax_grad_is_lse_gradient():
             ym = y.copy(); ym[j, d] -= step
             fd = (g * (oracle.lse(x, yp, h, eps=eps)[0] - oracle.lse(x, ym, h, eps=eps)[0])).sum() / (2 * step)
             assert abs(Gy[j, d] - fd) <= 1e-7 * dGy[j, d] + 1e-9
+
+
+def test_lse_conditioning_closed_forms():
+    """oracle_lse_cond (the R6b metric's C_i): one j gives C = |x-y|^2/eps + |h|; equal exponents
+    give the plain average of the magnitudes."""
+    x = np.array([[0.1, 0.2, 0.3]]); y = np.array([[0.4, 0.0, 0.3]])
+    a, _, c = oracle.lse(x, y, np.array([-2.5]), eps=0.1, cond=True)
+    assert abs(c[0] - (0.13 / 0.1 + 2.5)) < 1e-12
+    y2 = np.array([[0.1, 0.2, 0.3], [0.1, 0.2, 0.3]])
+    a, _, c = oracle.lse(x, y2, np.array([1.0, -1.0]), eps=0.1, cond=True)
+    p = np.exp(np.array([1.0, -1.0]) - a[0])
+    assert abs(c[0] - (p[0] * 1.0 + p[1] * 1.0)) < 1e-12
