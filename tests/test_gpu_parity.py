@@ -945,3 +945,36 @@ def test_lse_grad_shapes(G, M, N, D):
     oS, oG, dS, dG = oracle.softmax_grad(x, y, alpha=-a, beta=h, coef=g, eps=eps)
     assert_sum_parity(host(S), oS, dS, what=f"softmax sum M={M}")
     assert_sum_parity(host(gx), oG, dG, what=f"lse grad x M={M}")
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("GENRED_RANDOM_LARGE_SEEDS", "24")))))
+def test_randomized_large_n_against_oracle(G, seed):
+    """Seeded random cases with a long j axis (small-M CTAs, many record-pair splits, warp merges,
+    two-level K-list merges), checked on sampled rows."""
+    rng = np.random.default_rng(50_000 + seed)
+    red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin"]))
+    M = int(rng.choice([1, 5, 33, 64, 65, 300, 5000]))
+    N = int(rng.choice([100_003, 300_000]))
+    D = int(rng.integers(1, 5))
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    rows = np.unique(rng.integers(0, M, size=min(M, 40)))
+    if red in ("gauss", "gauss_sum_gradx"):
+        b = rng.standard_normal((N, 1)).astype(np.float32)
+        sigma = float(rng.choice([0.2, 0.5]))
+        res = G.eval(red, "sum", dev(x), dev(y), dev(b), scale=sigma)
+        res = res if isinstance(res, tuple) else (res,)
+        o, den = oracle.gauss_sum(x, y, b, sigma=sigma, rows=rows)
+        assert_sum_parity(host(res[0])[rows], o, den, what=f"large seed {seed} sum")
+        if red == "gauss_sum_gradx":
+            og, deng = oracle.gauss_gradx(x, y, b, None, sigma=sigma, rows=rows)
+            assert_sum_parity(host(res[1])[rows], og, deng, what=f"large seed {seed} grad")
+    elif red == "lse":
+        h = (rng.standard_normal(N)).astype(np.float32)
+        a = G.eval("sqdist", "lse", dev(x), dev(y), dev(h), scale=0.05, out_dtype="float64")
+        o, _, cond = oracle.lse(x, y, h, eps=0.05, rows=rows, cond=True)
+        assert_lse_parity(host(a)[rows], o, rel=True, cond=cond, D=D, what=f"large seed {seed} lse")
+    else:
+        K = int(rng.choice([1, 7, 16]))
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+        od, oj = oracle.argkmin(x, y, K + 1, rows=rows)
+        argk_check(host(d)[rows], host(j)[rows], od, oj, K, what=f"large seed {seed} argk")
