@@ -517,7 +517,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             const int Rs = sum_smm_rows(mode);
             const int64_t groups = (M + Rs - 1) / Rs;
             const int64_t slots = (int64_t)ctx->num_sms * sum_smm_occupancy(mode, D);
-            const int S = choose_split(groups, pl.npv, kSplitGrain, kMinSmmPairs, slots, nullptr, kMaxSplitSmm);
+            const int S = choose_split(groups, pl.npv, kSplitGrain, kMinSmmPairs, slots, nullptr, kMaxSplitSmm, 2e-4);
             pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
             pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
             pl.R = Rs;
@@ -629,7 +629,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             const int Rs = lse_smm_rows(D);
             const int64_t groups = (M + Rs - 1) / Rs;
             const int S = choose_split(groups, pl.npv, kSplitGrain, kMinSmmPairs, (int64_t)ctx->num_sms * 2,
-                                       nullptr, kMaxSplitSmm);
+                                       nullptr, kMaxSplitSmm, 2e-4);
             pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
             pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
             pl.R = Rs;
@@ -700,6 +700,15 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     const int K = a->K;
     const int R = argk_rows_per_thread(K);
     Plan pl = make_plan(ctx, a, 2, R, D, K, 0, true);
+    // small M: one row per CTA, its threads split j (see the Sum path)
+    const bool smm = a->split_j <= 0 && M <= kSmmMaxM && N > kDirectMaxN;
+    if (smm) {
+        const int S = choose_split(M, pl.npv, kSplitGrain, kMinSmmPairs, (int64_t)ctx->num_sms, nullptr,
+                                   kMaxSplitSmm, 2e-4);
+        pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+        pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+        pl.R = 1;
+    }
     const int RS = pack_record_stride(PACK_ARGKMIN, D, 0);
     const int64_t npairs = pl.ntiles * (kTileJ / 2);
     const size_t jbytes = al256((size_t)npairs * RS * 4);
@@ -722,7 +731,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
     L.pdist = pdist; L.pidx = pidx;
     int ctas = 0;
     prof_event(ctx, true, st);
-    e = launch_argk(L, st, &ctas);
+    e = smm ? launch_argk_smm(L, st, &ctas) : launch_argk(L, st, &ctas);
     prof_event(ctx, false, st);
     if (e != cudaSuccess) return cuda_fail(ctx, e, "argkmin kernel");
     int kernels = 2;
@@ -739,7 +748,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         kernels++;
     }
     ctx->launches += kernels;
-    ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = kConsumerWarps * 32 * pl.R;
+    ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? 1 : kConsumerWarps * 32 * pl.R;
     ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
     ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
     return GENRED_OK;

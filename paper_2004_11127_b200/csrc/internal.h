@@ -152,6 +152,9 @@ struct ArgkLaunch {
     int64_t n_units = 0;
 };
 cudaError_t launch_argk(const ArgkLaunch &a, cudaStream_t st, int *ctas);
+// Small-M mode (argk_kernel.cu): one row per CTA, threads split j, K-round CTA merge; grid =
+// M * split, split-major; partial lists as launch_argk's.
+cudaError_t launch_argk_smm(const ArgkLaunch &a, cudaStream_t st, int *ctas);
 int argk_occupancy(int D, int K, int R);
 int argk_rows_per_thread(int K);
 

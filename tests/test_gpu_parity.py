@@ -296,13 +296,17 @@ def test_argkmin_duplicates_across_splits(G, split):
 
 @pytest.mark.parametrize("M,K", [(1, 1), (3, 10), (50, 32)])
 def test_argkmin_small_m_many_splits(G, M, K):
-    """Few query rows against a large N: many record-pair j-splits whose K-lists merge in two
-    levels (groups of 64, then the group lists) under the (d, j) order."""
+    """Few query rows against a large N: the small-M mode (one row per CTA, its threads split j,
+    K-round CTA merge) and many record-pair j-splits whose K-lists merge in two levels (groups of
+    64, then the group lists) under the (d, j) order."""
     N = 400_000
     rng = np.random.default_rng(M * 7 + K)
     x = rng.random((M, 3)).astype(np.float32); y = rng.random((N, 3)).astype(np.float32)
     d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
-    assert G.last_plan()["split_j"] > 64, G.last_plan()
+    plan = G.last_plan()
+    assert plan["rows_per_cta"] == 1, plan                  # small-M mode: one row per CTA
+    if M == 1:
+        assert plan["split_j"] > 64, plan                   # two-level K-list merge
     od, oj = oracle.argkmin(x, y, K + 1)
     argk_check(host(d), host(j), od, oj, K, what=f"argk small M={M} K={K}")
 
