@@ -7,14 +7,16 @@
 // s_i = sum_j 2^(v_ij - m_i) (reading R6 in DESIGN.md):
 //   * RAW differences d = x - y (no pre-scaling of coordinates: the query shift of a pre-scaled
 //     x costs up to 1.35e-6 in a_i);
-//   * t = fma(negc, |d|^2, h' - m) then MUFU.EX2; two j's per packed FADD2/FFMA2;
+//   * t = fma(negc, |d|^2, h'_hi - m) then MUFU.EX2, times c = 2^(h' - h'_hi) when h != 0
+//     (reading R6c); two j's per packed FADD2/FFMA2;
 //   * lazy rescale: terms are summed per 16-j sub-chunk into a fresh fp32 pair; if that sum
 //     exceeds 2^16 (or overflows) the sub-chunk is discarded, m is
 //     set to the sub-chunk's exact max v (never m + t), s is rescaled in fp64 and the sub-chunk
 //     is recomputed -- rare (a few times per row);
 //   * fp32 partials are promoted to fp64 every 128 j; the output is finalised in fp64:
 //     a_i = ln2 (m_i + log2 s_i).
-// Pipeline and tiling are those of sum_kernel.cu (bulk-copy ring of 512-record j-tiles).
+// Pipeline and tiling are those of sum_kernel.cu (bulk-copy ring of 512-record j-tiles); the
+// small-M variant (lse_smm_kernel) gives each CTA a few rows whose threads split j.
 #include <math.h>
 
 #include "device.cuh"

@@ -6,16 +6,19 @@
 //   SQDIST_SUM  a_i   = sum_j |x_i - y_j|^2 b_j                           (test combination)
 //
 // Design (B200-first; the paper's GPU Gems "tiled map-reduce", is prior art):
-//   * one CTA owns 256*R i-rows, kept in registers (R rows per math thread), and one j-range;
-//   * a producer warp streams j-tiles (512 records, pair-interleaved, pre-scaled by
-//     s = sqrt(log2 e)/sigma so that exp(-|x-y|^2/sigma^2) = 2^(-|x'-y'|^2)) from HBM/L2 into a
-//     4-stage shared-memory ring with cp.async.bulk (TMA engine) completing on mbarriers;
+//   * one CTA owns 256*R i-rows, kept in registers (R rows per math thread), and one j-range of
+//     record pairs (a j-split);
+//   * j-tiles (512 records, pair-interleaved, pre-scaled by s = sqrt(log2 e)/sigma so that
+//     exp(-|x-y|^2/sigma^2) = 2^(-|x'-y'|^2)) stream from HBM/L2 into a 4-stage shared-memory
+//     ring with cp.async.bulk (TMA engine) completing on mbarriers; the last warp to release a
+//     stage refills it (all 8 warps are math warps, device.cuh JRing);
 //   * math warps read each record pair once per thread (broadcast LDS.128) and evaluate two j's
-//     at a time with packed FADD2/FMUL2/FFMA2 and two MUFU.EX2 (ex2.approx.ftz), so a pair costs
-//     3.5 issue slots of FP32 work + 1 MUFU for D=3 (the MUFU pipe, 16/clk/SM, is the bound);
+//     at a time with packed FADD2/FMUL2/FFMA2 and two MUFU.EX2 (ex2.approx.ftz): in the expanded
+//     form a pair costs 4 FP32 lane-ops + 1 MUFU for D=3 (the MUFU pipe, 16/clk/SM, is the bound);
 //   * per-tile fp32 partials are promoted to fp64 every 512 j (reading R18 in DESIGN.md);
-//   * j-splits (grid = i-tiles x splits) fill all 148 SMs; their fp64 partials are merged in a
-//     fixed order by sum_finalize (deterministic, no float atomics).
+//   * record-pair j-splits (grid = i-tiles x splits) fill all 148 SMs; their fp64 partials are
+//     merged in a fixed order by sum_finalize (deterministic, no float atomics);
+//   * the pair loop itself lives in sum_body.cuh, shared with the small-M kernels (sum_smm.cu).
 #include <math.h>
 #include <stdio.h>
 #include <stdlib.h>
