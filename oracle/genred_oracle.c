@@ -19,6 +19,7 @@
  *   oracle_gauss_gradx  O2  G_i = sum_j (-2/sigma^2)(x_i-y_j) e_ij <b_j,g_i>  PAPER.md:141-147, 168 (R10)
  *   oracle_lse          O3  F = -|x_i-y_j|^2/eps + h_j ; a_i = m_i + log sum_j exp(F_ij - m_i)
  *   oracle_lse_cond         the metric's conditioning of O3 (reading R6b)
+ *   oracle_gauss_cond       the metric's conditioning of O1 / O2 (reading R4c)
  *                                                                          PAPER.md:85, 134 (R5)
  *   oracle_argkmin      O4  K smallest (|x_i-y_j|^2, j) in lexicographic order   PAPER.md:85, 134 (R7-R9)
  *   oracle_sqdist_sum   O5  sum_j |x_i-y_j|^2 b_j  (test combination)
@@ -142,6 +143,48 @@ void oracle_gauss_gradx(int64_t M, int64_t N, int D, int E, double sigma,
         }
         free(acc);
         free(den);
+    }
+}
+
+/* Conditioning of O1 (grad = 0) / O2 (grad = 1) for the error metric (reading R4c), per output
+ * column c (E columns of O1, D of O2), with term_ij the elementary terms whose |.| sum is the R4
+ * denominator and u_ij = |x_i - y_j|^2 / sigma^2 the exponent (k_ij = exp(-u_ij)):
+ *   cond[r, c] = sum_j |term_ij| u_ij      -- an fp32 evaluation rounds u_ij by a few ulps, which
+ *                                             moves k_ij by that relative amount times u_ij;
+ *   tail[r, c] = sum_j |term_ij| [u_ij log2(e) >= 100]  -- terms below 2^-100: a product of k_ij
+ *                                             with the other factors leaves fp32's normal range. */
+void oracle_gauss_cond(int64_t M, int64_t N, int D, int E, double sigma, int grad,
+                       const double *x, const double *y, const double *b, const double *g,
+                       const int64_t *rows, int64_t nrows, double *cond, double *tail) {
+    int64_t R = rows ? nrows : M;
+    double inv_s2 = 1.0 / (sigma * sigma);
+    const int C = grad ? D : E;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t i = row_of(rows, r);
+        nsum *cs = calloc((size_t)C, sizeof(nsum));
+        nsum *ts = calloc((size_t)C, sizeof(nsum));
+        for (int64_t j = 0; j < N; ++j) {
+            const double u = sqdist(x + i * D, y + j * D, D) * inv_s2;
+            const double k = exp(-u);
+            const int deep = u * 1.4426950408889634 >= 100.0;
+            double bga = 0.0;
+            if (grad)
+                for (int e = 0; e < E; ++e)
+                    bga += fabs((b ? b[j * E + e] : 1.0) * (g ? g[i * E + e] : 1.0));
+            for (int c = 0; c < C; ++c) {
+                const double t = grad ? fabs(2.0 * inv_s2 * (x[i * D + c] - y[j * D + c]) * k) * bga
+                                      : fabs(k * (b ? b[j * E + c] : 1.0));
+                nsum_add(&cs[c], t * u);
+                if (deep) nsum_add(&ts[c], t);
+            }
+        }
+        for (int c = 0; c < C; ++c) {
+            cond[r * C + c] = nsum_get(&cs[c]);
+            tail[r * C + c] = nsum_get(&ts[c]);
+        }
+        free(cs);
+        free(ts);
     }
 }
 

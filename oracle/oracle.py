@@ -48,6 +48,8 @@ def _load():
             lib.oracle_lse.argtypes = [I64, I64, I32, F64, P, P, P, P, I64, P, P]
             lib.oracle_lse_cond.argtypes = [I64, I64, I32, F64, P, P, P, P, I64, P, P]
             lib.oracle_lse_cond.restype = None
+            lib.oracle_gauss_cond.argtypes = [I64, I64, I32, I32, F64, I32, P, P, P, P, P, I64, P, P]
+            lib.oracle_gauss_cond.restype = None
             lib.oracle_argkmin.argtypes = [I64, I64, I32, I32, P, P, P, I64, P, P]
             lib.oracle_sqdist_sum.argtypes = [I64, I64, I32, I32, P, P, P, P, I64, P, P]
             lib.oracle_softmax_grad.argtypes = [I64, I64, I32, F64, P, P, P, P, P, P, P, I64, P, P, P, P]
@@ -91,8 +93,9 @@ def _rows(rows):
     return r, int(r.shape[0])
 
 
-def gauss_sum(x, y, b=None, sigma=1.0, rows=None):
-    """O1.  Returns (a [R,E], denom [R,E]) in fp64."""
+def gauss_sum(x, y, b=None, sigma=1.0, rows=None, cond=False):
+    """O1.  Returns (a [R,E], denom [R,E]) in fp64.  cond=True also returns the R4c metric's
+    (cond [R,E], tail [R,E]) (oracle_gauss_cond)."""
     x = _f64(x); y = _f64(y)
     M, D = x.shape; N = y.shape[0]
     b = _f64(b)
@@ -102,11 +105,17 @@ def gauss_sum(x, y, b=None, sigma=1.0, rows=None):
     out = np.empty((R, E)); den = np.empty((R, E))
     _load().oracle_gauss_sum(M, N, D, E, float(sigma), _ptr(x), _ptr(y), _ptr(b), _ptr(r), nr,
                              _ptr(out), _ptr(den))
-    return out, den
+    if not cond:
+        return out, den
+    cc = np.empty((R, E)); tt = np.empty((R, E))
+    _load().oracle_gauss_cond(M, N, D, E, float(sigma), 0, _ptr(x), _ptr(y), _ptr(b), None,
+                              _ptr(r), nr, _ptr(cc), _ptr(tt))
+    return out, den, cc, tt
 
 
-def gauss_gradx(x, y, b=None, g=None, sigma=1.0, rows=None):
-    """O2.  Returns (G [R,D], denom [R,D]) in fp64."""
+def gauss_gradx(x, y, b=None, g=None, sigma=1.0, rows=None, cond=False):
+    """O2.  Returns (G [R,D], denom [R,D]) in fp64.  cond=True also returns the R4c metric's
+    (cond [R,D], tail [R,D]) (oracle_gauss_cond)."""
     x = _f64(x); y = _f64(y)
     M, D = x.shape; N = y.shape[0]
     b = _f64(b); g = _f64(g)
@@ -120,7 +129,12 @@ def gauss_gradx(x, y, b=None, g=None, sigma=1.0, rows=None):
     out = np.empty((R, D)); den = np.empty((R, D))
     _load().oracle_gauss_gradx(M, N, D, E, float(sigma), _ptr(x), _ptr(y), _ptr(b), _ptr(g),
                                _ptr(r), nr, _ptr(out), _ptr(den))
-    return out, den
+    if not cond:
+        return out, den
+    cc = np.empty((R, D)); tt = np.empty((R, D))
+    _load().oracle_gauss_cond(M, N, D, E, float(sigma), 1, _ptr(x), _ptr(y), _ptr(b), _ptr(g),
+                              _ptr(r), nr, _ptr(cc), _ptr(tt))
+    return out, den, cc, tt
 
 
 def lse(x, y, h=None, eps=1.0, rows=None, cond=False):

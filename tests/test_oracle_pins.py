@@ -372,3 +372,41 @@ def test_lse_conditioning_closed_forms():
     a, _, c = oracle.lse(x, y2, np.array([1.0, -1.0]), eps=0.1, cond=True)
     p = np.exp(np.array([1.0, -1.0]) - a[0])
     assert abs(c[0] - (p[0] * 1.0 + p[1] * 1.0)) < 1e-12
+
+
+def test_gauss_conditioning_by_bandwidth_derivative():
+    """oracle_gauss_cond (the R4c metric's cond, tail) against the oracle's own denominators on a
+    different route: S(lam) = sum_j |b_j| exp(-lam u_ij) is the O1 denominator at sigma/sqrt(lam),
+    so cond = -dS/dlam at lam = 1; the O2 denominator is lam A(lam), so cond = den - d den/dlam.
+    tail = the denominator restricted to the j with u log2(e) >= 100 (a y subset)."""
+    rng = np.random.default_rng(7)
+    x = rng.random((9, 3)) * 2.0
+    y = rng.random((40, 3)) * 2.0
+    b = rng.standard_normal((40, 2))
+    g = rng.standard_normal((9, 2))
+    sigma, h = 0.7, 1e-5
+    _, den, cond, tail = oracle.gauss_sum(x, y, b, sigma=sigma, cond=True)
+    Sp = oracle.gauss_sum(x, y, b, sigma=sigma / np.sqrt(1 + h))[1]
+    Sm = oracle.gauss_sum(x, y, b, sigma=sigma / np.sqrt(1 - h))[1]
+    np.testing.assert_allclose(cond, -(Sp - Sm) / (2 * h), rtol=1e-6)
+    assert np.all(tail == 0.0)                      # u <= 12/0.49 ~ 24 < 100 / log2(e)
+    _, dg, cg, tg = oracle.gauss_gradx(x, y, b, g, sigma=sigma, cond=True)
+    Ap = oracle.gauss_gradx(x, y, b, g, sigma=sigma / np.sqrt(1 + h))[1]
+    Am = oracle.gauss_gradx(x, y, b, g, sigma=sigma / np.sqrt(1 - h))[1]
+    np.testing.assert_allclose(cg, dg - (Ap - Am) / (2 * h), rtol=1e-6, atol=1e-12 * dg.max())
+    assert np.all(tg == 0.0)
+    # deep tail: y far enough that some u log2(e) >= 100 (u >= 69.3), the rest near
+    sig = 0.1
+    xn = x * 0.05
+    yf = np.concatenate([y * 0.05, 1.5 + y * 0.05], 0)   # 40 near (u <= 3), 40 at 470 <= u <= 675
+    bf = np.concatenate([b, b], 0)
+    _, den2, _, tail2 = oracle.gauss_sum(xn, yf, bf, sigma=sig, cond=True)
+    far = oracle.gauss_sum(xn, yf[40:], bf[40:], sigma=sig)[1]
+    assert np.all(far > 0) and np.all(tail2 < 1e-200 * den2)
+    np.testing.assert_array_equal(tail2, far)
+    _, _, _, tgf = oracle.gauss_gradx(xn, yf, bf, g, sigma=sig, cond=True)
+    np.testing.assert_array_equal(tgf, oracle.gauss_gradx(xn, yf[40:], bf[40:], g, sigma=sig)[1])
+    # moderately deep: one j at u log2(e) = 110 contributes exactly its term to tail and den
+    x1 = np.zeros((1, 1)); y1 = np.array([[np.sqrt(110 / 1.4426950408889634)]]); b1 = np.ones((1, 1))
+    _, d1, c1, t1 = oracle.gauss_sum(x1, y1, b1, sigma=1.0, cond=True)
+    assert t1[0, 0] == d1[0, 0] > 0 and np.isclose(c1[0, 0], d1[0, 0] * 110 / 1.4426950408889634)
