@@ -26,7 +26,7 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
     float *sm = reinterpret_cast<float *>(pack_smem4);
     const float NEG_INF = -INFINITY;
     const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
-    const bool raw = kind == PACK_GAUSS_AUTO_RAW;           // direct records: -y instead of -s y
+    const bool raw = kind == PACK_GAUSS_AUTO_RAW;           // + the b y' slots (gradient modes)
     const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
     const int EB = (gauss || sumk) ? (b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);   // staged b / h columns
     float *ys = sm;                           // [512][D]
@@ -59,7 +59,7 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                         r = valid ? s * (v - geo.c[d]) : 0.0f;        // y' = s (y - c)
                         w += (double)r * (double)r;
                     } else {
-                        r = valid ? (raw ? -v : -(s * v)) : 0.0f;
+                        r = valid ? -v : 0.0f;              // direct: raw -y (R18d, R18e)
                     }
                     rec[2 * d + h] = r;
                 }
@@ -181,7 +181,7 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
                     r = valid ? s * (v - geo.c[d]) : 0.0f;
                     w += (double)r * (double)r;
                 } else {
-                    r = valid ? (kind == PACK_GAUSS_AUTO_RAW ? -v : -(s * v)) : 0.0f;
+                    r = valid ? (gauto ? -v : -(s * v)) : 0.0f;   // Gaussian direct: raw -y
                 }
                 rec[2 * d + h] = r;
             }

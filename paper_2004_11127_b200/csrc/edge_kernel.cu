@@ -12,7 +12,8 @@
 //     (the bytes in flight per SM, not the thread count, set the achieved HBM bandwidth);
 //   * a thread evaluates its rows from shared memory in the direct form (no bounding-box pass
 //     over x, which would be a second full read) and stores a with coalesced writes.
-// The j-records are the PACK_GAUSS_AUTO direct records (-s y_j pairs, w slot, b_j pairs).
+// The j-records are the PACK_GAUSS_AUTO direct records (raw -y_j pairs, w slot, b_j pairs;
+// the kernel scales |x - y|^2 by s^2 as sum_body.cuh's direct form, reading R18e).
 #include <math.h>
 
 #include <algorithm>
@@ -46,6 +47,7 @@ sum_edge_kernel(const float *__restrict__ x, const float *__restrict__ J, int np
     const int64_t ntiles = (M + kRowsPerTile - 1) / kRowsPerTile;
     const int64_t nfull = M / kRowsPerTile;           // tiles copied whole (16-byte multiple)
     constexpr uint32_t kTileBytes = kRowsPerTile * D * 4;
+    const float2 negs2 = dup2(-(s * s));               // as sum_body.cuh's direct form
 
     if (threadIdx.x == 0) {
         for (int k = 0; k < kStages; ++k) mbar_init(&full[k], 1);
@@ -75,13 +77,13 @@ sum_edge_kernel(const float *__restrict__ x, const float *__restrict__ J, int np
 #pragma unroll
             for (int r = 0; r < kRows; ++r)
 #pragma unroll
-                for (int d = 0; d < D; ++d) xr[r][d] = s * xs[(r * kThreads + threadIdx.x) * D + d];
+                for (int d = 0; d < D; ++d) xr[r][d] = xs[(r * kThreads + threadIdx.x) * D + d];
         } else {
 #pragma unroll
             for (int r = 0; r < kRows; ++r) {
                 const int64_t i = row0 + r * kThreads + threadIdx.x;
 #pragma unroll
-                for (int d = 0; d < D; ++d) xr[r][d] = i < M ? s * __ldg(x + i * D + d) : 0.0f;
+                for (int d = 0; d < D; ++d) xr[r][d] = i < M ? __ldg(x + i * D + d) : 0.0f;
             }
         }
         __syncthreads();                                  // every thread is done with stage st
@@ -109,9 +111,10 @@ sum_edge_kernel(const float *__restrict__ x, const float *__restrict__ J, int np
 #pragma unroll
                 for (int d = 1; d < D; ++d) {
                     dd = add2(dup2(xr[r][d]), ny[d]);
-                    q = fma2(dd, dd, q);                  // |x' - y'|^2 (direct form)
+                    q = fma2(dd, dd, q);                  // |x - y|^2 (raw differences, R18e)
                 }
-                const float2 e = make_float2(ex2(-q.x), ex2(-q.y));
+                const float2 t = mul2(q, negs2);                    // -s^2 |x - y|^2
+                const float2 e = make_float2(ex2(t.x), ex2(t.y));
                 acc[r] = fma2(e, bv, acc[r]);
             }
         }

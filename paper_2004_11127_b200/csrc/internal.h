@@ -59,9 +59,9 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 // (padding up to npairs) hold y = 0 and b = 0 (Sum), or y = +inf and h = -inf (LSE, ArgKMin),
 // which contribute nothing.
 // PACK_GAUSS_AUTO (Gaussian Sum): decodes the bounding box `geo` (geo.cuh) and writes either the
-// expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-s y, 0, b).
-// PACK_GAUSS_AUTO_RAW (gradient modes): as PACK_GAUSS_AUTO, but the direct records hold -y (raw),
-// so the kernel forms raw differences x - y (reading R18d).
+// expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-y raw, 0, b): the kernel
+// forms raw differences x - y and scales their squared norm by s^2 (readings R18d, R18e).
+// PACK_GAUSS_AUTO_RAW (gradient modes): as PACK_GAUSS_AUTO, plus the b y' slots (kGradBY).
 // PACK_GAUSS_DIRECT: the direct records when the box rules the expanded form out, else nothing
 // (the tensor-core kernel, gauss_tc.cu, takes the expanded case).
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,

@@ -88,7 +88,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
     constexpr bool POLY = kPolyShare && XP && R == 4;
     constexpr int HH = SMM ? 1 : (MODE == 1 || MODE == 2) ? GENRED_GRAD_HH : GENRED_SUM_HH;   // record pairs per iteration
-    constexpr bool RAWD = !XP && (MODE == 1 || MODE == 2);   // direct gradient: raw differences
+    constexpr bool RAWD = !XP && Cfg::EXP;           // direct Gaussian modes: raw differences
     const float2 negs2 = dup2(-(p.s * p.s));
     const int ct = threadIdx.x;
     float xr[R][D];
@@ -107,9 +107,11 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
                 xsq[r] += (double)xs * (double)xs;
                 xr[r][d] = 2.0f * xs;                                      // exact doubling
             } else {
-                // direct form: pre-scaled s x for the Sum; RAW x for the gradient modes, whose
-                // linear factor (x - y) must come from a raw fp32 difference (exact for nearby
-                // coordinates, Sterbenz) -- s x - s y loses it when x ~ y (R18d)
+                // direct Gaussian form: RAW x.  The difference x - y is then exact for nearby
+                // coordinates (Sterbenz) and rounded relative to |x - y| otherwise; s x - s y
+                // would round each term at ulp(s |x|), which loses the gradient's linear factor
+                // when x ~ y (R18d) and the exponent of clouds far from the origin or
+                // wide against sigma (R18e).  |x - y|^2 is scaled by s^2 afterwards.
                 xr[r][d] = RAWD ? v : p.s * v;
             }
         }

@@ -982,3 +982,40 @@ def test_randomized_large_n_against_oracle(G, seed):
         d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
         od, oj = oracle.argkmin(x, y, K + 1, rows=rows)
         argk_check(host(d)[rows], host(j)[rows], od, oj, K, what=f"large seed {seed} argk")
+
+
+@pytest.mark.parametrize("seed", list(range(int(os.environ.get("GENRED_RANDOM_HARD_SEEDS", "24")))))
+def test_randomized_hard_inputs(G, seed):
+    """Seeded random cases on awkward data: far offsets, duplicated points (x rows inside y),
+    clustered clouds, tiny and wide bandwidths, signed signals."""
+    rng = np.random.default_rng(90_000 + seed)
+    D = int(rng.integers(1, 5))
+    M = int(rng.choice([1, 17, 700, 3000])); N = int(rng.choice([3, 200, 5000, 40_000]))
+    off = float(rng.choice([0.0, 100.0, -1000.0]))
+    spread = float(rng.choice([1e-3, 1.0, 30.0]))
+    x = (off + spread * rng.random((M, D))).astype(np.float32)
+    y = (off + spread * rng.random((N, D))).astype(np.float32)
+    k = min(M, N) // 2
+    y[:k] = x[:k]                                              # exact duplicates
+    red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin"]))
+    tag = f"hard seed {seed} (D={D} M={M} N={N} off={off} spread={spread})"
+    if red in ("gauss", "gauss_sum_gradx"):
+        b = rng.standard_normal((N, 1)).astype(np.float32)
+        sigma = float(spread * rng.choice([0.05, 0.5, 5.0]))
+        res = G.eval(red, "sum", dev(x), dev(y), dev(b), scale=sigma)
+        res = res if isinstance(res, tuple) else (res,)
+        o, den, C, T = oracle.gauss_sum(x, y, b, sigma=sigma, cond=True)
+        assert_sum_parity(host(res[0]), o, den, what=f"{tag} sum", cond=(C, T), D=D)
+        if red == "gauss_sum_gradx":
+            og, deng, Cg, Tg = oracle.gauss_gradx(x, y, b, None, sigma=sigma, cond=True)
+            assert_sum_parity(host(res[1]), og, deng, what=f"{tag} grad", cond=(Cg, Tg), D=D)
+    elif red == "lse":
+        eps = float(spread ** 2 * rng.choice([0.01, 0.3]))
+        a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=eps, out_dtype="float64")
+        o, _, cond = oracle.lse(x, y, None, eps=eps, cond=True)
+        assert_lse_parity(host(a), o, rel=True, cond=cond, D=D, what=f"{tag} lse")
+    else:
+        K = int(rng.choice([1, 4, 10]))
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+        od, oj = oracle.argkmin(x, y, K + 1)
+        argk_check(host(d), host(j), od, oj, K, what=f"{tag} argk")
