@@ -995,27 +995,37 @@ def test_randomized_hard_inputs(G, seed):
     spread = float(rng.choice([1e-3, 1.0, 30.0]))
     x = (off + spread * rng.random((M, D))).astype(np.float32)
     y = (off + spread * rng.random((N, D))).astype(np.float32)
+    if rng.random() < 0.33:                                    # clustered: 5 tight blobs
+        cen = off + spread * rng.random((5, D))
+        x = (cen[rng.integers(0, 5, M)] + 1e-3 * spread * rng.standard_normal((M, D))).astype(np.float32)
+        y = (cen[rng.integers(0, 5, N)] + 1e-3 * spread * rng.standard_normal((N, D))).astype(np.float32)
     k = min(M, N) // 2
     y[:k] = x[:k]                                              # exact duplicates
     red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin"]))
-    tag = f"hard seed {seed} (D={D} M={M} N={N} off={off} spread={spread})"
+    split = int(rng.choice([0, 0, 3]))
+    E = int(rng.choice([1, 1, 2, 3]))
+    tag = f"hard seed {seed} (D={D} M={M} N={N} E={E} off={off} spread={spread} split={split})"
     if red in ("gauss", "gauss_sum_gradx"):
-        b = rng.standard_normal((N, 1)).astype(np.float32)
+        b = rng.standard_normal((N, E)).astype(np.float32)
+        g = rng.standard_normal((M, E)).astype(np.float32) if E > 1 else None
         sigma = float(spread * rng.choice([0.05, 0.5, 5.0]))
-        res = G.eval(red, "sum", dev(x), dev(y), dev(b), scale=sigma)
+        args = (dev(x), dev(y), dev(b)) + ((dev(g),) if (red != "gauss" and g is not None) else ())
+        res = G.eval(red, "sum", *args, scale=sigma, split_j=split)
         res = res if isinstance(res, tuple) else (res,)
         o, den, C, T = oracle.gauss_sum(x, y, b, sigma=sigma, cond=True)
         assert_sum_parity(host(res[0]), o, den, what=f"{tag} sum", cond=(C, T), D=D)
         if red == "gauss_sum_gradx":
-            og, deng, Cg, Tg = oracle.gauss_gradx(x, y, b, None, sigma=sigma, cond=True)
+            og, deng, Cg, Tg = oracle.gauss_gradx(x, y, b, g, sigma=sigma, cond=True)
             assert_sum_parity(host(res[1]), og, deng, what=f"{tag} grad", cond=(Cg, Tg), D=D)
     elif red == "lse":
         eps = float(spread ** 2 * rng.choice([0.01, 0.3]))
-        a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=eps, out_dtype="float64")
-        o, _, cond = oracle.lse(x, y, None, eps=eps, cond=True)
+        h = (rng.standard_normal(N) * 3).astype(np.float32) if rng.random() < 0.5 else None
+        a = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=eps,
+                   split_j=split, out_dtype="float64")
+        o, _, cond = oracle.lse(x, y, h, eps=eps, cond=True)
         assert_lse_parity(host(a), o, rel=True, cond=cond, D=D, what=f"{tag} lse")
     else:
         K = int(rng.choice([1, 4, 10]))
-        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K)
+        d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)
         od, oj = oracle.argkmin(x, y, K + 1)
         argk_check(host(d), host(j), od, oj, K, what=f"{tag} argk")
