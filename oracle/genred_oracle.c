@@ -20,6 +20,7 @@
  *   oracle_lse          O3  F = -|x_i-y_j|^2/eps + h_j ; a_i = m_i + log sum_j exp(F_ij - m_i)
  *   oracle_lse_cond         the metric's conditioning of O3 (reading R6b)
  *   oracle_gauss_cond       the metric's conditioning of O1 / O2 (reading R4c)
+ *   oracle_softmax_cond     the metric's conditioning of O6 (reading R4c)
  *                                                                          PAPER.md:85, 134 (R5)
  *   oracle_argkmin      O4  K smallest (|x_i-y_j|^2, j) in lexicographic order   PAPER.md:85, 134 (R7-R9)
  *   oracle_sqdist_sum   O5  sum_j |x_i-y_j|^2 b_j  (test combination)
@@ -344,5 +345,50 @@ void oracle_softmax_grad(int64_t M, int64_t N, int D, double eps,
         }
         free(g);
         free(gd);
+    }
+}
+
+/* Conditioning of O6 for the error metric (reading R4c, as oracle_gauss_cond): with the exponent's
+ * parts u_ij = |x_i - y_j|^2/eps, alpha_i, beta_j (each rounded in fp32 by a few ulps) and the
+ * elementary terms of S_i (w_ij = sig_j p_ij) and G_i[d] (c_i w_ij (-2/eps)(x_i - y_j)_d):
+ *   cond = sum_j |term_ij| (u_ij + |alpha_i| + |beta_j|),
+ *   tail = sum_j |term_ij| [(-u_ij + alpha_i + beta_j) log2(e) <= -100]. */
+void oracle_softmax_cond(int64_t M, int64_t N, int D, double eps,
+                         const double *x, const double *y, const double *alpha, const double *beta,
+                         const double *sig, const double *coef,
+                         const int64_t *rows, int64_t nrows,
+                         double *cond_sum, double *cond_grad, double *tail_sum, double *tail_grad) {
+    int64_t R = rows ? nrows : M;
+#pragma omp parallel for schedule(dynamic, 1)
+    for (int64_t r = 0; r < R; ++r) {
+        int64_t i = row_of(rows, r);
+        nsum cs = {0.0, 0.0}, ts = {0.0, 0.0};
+        nsum *cg = calloc((size_t)D, sizeof(nsum));
+        nsum *tg = calloc((size_t)D, sizeof(nsum));
+        double c = coef ? coef[i] : 1.0;
+        double ai = alpha ? alpha[i] : 0.0;
+        for (int64_t j = 0; j < N; ++j) {
+            const double u = sqdist(x + i * D, y + j * D, D) / eps;
+            const double bj = beta ? beta[j] : 0.0;
+            const double z = -u + ai + bj;
+            const double mag = u + fabs(ai) + fabs(bj);
+            const int deep = z * 1.4426950408889634 <= -100.0;
+            const double w = fabs((sig ? sig[j] : 1.0) * exp(z));
+            nsum_add(&cs, w * mag);
+            if (deep) nsum_add(&ts, w);
+            for (int d = 0; d < D; ++d) {
+                const double t = fabs(c * w * (-2.0 / eps) * (x[i * D + d] - y[j * D + d]));
+                nsum_add(&cg[d], t * mag);
+                if (deep) nsum_add(&tg[d], t);
+            }
+        }
+        cond_sum[r] = nsum_get(&cs);
+        tail_sum[r] = nsum_get(&ts);
+        for (int d = 0; d < D; ++d) {
+            cond_grad[r * D + d] = nsum_get(&cg[d]);
+            tail_grad[r * D + d] = nsum_get(&tg[d]);
+        }
+        free(cg);
+        free(tg);
     }
 }

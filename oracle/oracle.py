@@ -50,6 +50,8 @@ def _load():
             lib.oracle_lse_cond.restype = None
             lib.oracle_gauss_cond.argtypes = [I64, I64, I32, I32, F64, I32, P, P, P, P, P, I64, P, P]
             lib.oracle_gauss_cond.restype = None
+            lib.oracle_softmax_cond.argtypes = [I64, I64, I32, F64, P, P, P, P, P, P, P, I64, P, P, P, P]
+            lib.oracle_softmax_cond.restype = None
             lib.oracle_argkmin.argtypes = [I64, I64, I32, I32, P, P, P, I64, P, P]
             lib.oracle_sqdist_sum.argtypes = [I64, I64, I32, I32, P, P, P, P, I64, P, P]
             lib.oracle_softmax_grad.argtypes = [I64, I64, I32, F64, P, P, P, P, P, P, P, I64, P, P, P, P]
@@ -181,9 +183,10 @@ def sqdist_sum(x, y, b=None, rows=None):
     return out, den
 
 
-def softmax_grad(x, y, alpha=None, beta=None, sig=None, coef=None, eps=1.0, rows=None):
+def softmax_grad(x, y, alpha=None, beta=None, sig=None, coef=None, eps=1.0, rows=None, cond=False):
     """O6.  p_ij = exp(-|x_i-y_j|^2/eps + alpha_i + beta_j); returns (S [R], G [R,D], denS, denG)
-    with S_i = sum_j sig_j p_ij and G_i = coef_i sum_j sig_j p_ij (-2/eps)(x_i - y_j)."""
+    with S_i = sum_j sig_j p_ij and G_i = coef_i sum_j sig_j p_ij (-2/eps)(x_i - y_j).
+    cond=True appends the R4c metric's (condS, condG, tailS, tailG) (oracle_softmax_cond)."""
     x = _f64(x); y = _f64(y)
     M, D = x.shape; N = y.shape[0]
     a, b_, s_, c_ = (None if v is None else _f64(v).reshape(-1) for v in (alpha, beta, sig, coef))
@@ -192,4 +195,9 @@ def softmax_grad(x, y, alpha=None, beta=None, sig=None, coef=None, eps=1.0, rows
     S = np.empty(R); G = np.empty((R, D)); dS = np.empty(R); dG = np.empty((R, D))
     _load().oracle_softmax_grad(M, N, D, float(eps), _ptr(x), _ptr(y), _ptr(a), _ptr(b_), _ptr(s_),
                                 _ptr(c_), _ptr(r), nr, _ptr(S), _ptr(G), _ptr(dS), _ptr(dG))
-    return S, G, dS, dG
+    if not cond:
+        return S, G, dS, dG
+    cS = np.empty(R); cG = np.empty((R, D)); tS = np.empty(R); tG = np.empty((R, D))
+    _load().oracle_softmax_cond(M, N, D, float(eps), _ptr(x), _ptr(y), _ptr(a), _ptr(b_), _ptr(s_),
+                                _ptr(c_), _ptr(r), nr, _ptr(cS), _ptr(cG), _ptr(tS), _ptr(tG))
+    return S, G, dS, dG, cS, cG, tS, tG

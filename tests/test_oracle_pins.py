@@ -410,3 +410,29 @@ def test_gauss_conditioning_by_bandwidth_derivative():
     x1 = np.zeros((1, 1)); y1 = np.array([[np.sqrt(110 / 1.4426950408889634)]]); b1 = np.ones((1, 1))
     _, d1, c1, t1 = oracle.gauss_sum(x1, y1, b1, sigma=1.0, cond=True)
     assert t1[0, 0] == d1[0, 0] > 0 and np.isclose(c1[0, 0], d1[0, 0] * 110 / 1.4426950408889634)
+
+
+def test_softmax_conditioning_identities():
+    """oracle_softmax_cond (R4c for O6) on routes other than its own loop: with alpha = beta = 0,
+    condS = -dS/dlam and condG = denG - d denG/dlam for eps -> eps/lam (O6's denominators); a
+    constant alpha_i = c > 0 multiplies every term by e^c and adds c to each magnitude, so
+    cond(c) = e^c (cond(0) + c den(0)); tail = the denominators over the deep-tail y subset."""
+    rng = np.random.default_rng(8)
+    x = rng.random((7, 2)); y = rng.random((30, 2)); sig = rng.standard_normal(30); coef = rng.standard_normal(7)
+    eps, h = 0.3, 1e-5
+    S, G, dS, dG, cS, cG, tS, tG = oracle.softmax_grad(x, y, sig=sig, coef=coef, eps=eps, cond=True)
+    Sp, _, dSp, dGp = oracle.softmax_grad(x, y, sig=sig, coef=coef, eps=eps / (1 + h))
+    Sm, _, dSm, dGm = oracle.softmax_grad(x, y, sig=sig, coef=coef, eps=eps / (1 - h))
+    np.testing.assert_allclose(cS, -(dSp - dSm) / (2 * h), rtol=1e-6)
+    np.testing.assert_allclose(cG, dG - (dGp - dGm) / (2 * h), rtol=1e-6, atol=1e-12 * dG.max())
+    assert np.all(tS == 0) and np.all(tG == 0)
+    c = 0.75
+    _, _, dS1, dG1, cS1, cG1, _, _ = oracle.softmax_grad(x, y, alpha=np.full(7, c), sig=sig, coef=coef,
+                                                         eps=eps, cond=True)
+    np.testing.assert_allclose(cS1, np.exp(c) * (cS + c * dS), rtol=1e-12)
+    np.testing.assert_allclose(cG1, np.exp(c) * (cG + c * dG), rtol=1e-12)
+    beta = np.concatenate([np.zeros(15), np.full(15, -80.0)])      # second half: z log2 e <= -100
+    r = oracle.softmax_grad(x, y, beta=beta, sig=sig, coef=coef, eps=eps, cond=True)
+    sub = oracle.softmax_grad(x, y[15:], beta=beta[15:], sig=sig[15:], coef=coef, eps=eps)
+    np.testing.assert_array_equal(r[6], sub[2])
+    np.testing.assert_array_equal(r[7], sub[3])
