@@ -1001,7 +1001,7 @@ def test_randomized_hard_inputs(G, seed):
         y = (cen[rng.integers(0, 5, N)] + 1e-3 * spread * rng.standard_normal((N, D))).astype(np.float32)
     k = min(M, N) // 2
     y[:k] = x[:k]                                              # exact duplicates
-    red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin"]))
+    red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin", "lse_grad"]))
     split = int(rng.choice([0, 0, 3]))
     E = int(rng.choice([1, 1, 2, 3]))
     tag = f"hard seed {seed} (D={D} M={M} N={N} E={E} off={off} spread={spread} split={split})"
@@ -1024,6 +1024,18 @@ def test_randomized_hard_inputs(G, seed):
                    split_j=split, out_dtype="float64")
         o, _, cond = oracle.lse(x, y, h, eps=eps, cond=True)
         assert_lse_parity(host(a), o, rel=True, cond=cond, D=D, what=f"{tag} lse")
+    elif red == "lse_grad":                                     # the LSE backward (softmax) kernel
+        eps = float(spread ** 2 * rng.choice([0.01, 0.3]))
+        h = (rng.standard_normal(N) * 3).astype(np.float32)
+        gg = rng.standard_normal(M).astype(np.float32)
+        a, _ = oracle.lse(x, y, h, eps=eps)
+        S, gx = G.eval("lse_grad", "sum", dev(x), dev(y), None, dev(gg), scale=eps,
+                       out_dtype="float64", row_shift=dev(-a), col_shift=dev(h.astype(np.float64)),
+                       split_j=split)
+        oS, oG, dS, dG, cS, cG, tS, tG = oracle.softmax_grad(x, y, alpha=-a, beta=h, coef=gg, eps=eps,
+                                                             cond=True)
+        assert_sum_parity(host(S), oS, dS, what=f"{tag} softmax sum", cond=(cS, tS), D=D)
+        assert_sum_parity(host(gx), oG, dG, what=f"{tag} lse grad x", cond=(cG, tG), D=D)
     else:
         K = int(rng.choice([1, 4, 10]))
         d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)
