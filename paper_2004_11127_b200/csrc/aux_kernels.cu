@@ -21,8 +21,11 @@ namespace genred {
 __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__restrict__ y,
                                                    const float *__restrict__ b, int64_t N, int D, int E,
                                                    float s, double hscale, int64_t npairs, int RS,
-                                                   float *__restrict__ J, const uint32_t *geo_enc) {
+                                                   float *__restrict__ J, const uint32_t *geo_enc,
+                                                   const float *__restrict__ bx = nullptr, int64_t bM = 0,
+                                                   uint32_t *geo_out = nullptr) {
     extern __shared__ float4 pack_smem4[];
+    __shared__ uint32_t sgeo[32];
     float *sm = reinterpret_cast<float *>(pack_smem4);
     const float NEG_INF = -INFINITY;
     const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
@@ -33,6 +36,71 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
     float *bs = ys + kTileJ * D;              // [512][EB]
     float *outs = bs + kTileJ * EB;           // [256][RS]  (16-byte aligned: 512 (D + EB) floats)
     Geo geo{};
+    if (geo_out) {
+        // fused bounding box (small problems): the same encoded minima / inverted maxima that
+        // bbox_kernel reduces, computed by every block over all of y (words 0..15) and x (16..31)
+        __shared__ float blo[2][8][8], bhi[2][8][8];
+        // both clouds in one loop, 4 rows of each per thread and iteration with every load issued
+        // before the min/max: one memory round trip per 1024 rows instead of one per 256
+        float lo[2][8], hi[2][8];
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int d = 0; d < 8; ++d) { lo[q][d] = INFINITY; hi[q][d] = -INFINITY; }
+        const int64_t rmax = max(N, bM);
+        for (int64_t r0 = threadIdx.x; r0 < rmax; r0 += 4 * (int64_t)blockDim.x) {
+            float v[2][4][8];
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int64_t r = r0 + u * (int64_t)blockDim.x;
+                    const bool ok = r < (q == 0 ? N : bM);
+                    const float *src = q == 0 ? y : bx;
+#pragma unroll
+                    for (int d = 0; d < 8; ++d)
+                        v[q][u][d] = (d < D && ok) ? __ldg(src + r * D + d) : NAN;   // NaN: ignored by fminf/fmaxf
+                }
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+#pragma unroll
+                    for (int d = 0; d < 8; ++d) {
+                        lo[q][d] = fminf(lo[q][d], v[q][u][d]);
+                        hi[q][d] = fmaxf(hi[q][d], v[q][u][d]);
+                    }
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q)
+#pragma unroll
+            for (int d = 0; d < 8; ++d)
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    lo[q][d] = fminf(lo[q][d], __shfl_xor_sync(0xffffffffu, lo[q][d], o));
+                    hi[q][d] = fmaxf(hi[q][d], __shfl_xor_sync(0xffffffffu, hi[q][d], o));
+                }
+        const int warp = threadIdx.x >> 5;
+        if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+            for (int q = 0; q < 2; ++q)
+#pragma unroll
+                for (int d = 0; d < 8; ++d) { blo[q][warp][d] = lo[q][d]; bhi[q][warp][d] = hi[q][d]; }
+        }
+        __syncthreads();
+        if (threadIdx.x < 16) {
+            const int q = threadIdx.x >> 3, d = threadIdx.x & 7;
+            float l = blo[q][0][d], h = bhi[q][0][d];
+            for (int w = 1; w < (int)(blockDim.x >> 5); ++w) { l = fminf(l, blo[q][w][d]); h = fmaxf(h, bhi[q][w][d]); }
+            // an empty side leaves (+inf, -inf): decodes as non-finite -> the direct form,
+            // as the 0xff-initialised words of the bbox_kernel path do
+            sgeo[16 * q + d] = f2ord(l);
+            sgeo[16 * q + 8 + d] = ~f2ord(h);
+        }
+        __syncthreads();
+        if (blockIdx.x == 0 && threadIdx.x < 32) geo_out[threadIdx.x] = sgeo[threadIdx.x];
+        geo_enc = sgeo;
+    }
     if (gauss) {
         geo = geo_decode(geo_enc, D, s);      // expanded or direct per the bounding box
         if (kind == PACK_GAUSS_DIRECT && geo.expanded) return;   // gauss_tc.cu takes this call
@@ -129,6 +197,23 @@ cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int
     if (blocks > 148 * 8) blocks = 148 * 8;
     if (blocks < 1) blocks = 1;
     pack_kernel<<<(unsigned)blocks, 256, smem, st>>>(kind, y, b, N, D, E, s, hscale, npairs, RS, J, geo);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_pack_boxed(int kind, const float *y, const float *b, int64_t N, int D, int E,
+                              float s, int64_t npairs, float *J, const float *x, int64_t M,
+                              uint32_t *geo, cudaStream_t st) {
+    const int RS = pack_record_stride(kind, D, E);
+    const int smem = pack_smem_bytes(kind, D, E, RS, b != nullptr);
+    if (smem > 48 * 1024) {
+        const cudaError_t e = smem_opt_in((const void *)pack_kernel, 96 * 1024);
+        if (e != cudaSuccess) return e;
+    }
+    int64_t blocks = (npairs + 255) / 256;
+    if (blocks > 148 * 8) blocks = 148 * 8;
+    if (blocks < 1) blocks = 1;
+    pack_kernel<<<(unsigned)blocks, 256, smem, st>>>(kind, y, b, N, D, E, s, 0.0, npairs, RS, J,
+                                                      nullptr, x, M, geo);
     return cudaGetLastError();
 }
 

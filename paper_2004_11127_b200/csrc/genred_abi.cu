@@ -553,7 +553,9 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // direct form costs nothing and the bounding-box pass over y (a full read of y) is skipped.
         const bool no_box = tiny_n || (M <= kDirectMaxM && !tc);
         if (no_box) geo = nullptr;
-        if (mode != 3 && !no_box) {
+        // small problems: the box is reduced inside the pack kernel (one launch fewer)
+        const bool boxed_pack = mode != 3 && !no_box && !tc && std::max(M, N) <= kFusedBoxMax;
+        if (mode != 3 && !no_box && !boxed_pack) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
@@ -572,7 +574,8 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             if (e != cudaSuccess) return cuda_fail(ctx, e, "tensor-core Gaussian sum");
             kernels += tk;
         }
-        e = launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
+        e = boxed_pack ? launch_pack_boxed(pk, a->y, a->b, N, D, E, sc, npairs, J, a->x, M, geo, st)
+                       : launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         if (tiny_n && mode == 0 && E == 1 && D <= 4 && N <= sum_edge_max_n() &&
             ((uintptr_t)a->x & 15) == 0) {

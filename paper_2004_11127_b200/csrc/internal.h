@@ -67,6 +67,13 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
                         float s, double hscale, int64_t npairs, float *J, cudaStream_t st,
                         const uint32_t *geo = nullptr);
+// Small problems (max(M, N) <= kFusedBoxMax): pack with the bounding box reduced inside the pack
+// kernel (every block reduces the whole of x and y, block 0 stores geo), replacing the memset +
+// bbox_kernel pair by nothing: one launch fewer on the latency-bound C1 path.
+constexpr int64_t kFusedBoxMax = 4096;
+cudaError_t launch_pack_boxed(int kind, const float *y, const float *b, int64_t N, int D, int E,
+                              float s, int64_t npairs, float *J, const float *x, int64_t M,
+                              uint32_t *geo, cudaStream_t st);
 // Per-coordinate bounding boxes of y (N x D) and x (M x D) into geo[32] (encoded, geo.cuh).
 cudaError_t launch_bbox(const float *x, int64_t M, const float *y, int64_t N, int D, uint32_t *geo,
                         cudaStream_t st);
