@@ -38,6 +38,8 @@ struct genred_ctx {
     bool gauss_tc = false;                                     // GENRED_GAUSS_TC=1 enables (opt-in)
     int geo_D = 0;
     float geo_s = 0.f;
+    unsigned *tile_done = nullptr;                             // split-merge arrival counters (zero at rest)
+    int64_t tile_done_cap = 0;
     bool profiling = false;
     std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
     int nprof = 0;
@@ -238,6 +240,21 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
         pl.split = (int)((pl.ntiles + pl.tiles_per_split - 1) / pl.tiles_per_split);
     }
     return pl;
+}
+
+// Per-row-tile arrival counters of the in-kernel split merge: zeroed once when allocated; every
+// merging CTA resets its counter, so they are zero again whenever the stream is idle.
+genred_status ensure_tile_done(genred_ctx *ctx, int64_t n) {
+    if (n <= ctx->tile_done_cap) return GENRED_OK;
+    const int64_t cap = std::max<int64_t>(n, 1024);
+    if (ctx->tile_done) { cudaFree(ctx->tile_done); ctx->tile_done = nullptr; ctx->tile_done_cap = 0; }
+    if (cudaMalloc(&ctx->tile_done, cap * sizeof(unsigned)) != cudaSuccess ||
+        cudaMemset(ctx->tile_done, 0, cap * sizeof(unsigned)) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(ctx, GENRED_E_NOMEM, "split-merge counter allocation failed");
+    }
+    ctx->tile_done_cap = cap;
+    return GENRED_OK;
 }
 
 genred_status ensure(genred_ctx *ctx, void **buf, size_t *cap, size_t need) {
@@ -599,13 +616,23 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
         L.direct_only = tc ? 1 : 0;
+        // Few partials per row tile: the last CTA of each row tile merges them (no finalize
+        // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.
+        const int64_t tile_rows = (int64_t)kConsumerWarps * 32 * pl.R;
+        const bool fused_merge = pl.split > 1 && !smm && !tc &&
+                                 std::min<int64_t>(tile_rows, M) * C * pl.split <= 16384;
+        if (fused_merge) {
+            s = ensure_tile_done(ctx, pl.itiles);
+            if (s != GENRED_OK) return s;
+            L.tile_done = ctx->tile_done;
+        }
         int sctas = 0;
         if (!tc) prof_event(ctx, true, st);
         e = smm ? launch_sum_smm(L, st, &sctas) : launch_sum(L, st, &sctas);
         if (!tc) prof_event(ctx, false, st);
         if (!tc) ctas = sctas;
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
-        if (pl.split > 1) {
+        if (pl.split > 1 && !fused_merge) {
             const int cols_sum = (mode == 1) ? 0 : E;
             e = launch_sum_finalize(part, pl.split, M, C, cols_sum, a->g, E, 1.0, scale_grad, mode,
                                     a->out, out_f64, a->out_grad, st);
@@ -833,6 +860,7 @@ void genred_destroy(genred_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->stage) cudaFree(ctx->stage);
+    if (ctx->tile_done) cudaFree(ctx->tile_done);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     cudaSetDevice(prev);
     delete ctx;

@@ -113,6 +113,7 @@ struct SumLaunch {
     const RangeUnit *units;   // block-sparse ranges (device), or nullptr
     int64_t n_units;
     int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
+    unsigned *tile_done = nullptr;  // split > 1: zeroed per-row-tile counters -> merge in the kernel
     int num_sms = 148;        // persistent grid: at most num_sms x occupancy CTAs
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);

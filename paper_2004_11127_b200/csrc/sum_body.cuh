@@ -64,6 +64,8 @@ struct SumParams {
     const RangeUnit *units;   // block-sparse ranges: one unit per (cluster, row tile)
     int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
     int64_t n_work;           // work units; the persistent grid walks w = blockIdx.x, + gridDim.x, ...
+    unsigned *tile_done;      // split > 1, row tiles only: per-row-tile arrival counters (all zero
+                              // between calls); the last CTA of a row tile merges its partials
 };
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
@@ -364,6 +366,46 @@ constexpr int sum_min_blocks() {
     return 2;
 }
 
+// Split-j merge folded into the pair-loop kernel: the CTA that finishes a
+// row tile last (arrival counter, release/acquire through __threadfence) sums the tile's S
+// partials in split order 0..S-1 -- the order and arithmetic of sum_finalize_kernel, so the
+// result is bitwise that of the two-kernel path -- and resets the counter for the next call.
+template <int MODE, int D, int E, int R>
+__device__ __forceinline__ void sum_tile_merge(const SumParams &p, int64_t itile, int64_t row0, int64_t row_end) {
+    using Cfg = SumCfg<MODE, D, E>;
+    constexpr int NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C;
+    __shared__ int s_last;
+    __syncthreads();                                   // every thread's partials are stored
+    if (threadIdx.x == 0) {
+        __threadfence();
+        const unsigned prev = atomicAdd(p.tile_done + itile, 1u);
+        s_last = prev == (unsigned)(p.split - 1);
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();                                   // acquire: the other CTAs' partials
+    const int64_t rows = min(row_end, row0 + (int64_t)(kConsumerWarps * 32 * R)) - row0;
+    for (int64_t t = threadIdx.x; t < rows * C; t += blockDim.x) {
+        const int64_t i = row0 + t / C;
+        const int c = (int)(t % C);
+        double acc = 0.0;
+        for (int q = 0; q < p.split; ++q) acc += __ldcg(p.part + ((int64_t)q * p.M + i) * C + c);
+        if (c < NS) {
+            const double v = acc * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i * NS + c] = v;
+            else ((float *)p.out)[i * NS + c] = (float)v;
+        } else if constexpr (NG > 0) {
+            double v = acc * p.scale_grad;
+            if (E == 1 && p.g) v *= (double)__ldg(p.g + i);
+            const int dc = c - NS;
+            if (MODE == 2) p.out_grad[i * D + dc] = (float)v;
+            else if (p.out_f64) ((double *)p.out)[i * D + dc] = v;
+            else ((float *)p.out)[i * D + dc] = (float)v;
+        }
+    }
+    if (threadIdx.x == 0) p.tile_done[itile] = 0u;     // ready for the next call on the stream
+}
+
 // The grid walks the work units w = blockIdx.x, blockIdx.x + gridDim.x, ...; a unit is (row
 // tile, j-split), (row group, j-split) in the small-M mode, or one block-sparse range unit.  The
 // launch uses one CTA per unit (measured faster than a persistent grid, see sum_kernel.cu).
@@ -413,6 +455,7 @@ sum_kernel(const SumParams p) {
         Geo geo{};
         sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
     }
+    if (!SMM && p.tile_done && !p.units) sum_tile_merge<MODE, D, E, R>(p, w / p.split, row0, row_end);
     }
 }
 
