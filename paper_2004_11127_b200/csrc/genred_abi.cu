@@ -987,6 +987,17 @@ genred_status genred_profile(genred_ctx *ctx, int32_t enable) {
     if (!ctx) return GENRED_E_INVALID;
     ctx->profiling = enable != 0;
     ctx->nprof = 0;
+    // create the first 1024 (start, stop) pairs now: cudaEventCreate inside a caller's timed
+    // region would add host latency to launch-bound calls (C1)
+    int prev = 0;
+    cudaGetDevice(&prev);
+    if (prev != ctx->device) cudaSetDevice(ctx->device);
+    while (ctx->profiling && ctx->ev.size() < 2048) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) { cudaGetLastError(); break; }
+        ctx->ev.push_back(e);
+    }
+    if (prev != ctx->device) cudaSetDevice(prev);
     return GENRED_OK;
 }
 

@@ -191,6 +191,34 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     (host mode: staged H2D -> kernels -> D2H inside libgenred, synchronous).
     Returns out (and out_grad / out_idx when applicable).
     """
+    a, res, keep = prepare(formula, reduction, x, y, b, g, scale=scale, K=K, out=out,
+                           out_dtype=out_dtype, out_grad=out_grad, out_idx=out_idx,
+                           lse_state=lse_state, split_j=split_j, j_offset=j_offset,
+                           row_shift=row_shift, col_shift=col_shift, ranges=ranges)
+    if isinstance(x, np.ndarray):
+        dev, sptr = None, None
+    else:
+        import torch
+        dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
+        s = stream if stream is not None else torch.cuda.current_stream(dev)
+        sptr = ctypes.c_void_p(s.cuda_stream)
+    ctx = context(dev)
+    st = load().genred_eval(ctx, ctypes.byref(a), sptr)
+    del keep
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+    return res
+
+
+def prepare(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1.0, K: int = 1,
+            out=None, out_dtype: str = "float32", out_grad=None, out_idx=None, lse_state=None,
+            split_j: int = 0, j_offset: int = 0, row_shift=None, col_shift=None, ranges=None):
+    """Marshal eval()'s arguments into a genred_args struct (allocating missing outputs).
+
+    Returns (args, result, keepalive): ``eval_args(args)`` then repeats the same call with no
+    Python-side marshalling (a fixed call in a loop: the benchmark's timed steps).  The caller
+    keeps ``keepalive`` (host range arrays) and every tensor alive while the struct is in use.
+    """
     host = isinstance(x, np.ndarray)
     M, D = int(x.shape[0]), int(x.shape[1])
     N = int(y.shape[0])
@@ -243,26 +271,19 @@ def eval(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float = 1
     a.out_grad, a.out_idx, a.lse_state = _ptr(out_grad), _ptr(out_idx), _ptr(lse_state)
     a.j_offset = int(j_offset)
     a.row_shift, a.col_shift = _ptr(row_shift), _ptr(col_shift)
+    keep = None
     if ranges is not None:              # (ranges_i (C,2), slices (C,), ranges_j (L,2)) host int64
         ri, sl, rj = (np.ascontiguousarray(np.asarray(v, dtype=np.int64)) for v in ranges)
         a.n_ranges = int(ri.shape[0])
         a.ranges_i, a.slices, a.ranges_j = ri.ctypes.data, sl.ctypes.data, rj.ctypes.data
-    if host:
-        dev, sptr = None, None
-    else:
-        import torch
-        dev = x.device.index if x.device.index is not None else torch.cuda.current_device()
-        s = stream if stream is not None else torch.cuda.current_stream(dev)
-        sptr = ctypes.c_void_p(s.cuda_stream)
-    ctx = context(dev)
-    st = load().genred_eval(ctx, ctypes.byref(a), sptr)
-    if st != OK:
-        raise GenredError(st, load().genred_last_error(ctx).decode())
+        keep = (ri, sl, rj)
     if r == REDUCTIONS["argkmin"]:
-        return out, out_idx
-    if f in (FORMULAS["gauss_sum_gradx"], FORMULAS["lse_grad"]):
-        return out, out_grad
-    return out
+        res = (out, out_idx)
+    elif f in (FORMULAS["gauss_sum_gradx"], FORMULAS["lse_grad"]):
+        res = (out, out_grad)
+    else:
+        res = out
+    return a, res, keep
 
 
 def eval_args(args: Args, stream=None, device: int | None = None) -> None:
