@@ -619,7 +619,8 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // Few partials per row tile: the last CTA of each row tile merges them (no finalize
         // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.
         const int64_t tile_rows = (int64_t)kConsumerWarps * 32 * pl.R;
-        const bool fused_merge = pl.split > 1 && !smm && !tc &&
+        const char *fmv = getenv("GENRED_FUSED_MERGE");          // "0": always the finalize kernel
+        const bool fused_merge = pl.split > 1 && !smm && !tc && !(fmv && atoi(fmv) == 0) &&
                                  std::min<int64_t>(tile_rows, M) * C * pl.split <= 16384;
         if (fused_merge) {
             s = ensure_tile_done(ctx, pl.itiles);

@@ -1041,3 +1041,38 @@ def test_randomized_hard_inputs(G, seed):
         d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=K, split_j=split)
         od, oj = oracle.argkmin(x, y, K + 1)
         argk_check(host(d), host(j), od, oj, K, what=f"{tag} argk")
+
+
+@pytest.mark.parametrize("formula,E,g", [("gauss", 1, False), ("gauss", 2, False),
+                                         ("gauss_gradx", 1, True), ("gauss_sum_gradx", 1, True),
+                                         ("gauss_sum_gradx", 2, True)])
+@pytest.mark.parametrize("M,N,split", [(1000, 1000, 0), (2500, 3100, 5), (700, 20000, 0)])
+def test_fused_split_merge_bitwise(G, monkeypatch, formula, E, g, M, N, split):
+    """The last-CTA split merge inside the pair-loop kernel (DESIGN a7/a8) sums the partials in
+    the finalize kernel's order: bitwise equal to the two-kernel path, one launch fewer, and the
+    arrival counters are back at zero after every call (repeated calls are bitwise equal)."""
+    x = synth.uniform3(M, 501); y = synth.uniform3(N, 502)
+    b = synth.signal(N, 503, E=E, signed=True)
+    gg = dev(synth.cotangent(M, 504, E=E)) if g else None
+
+    def run():
+        r = G.eval(formula, "sum", dev(x), dev(y), dev(b), gg, scale=0.5, split_j=split)
+        r = r if isinstance(r, tuple) else (r,)
+        return [host(t) for t in r], G.last_plan()
+
+    monkeypatch.setenv("GENRED_FUSED_MERGE", "0")
+    ref, p0 = run()
+    monkeypatch.setenv("GENRED_FUSED_MERGE", "1")
+    got, p1 = run()
+    again, _ = run()
+    assert p0["split_j"] == p1["split_j"] > 1, (p0, p1)
+    fused = p1["kernels"] == p0["kernels"] - 1         # tiles with <= 16 K partials merge in-kernel
+    assert fused or p1["kernels"] == p0["kernels"], (p0, p1)
+    if (M, N) == (1000, 1000):
+        assert fused and p1["kernels"] == 2, p1        # C1: pack (+ box) and the pair loop
+    for a, c, d in zip(ref, got, again):
+        np.testing.assert_array_equal(a, c)
+        np.testing.assert_array_equal(c, d)
+    if formula == "gauss":
+        o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
+        assert_sum_parity(got[0], o, den, what=f"fused merge {M}x{N}")
