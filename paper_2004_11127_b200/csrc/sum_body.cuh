@@ -389,7 +389,8 @@ __device__ __forceinline__ void sum_tile_merge(const SumParams &p, int64_t itile
         const int64_t i = row0 + t / C;
         const int c = (int)(t % C);
         double acc = 0.0;
-        for (int q = 0; q < p.split; ++q) acc += __ldcg(p.part + ((int64_t)q * p.M + i) * C + c);
+#pragma unroll 8
+        for (int q = 0; q < p.split; ++q) acc += __ldcg(p.part + ((int64_t)q * p.M + i) * C + c);   // 8 loads in flight
         if (c < NS) {
             const double v = acc * p.scale_sum;
             if (p.out_f64) ((double *)p.out)[i * NS + c] = v;
