@@ -65,6 +65,10 @@ def workload(cid: int) -> dict:
         #            is the MUFU's either way (min(16/1, 128/7) = 16 pairs/clk/SM)
         return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=7, mufu=1,
                     out_dtype="float32")
+    if cid == 7:   # j-sharded Gaussian Sum (M << N): as C5 per rank, fp64 partials all-reduced
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=4, mufu=1, out_dtype="float64")
+    if cid == 8:   # j-sharded LSE: as C3 per rank, (m, s) states all-gathered and combined
+        return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
     if cid == 6:   # Cedge: N tiny -> 12 B of x read + 4 B of a written per row (HBM-bound)
@@ -141,6 +145,18 @@ def ncu_traffic(cid: int, n: int = 0):
     return d.get(f"C{cid}")
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (what `lscpu` reports as "Model name")."""
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
 def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
     """The fp64 oracle as it stands, on a bounded row sample of the same workload."""
     import oracle
@@ -150,7 +166,7 @@ def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
         od, oj = oracle.argkmin(x, y, c.K, rows=rows)
         dt = time.perf_counter() - t0
         res = {"value": len(rows) * c.N / dt, "unit": UNIT, "cores": oracle.num_threads(),
-               "kind": "oracle", "seconds": round(dt, 3),
+               "cpu_model": cpu_model(), "kind": "oracle", "seconds": round(dt, 3),
                "sample": f"{len(rows)} seeded rows x all N={c.N}, D={c.D} (fp64 direct differences)"}
         if gpu_rows is not None:
             res["index_match_frac_vs_gpu"] = float(np.mean(np.asarray(gpu_rows) == oj))
@@ -165,7 +181,7 @@ def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
         o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
     dt = time.perf_counter() - t0
     res = {"value": len(rows) * c.N / dt, "unit": UNIT, "cores": oracle.num_threads(),
-           "kind": "oracle", "seconds": round(dt, 3),
+           "cpu_model": cpu_model(), "kind": "oracle", "seconds": round(dt, 3),
            "sample": f"{len(rows)} seeded rows x all N={c.N} (fp64, OpenMP, Neumaier)"}
     if gpu_rows is not None:
         if den is not None:
@@ -230,11 +246,177 @@ def run_reference(args, rank: int, world: int) -> None:
         "data": "synthetic",
         "config": {"workload": c.name, "M": c.M, "N": c.N, "D": c.D, "E": c.E, "scale": c.scale,
                    "dist": args.dist, "parallelism": "host cores (rank 0 only)"},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
-                         "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "cpu_model": cpu_model(),
+                         "kind": "oracle", "sample": sample},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def gather_rows(dist, world: int, dev, t):
+    """All-gather equal-shaped 2-D tensors from every rank; every rank gets them concatenated in
+    rank order (gloo: through host memory)."""
+    if world == 1:
+        return t
+    import torch
+    if dist.get_backend() == "gloo":
+        t = t.cpu()
+    parts = [torch.empty_like(t) for _ in range(world)]
+    dist.all_gather(parts, t)
+    return torch.cat(parts, 0)
+
+
+def shard_parity_sample(dist, world: int, rank: int, lo: int, res, per: int, seed: int = 777):
+    """`per` seeded rows of this rank's output shard `res` (global rows lo + local), gathered to
+    every rank: returns (global row indices [world*per], values [world*per, C] fp64)."""
+    import torch
+    Ml = res.shape[0]
+    per = min(per, Ml)
+    lrows = np.sort(np.random.default_rng(seed + rank).choice(Ml, size=per, replace=False))
+    vals = res[torch.from_numpy(lrows).to(res.device)].to(torch.float64).reshape(per, -1)
+    both = torch.cat([torch.from_numpy(lrows + lo).to(res.device, torch.float64)[:, None], vals], 1)
+    both = gather_rows(dist, world, res.device, both).cpu().numpy()
+    return both[:, 0].astype(np.int64), both[:, 1:]
+
+
+def run_jshard(args, rank: int, world: int, local: int, w: dict) -> None:
+    """j-shard mode (north star (d) "a j-sharded mode for M << N"): rank r owns
+    y[rN/G:(r+1)N/G] (and b), every rank holds all M rows of x, and one step = the public
+    dist.jshard_eval: the local Genred reduction, then the combine across ranks (Sum: fp64
+    all_reduce; LSE: all_gather of the (m, s) states + genred_combine_lse).  Each rank draws only
+    its slice of y (synth.uniform3_rows)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2004_11127_b200 import dist as gdist, genred
+
+    c = w["cfg"]
+    M, N = c.M, c.N
+    sd = synth.seeds(c.cid)
+    lo, hi = N * rank // world, N * (rank + 1) // world
+    x = synth.uniform3(M, sd["x"])
+    yl = synth.uniform3_rows(N, sd["y"], lo, hi)
+    bl = synth.signal_rows(N, sd["b"], lo, hi) if w["reduction"] == "sum" else None
+    dev = torch.device("cuda", local)
+    xd = torch.from_numpy(x).to(dev)
+    yd = torch.from_numpy(yl).to(dev)
+    bd = torch.from_numpy(bl).to(dev) if bl is not None else None
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        return gdist.jshard_eval(w["formula"], w["reduction"], xd, yd, bd, None, scale=c.scale,
+                                 j_offset=lo, out_dtype="float64")
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def reduce(v: float, op) -> float:
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=op)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        res = step()
+    barrier()
+    plan = genred.last_plan(local)
+    sampler = ClockSampler(local).start()
+    genred.profile(True, local)
+    l0 = genred.launch_count(local)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        res = step()
+    ev1.record(stream)
+    torch.cuda.synchronize(dev)
+    clocks = sampler.stop()
+    launches = genred.launch_count(local) - l0
+    kms = genred.profile_read(local)
+    genred.profile(False, local)
+    barrier()
+    ms_local = ev0.elapsed_time(ev1)
+    ms_total = reduce(ms_local, dist.ReduceOp.MAX if world > 1 else None)
+    launches = int(reduce(float(launches), dist.ReduceOp.SUM if world > 1 else None))
+    ms_step = ms_total / args.steps
+    value = M * N * args.steps / (ms_total * 1e-3)
+    kmean_local = statistics.mean(kms) if kms else float("nan")
+    kmean = reduce(kmean_local, dist.ReduceOp.MAX if world > 1 else None)
+    peaks = measured_peaks()
+    mhz_max = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
+    peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
+    achieved = M * (hi - lo) / (kmean * 1e-3)
+    roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": f"{w['formula']}/{w['reduction']} pair loop (one rank's j-slice)",
+                "kernel_ms": kmean, "share_of_step": kmean / ms_step if world == 1 else None,
+                "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
+                              f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                "pairs_per_launch": M * (hi - lo)}
+    mine = [float(rank), float(lo), float(hi), float(plan["split_j"]), float(plan["rows_per_cta"]),
+            float(plan["ctas"]), float(kmean_local), float(ms_local / args.steps)]
+    per_rank = gather_rows(dist, world, dev, torch.tensor([mine], dtype=torch.float64, device=dev))
+
+    # end to end: pinned host x, y-slice, b-slice -> device, jshard_eval, merged result -> host
+    e2e = None
+    if not args.no_e2e:
+        xh = torch.from_numpy(x).pin_memory()
+        yh = torch.from_numpy(yl).pin_memory()
+        bh = torch.from_numpy(bl).pin_memory() if bl is not None else None
+        oh = torch.empty(tuple(res.shape), dtype=res.dtype).pin_memory()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(args.steps):
+            xd.copy_(xh, non_blocking=True)
+            yd.copy_(yh, non_blocking=True)
+            if bh is not None:
+                bd.copy_(bh, non_blocking=True)
+            r = step()
+            oh.copy_(r, non_blocking=True)
+        e1.record(stream)
+        torch.cuda.synchronize(dev)
+        barrier()
+        e2e_ms = reduce(e0.elapsed_time(e1), dist.ReduceOp.MAX if world > 1 else None)
+        h2d = xh.numel() * 4 + yh.numel() * 4 + (bh.numel() * 4 if bh is not None else 0)
+        d2h = oh.numel() * oh.element_size()
+        e2e = {"value": M * N * args.steps / (e2e_ms * 1e-3), "unit": UNIT,
+               "h2d_bytes_per_step": int(reduce(float(h2d), dist.ReduceOp.SUM if world > 1 else None)),
+               "d2h_bytes_per_step": int(reduce(float(d2h), dist.ReduceOp.SUM if world > 1 else None)),
+               "ms_per_step": e2e_ms / args.steps, "api": "dist.jshard_eval (public API) from pinned host buffers"}
+
+    # parity: the merged rows against the fp64 oracle over ALL of y (rank 0 draws the full y)
+    cpu = None
+    if rank == 0 and not args.no_cpu:
+        import oracle
+        oracle.set_num_threads(os.cpu_count() or 1)
+        y = synth.uniform3(N, sd["y"])
+        b = synth.signal(N, sd["b"]) if w["reduction"] == "sum" else None
+        rows = np.sort(np.random.default_rng(777).choice(M, size=min(args.parity_rows, M), replace=False))
+        cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=res.cpu().numpy()[rows])
+        cpu["sample"] = f"{len(rows)} seeded rows (after the cross-rank combine) x all N={N}"
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": c.name, "M": M, "N": N, "D": c.D, "E": c.E, "scale": c.scale,
+                       "dist": "x U3, y U3", "b": "U[0,1)" if bl is not None else None,
+                       "parallelism": f"jshard{world}" if world > 1 else "single (j-shard path, 1 rank)",
+                       "combine": "all_reduce fp64 (Sum)" if w["reduction"] == "sum"
+                                  else "all_gather (m, s) + genred_combine_lse",
+                       "l2": "y slice larger than L2 at G <= 8 (1.2 GB / G); no flush",
+                       "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"], "ctas": plan["ctas"]},
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
+            "gpu_launches": launches,
+            "per_rank": [dict(zip(("rank", "j_lo", "j_hi", "split_j", "rows_per_cta", "ctas", "kernel_ms",
+                                   "step_ms"), [int(v) if k < 6 else round(v, 4) for k, v in enumerate(r)]))
+                         for r in per_rank.tolist()],
+        }
+        print(json.dumps(line), flush=True)
 
 
 def main() -> None:
@@ -243,7 +425,11 @@ def main() -> None:
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", type=int, default=5)
+    ap.add_argument("--config", type=int, default=0, help="BASELINE config (default 5; 7 with --mode jshard)")
+    ap.add_argument("--mode", default="ishard", choices=["ishard", "jshard"],
+                    help="multi-GPU partition (SURVEY.md 8(e)): i-shard (default) or j-shard (M << N)")
+    ap.add_argument("--parity-rows", type=int, default=128,
+                    help="N>1 / j-shard: seeded rows per rank checked against the oracle on rank 0")
     ap.add_argument("--dist", default="U3", choices=["U3", "GMM3"])
     ap.add_argument("--cpu-rows", type=int, default=0, help="oracle sample rows (cpu_baseline); 0 = auto")
     ap.add_argument("--ref-pairs", type=float, default=0, help="oracle pairs per reference step (0 = auto)")
@@ -254,6 +440,10 @@ def main() -> None:
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--edge-n", type=int, default=0, help="config 6 (Cedge): N (default 8)")
     args = ap.parse_args()
+    if not args.config:
+        args.config = 7 if args.mode == "jshard" else 5
+    if args.mode == "jshard" and args.config not in (7, 8):
+        raise SystemExit("--mode jshard runs the j-shard configs 7 (Gaussian Sum) or 8 (LSE)")
     if args.edge_n:
         if args.config != 6:
             raise SystemExit("--edge-n applies to --config 6")
@@ -277,11 +467,19 @@ def main() -> None:
     torch.cuda.set_device(local)
     if world > 1:
         if args.dist_backend == "nccl":
+            # communicator evidence: NCCL's INIT lines name every rank ("nranks N") in the log
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         else:
             dist.init_process_group("gloo")
     w = workload(args.config)
     c = w["cfg"]
+    if args.mode == "jshard":
+        run_jshard(args, rank, world, local, w)
+        if world > 1:
+            dist.destroy_process_group()
+        return
     M, N = c.M, c.N
     lo, hi = M * rank // world, M * (rank + 1) // world
     x, y, b = make_inputs(w, args.dist)
@@ -360,8 +558,8 @@ def main() -> None:
     value = M * N * args.steps / (ms_total * 1e-3)
 
     # dominant kernel roofline (this rank's launches; the slowest rank bounds the job)
-    kmean = statistics.mean(kms) if kms else float("nan")
-    kmean = max_over_ranks(kmean)
+    kmean_local = statistics.mean(kms) if kms else float("nan")
+    kmean = max_over_ranks(kmean_local)
     peaks = measured_peaks()
     mhz_max = float(peaks.get("sm_max_mhz", clocks.get("sm_max_mhz") or 1965.0))
     if argk:
@@ -442,15 +640,36 @@ def main() -> None:
                "d2h_bytes_per_step": int(sum_over_ranks(d2h)),
                "ms_per_step": e2e_ms / args.steps, "api": "genred_eval(memory=GENRED_MEM_HOST)"}
 
-    # ---------------- fp64 oracle on the host cores (rank 0, N=1 only) ----------------
+    # ---------------- per-rank plan and main-kernel time (all ranks -> rank 0) ----------------
+    mine = [float(rank), float(lo), float(hi), float(plan["split_j"]), float(plan["rows_per_cta"]),
+            float(plan["ctas"]), float(kmean_local), float(ev0.elapsed_time(ev1) / args.steps)]
+    per_rank = gather_rows(dist, world, dev, torch.tensor([mine], dtype=torch.float64, device=dev))
+    per_rank = [dict(zip(("rank", "row_lo", "row_hi", "split_j", "rows_per_cta", "ctas", "kernel_ms",
+                          "step_ms"), [int(v) if k < 6 else round(v, 4) for k, v in enumerate(r)]))
+                for r in per_rank.tolist()]
+
+    # ---------------- fp64 oracle on the host cores ----------------
+    # N = 1: a row sample sized for ~15 s of host work.  N > 1: `--parity-rows` seeded rows from
+    # EACH rank's shard are gathered to rank 0 and checked there, so every sharded line carries
+    # its own parity evidence (the oracle's rows/s is then timed on that sample).
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu:
-        import oracle
-        oracle.set_num_threads(os.cpu_count() or 1)
-        nrows = args.cpu_rows or max(16, min(M, 4_000_000, int(3e10 // (N * (c.D if argk else 1)))))
-        rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
-        gpu_rows = (out_idx if argk else out).cpu().numpy()[rows]
-        cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=gpu_rows)
+    if not args.no_cpu:
+        res = (out_idx if argk else out)
+        if world == 1:
+            nrows = args.cpu_rows or max(16, min(M, 4_000_000, int(3e10 // (N * (c.D if argk else 1)))))
+            rows = np.sort(np.random.default_rng(777).choice(M, size=min(nrows, M), replace=False))
+            gpu_rows = res.cpu().numpy()[rows]
+        else:
+            per = min(args.parity_rows, Ml)
+            rows, gpu_rows = shard_parity_sample(dist, world, rank, lo, res, per)
+            if argk:
+                gpu_rows = gpu_rows.astype(np.int64)
+        if rank == 0:
+            import oracle
+            oracle.set_num_threads(os.cpu_count() or 1)
+            cpu = cpu_baseline(w, x, y, b, rows, gpu_rows=gpu_rows)
+            if world > 1:
+                cpu["sample"] = f"{per} seeded rows of each of the {world} shards (all gathered to rank 0) x all N={N}"
 
     if rank == 0:
         line = {
@@ -458,7 +677,8 @@ def main() -> None:
             "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": c.name, "M": M, "N": N, "D": c.D, "E": c.E, "scale": c.scale,
-                       "dist": args.dist if w["reduction"] != "lse" else f"x {c.x_dist}, y {c.y_dist}",
+                       "dist": ("MNIST784" if argk else args.dist) if w["reduction"] != "lse"
+                               else f"x {c.x_dist}, y {c.y_dist}",
                        "b": "U[0,1)" if b is not None else None,
                        "parallelism": f"ishard{world}" if world > 1 else "single",
                        "l2": ("inputs larger than L2 (280 MB vs 126 MB); no flush" if c.cid == 5 else
@@ -470,6 +690,8 @@ def main() -> None:
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
         }
+        if world > 1:
+            line["per_rank"] = per_rank
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()

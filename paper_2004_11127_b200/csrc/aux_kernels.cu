@@ -28,7 +28,7 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
     __shared__ uint32_t sgeo[32];
     float *sm = reinterpret_cast<float *>(pack_smem4);
     const float NEG_INF = -INFINITY;
-    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_AUTO_RAW;
     const bool raw = kind == PACK_GAUSS_AUTO_RAW;           // + the b y' slots (gradient modes)
     const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
     const int EB = (gauss || sumk) ? (b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);   // staged b / h columns
@@ -103,7 +103,6 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
     }
     if (gauss) {
         geo = geo_decode(geo_enc, D, s);      // expanded or direct per the bounding box
-        if (kind == PACK_GAUSS_DIRECT && geo.expanded) return;   // gauss_tc.cu takes this call
     }
     const int t = threadIdx.x;
     for (int64_t blk = blockIdx.x; blk * 256 < npairs; blk += gridDim.x) {
@@ -170,14 +169,14 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
 }
 
 static int pack_smem_bytes(int kind, int D, int E, int RS, bool has_b) {
-    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT || kind == PACK_GAUSS_AUTO_RAW;
+    const bool gauss = kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_AUTO_RAW;
     const bool sumk = kind == PACK_GAUSS || kind == PACK_SQDIST_SUM;
     const int EB = (gauss || sumk) ? (has_b ? E : 0) : (kind == PACK_LSE_H ? 1 : 0);
     return (kTileJ * (D + EB) + 256 * RS) * 4;
 }
 
 int pack_record_stride(int kind, int D, int E) {
-    if (kind == PACK_GAUSS_AUTO || kind == PACK_GAUSS_DIRECT) return record_stride(D + 1, E);
+    if (kind == PACK_GAUSS_AUTO) return record_stride(D + 1, E);
     if (kind == PACK_GAUSS_AUTO_RAW) return gauss_record_stride(D, E, true);
     if (kind == PACK_ARGKMIN) return record_stride(D + 1, 0);      // + the j pair
     if (kind == PACK_LSE_HZ) return record_stride(D, 0);

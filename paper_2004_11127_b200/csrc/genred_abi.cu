@@ -34,8 +34,6 @@ struct genred_ctx {
     std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
     int *fallback_dev = nullptr;                               // k-NN rows rescanned exactly
     const uint32_t *geo_dev = nullptr;                         // Gaussian Sum bounding box
-    bool geo_tc = false;                                       // ... evaluated by gauss_tc.cu
-    bool gauss_tc = false;                                     // GENRED_GAUSS_TC=1 enables (opt-in)
     int geo_D = 0;
     float geo_s = 0.f;
     unsigned *tile_done = nullptr;                             // split-merge arrival counters (zero at rest)
@@ -242,14 +240,16 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
     return pl;
 }
 
-// Per-row-tile arrival counters of the in-kernel split merge: zeroed once when allocated; every
+// Per-row-tile arrival counters of the in-kernel split merge: zeroed once when allocated, by an
+// asynchronous memset on the caller's stream `st` (the stream the merging kernel runs on, which
+// may be a non-blocking stream: a legacy-stream memset would not be ordered before it); every
 // merging CTA resets its counter, so they are zero again whenever the stream is idle.
-genred_status ensure_tile_done(genred_ctx *ctx, int64_t n) {
+genred_status ensure_tile_done(genred_ctx *ctx, int64_t n, cudaStream_t st) {
     if (n <= ctx->tile_done_cap) return GENRED_OK;
     const int64_t cap = std::max<int64_t>(n, 1024);
     if (ctx->tile_done) { cudaFree(ctx->tile_done); ctx->tile_done = nullptr; ctx->tile_done_cap = 0; }
     if (cudaMalloc(&ctx->tile_done, cap * sizeof(unsigned)) != cudaSuccess ||
-        cudaMemset(ctx->tile_done, 0, cap * sizeof(unsigned)) != cudaSuccess) {
+        cudaMemsetAsync(ctx->tile_done, 0, cap * sizeof(unsigned), st) != cudaSuccess) {
         cudaGetLastError();
         return fail(ctx, GENRED_E_NOMEM, "split-merge counter allocation failed");
     }
@@ -504,22 +504,6 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         const int rmax = sum_rows_per_thread_max(mode, D, E);
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, mode, rmax);
         Plan pl = make_plan(ctx, a, 0, rmax, mode, D, E, true);
-        // Gaussian Sum, one signal column, D <= 3: the tensor-core kernel (gauss_tc.cu) takes
-        // the expanded case; the FP32 kernel behind it only the direct one.  Both use the same
-        // j-split (in 512-j tiles), chosen for 128-row units on one CTA per SM.
-        // Opt-in (GENRED_GAUSS_TC=1): the north star keeps small D on the FP32/MUFU pipes (its
-        // row (c)); this path measured +6% over them, not enough to deviate.
-        const char *tcv = getenv("GENRED_GAUSS_TC");
-        const bool tc = mode == 0 && E == 1 && D <= 3 && (tcv ? atoi(tcv) != 0 : ctx->gauss_tc);
-        if (tc) {
-            const int64_t units_i = (M + gauss_tc_rows_per_unit() - 1) / gauss_tc_rows_per_unit();
-            const int64_t n256 = 2 * pl.ntiles;                    // 256-j tiles of gauss_tc
-            const int S = a->split_j > 0 ? (int)std::min<int64_t>(std::min(a->split_j, kMaxSplit), n256)
-                                         : choose_split(units_i, n256, 1, 4, ctx->num_sms, nullptr);
-            pl.R = rmax;
-            pl.split = S;            // both kernels write S partials (empty ranges write zeros)
-            pl.pairs_per_split = ((pl.npv + S - 1) / S + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
-        }
         // Small M (north star (a), the warp-shuffle finish): when even one-row-per-thread tiles
         // split as far as j allows cannot fill the GPU, CTAs of a few rows whose 256 threads
         // share the rows and split j take over (sum_smm.cu).  Not for tiny N (edge kernel).
@@ -528,7 +512,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // split compute their rows bitwise as the unsharded call does.)
         // (Measured at N = 1e7: the small-M CTAs re-stream the j-records per R = 8 rows, so they
         // pay off only while most threads of a one-row-per-thread tile would idle, M <= 64.)
-        if (!tc && a->split_j <= 0 && N > kDirectMaxN && M <= kSmmMaxM && sum_smm_supported(mode, D, E))
+        if (a->split_j <= 0 && N > kDirectMaxN && M <= kSmmMaxM && sum_smm_supported(mode, D, E))
             smm = true;
         if (smm) {
             const int Rs = sum_smm_rows(mode);
@@ -539,20 +523,18 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
             pl.R = Rs;
         }
-        const int pk = mode == 3 ? PACK_SQDIST_SUM : tc ? PACK_GAUSS_DIRECT
+        const int pk = mode == 3 ? PACK_SQDIST_SUM
                      : (mode == 1 || mode == 2) ? PACK_GAUSS_AUTO_RAW : PACK_GAUSS_AUTO;
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
-        const size_t tbytes = tc ? al256(gauss_tc_scratch_bytes(M, N)) : 0;
-        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256 + tbytes);
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256);
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
         uint32_t *geo = (uint32_t *)((char *)ctx->scratch + jbytes + pbytes);
-        void *tscratch = (char *)ctx->scratch + jbytes + pbytes + 256;
         // parameter folding in fp64, rounded once to fp32 (R15, R18)
         float sc = 1.0f;
         double scale_grad = 0.0;
@@ -565,32 +547,19 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // Tiny N (the HBM-bound edge, SURVEY.md 8(d) Cedge): the pair loop is a few FP32 ops per
         // row, so the direct form is free and the bounding-box pass over x (a second full read
         // of x) is skipped; geo = nullptr selects the direct form on the device.
-        const bool tiny_n = N <= kDirectMaxN && !tc;
+        const bool tiny_n = N <= kDirectMaxN;
         // Few rows (M <= kDirectMaxM): the pair loop is bound by streaming the j-records, so the
         // direct form costs nothing and the bounding-box pass over y (a full read of y) is skipped.
-        const bool no_box = tiny_n || (M <= kDirectMaxM && !tc);
+        const bool no_box = tiny_n || M <= kDirectMaxM;
         if (no_box) geo = nullptr;
         // small problems: the box is reduced inside the pack kernel (one launch fewer)
-        const bool boxed_pack = mode != 3 && !no_box && !tc && std::max(M, N) <= kFusedBoxMax;
+        const bool boxed_pack = mode != 3 && !no_box && std::max(M, N) <= kFusedBoxMax;
         if (mode != 3 && !no_box && !boxed_pack) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
         }
         int ctas = 0;
-        if (tc) {
-            GaussTcLaunch T;
-            T.x = a->x; T.y = a->y; T.b = a->b; T.geo = geo; T.M = M; T.N = N; T.D = D; T.s = sc;
-            T.split = pl.split; T.tiles_per_split = (2 * pl.ntiles + pl.split - 1) / pl.split; T.scale_sum = 1.0;
-            T.out = a->out; T.out_f64 = out_f64; T.part = part; T.scratch = tscratch;
-            T.num_sms = ctx->num_sms;
-            T.ev_start = prof_event(ctx, true, nullptr, true);
-            T.ev_stop = prof_event(ctx, false, nullptr, true);
-            int tk = 0;
-            e = launch_gauss_tc(T, st, &ctas, &tk);
-            if (e != cudaSuccess) return cuda_fail(ctx, e, "tensor-core Gaussian sum");
-            kernels += tk;
-        }
         e = boxed_pack ? launch_pack_boxed(pk, a->y, a->b, N, D, E, sc, npairs, J, a->x, M, geo, st)
                        : launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
@@ -606,7 +575,6 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             ctx->plan.kernels = kernels; ctx->plan.path = 0; ctx->plan.tile_j = (int32_t)N;
             ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
             ctx->geo_dev = nullptr;
-            ctx->geo_tc = false;
             return GENRED_OK;
         }
         SumLaunch L;
@@ -615,23 +583,25 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
-        L.direct_only = tc ? 1 : 0;
         // Few partials per row tile: the last CTA of each row tile merges them (no finalize
-        // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.
+        // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.  Only up to 32
+        // splits: above that the finalize kernel sums lane-strided (sum_finalize_warp_kernel),
+        // and the fused merge must give bitwise its result (i-shards of one problem may take
+        // either path).
         const int64_t tile_rows = (int64_t)kConsumerWarps * 32 * pl.R;
         const char *fmv = getenv("GENRED_FUSED_MERGE");          // "0": always the finalize kernel
-        const bool fused_merge = pl.split > 1 && !smm && !tc && !(fmv && atoi(fmv) == 0) &&
+        const bool fused_merge = pl.split > 1 && pl.split <= 32 && !smm && !(fmv && atoi(fmv) == 0) &&
                                  std::min<int64_t>(tile_rows, M) * C * pl.split <= 16384;
         if (fused_merge) {
-            s = ensure_tile_done(ctx, pl.itiles);
+            s = ensure_tile_done(ctx, pl.itiles, st);
             if (s != GENRED_OK) return s;
             L.tile_done = ctx->tile_done;
         }
         int sctas = 0;
-        if (!tc) prof_event(ctx, true, st);
+        prof_event(ctx, true, st);
         e = smm ? launch_sum_smm(L, st, &sctas) : launch_sum(L, st, &sctas);
-        if (!tc) prof_event(ctx, false, st);
-        if (!tc) ctas = sctas;
+        prof_event(ctx, false, st);
+        ctas = sctas;
         if (e != cudaSuccess) return cuda_fail(ctx, e, "sum kernel");
         if (pl.split > 1 && !fused_merge) {
             const int cols_sum = (mode == 1) ? 0 : E;
@@ -645,7 +615,6 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
         ctx->geo_dev = mode != 3 ? geo : nullptr;
-        ctx->geo_tc = tc;
         ctx->geo_D = D;
         ctx->geo_s = sc;
         return GENRED_OK;
@@ -842,7 +811,6 @@ genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
     cudaSetDevice(cuda_device);
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
-    if (const char *v = getenv("GENRED_GAUSS_TC")) ctx->gauss_tc = atoi(v) != 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
     cudaSetDevice(prev);
@@ -970,7 +938,7 @@ genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
     *plan = ctx->plan;
     plan->fallback_rows = -1;
     if (ctx->plan.path == 0 && ctx->geo_dev && geo_expanded_host(ctx->geo_dev, ctx->geo_D, ctx->geo_s))
-        plan->path = ctx->geo_tc ? 3 : 2;                      // expanded form (tensor cores / FP32)
+        plan->path = 2;                                        // expanded form
     if (ctx->plan.path == 1 && ctx->fallback_dev) {
         int n = -1;
         if (cudaMemcpy(&n, ctx->fallback_dev, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {

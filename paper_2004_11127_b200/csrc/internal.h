@@ -50,7 +50,7 @@ inline int gauss_record_stride(int D, int E, bool grad) {
 inline int record_stride(int D, int E) { return ((2 * (D + E)) + 3) / 4 * 4; }
 
 enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKMIN = 3, PACK_LSE_H = 4,
-                PACK_GAUSS_AUTO = 5, PACK_GAUSS_DIRECT = 6, PACK_GAUSS_AUTO_RAW = 7 };
+                PACK_GAUSS_AUTO = 5, PACK_GAUSS_AUTO_RAW = 7 };
 
 // Pack y (N x D) and b (N x E) into the pair-interleaved j-record layout used by every small-D
 // kernel: pair p holds (-s*y_d[2p], -s*y_d[2p+1]) for d < D, then (b_e[2p], b_e[2p+1]) for e < E
@@ -62,8 +62,6 @@ enum PackKind { PACK_GAUSS = 0, PACK_SQDIST_SUM = 1, PACK_LSE_HZ = 2, PACK_ARGKM
 // expanded records (y' = s (y - c), w = -|y'|^2, b) or the direct ones (-y raw, 0, b): the kernel
 // forms raw differences x - y and scales their squared norm by s^2 (readings R18d, R18e).
 // PACK_GAUSS_AUTO_RAW (gradient modes): as PACK_GAUSS_AUTO, plus the b y' slots (kGradBY).
-// PACK_GAUSS_DIRECT: the direct records when the box rules the expanded form out, else nothing
-// (the tensor-core kernel, gauss_tc.cu, takes the expanded case).
 cudaError_t launch_pack(int kind, const float *y, const float *b, int64_t N, int D, int E,
                         float s, double hscale, int64_t npairs, float *J, cudaStream_t st,
                         const uint32_t *geo = nullptr);
@@ -112,7 +110,6 @@ struct SumLaunch {
     double *part;             // split > 1: split x M x C fp64 partials
     const RangeUnit *units;   // block-sparse ranges (device), or nullptr
     int64_t n_units;
-    int direct_only = 0;      // MODE 0: exit when the box allows the expanded form (gauss_tc runs)
     unsigned *tile_done = nullptr;  // split > 1: zeroed per-row-tile counters -> merge in the kernel
     int num_sms = 148;        // persistent grid: at most num_sms x occupancy CTAs
 };
@@ -208,27 +205,6 @@ int knn_tc_group();
 size_t knn_tc_scratch_bytes(int64_t M, int64_t N, int D, int K);
 cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info);
 
-// Gaussian Sum (MODE 0, E = 1, D <= 3) with the exponent contraction on the tensor cores
-// (gauss_tc.cu).  Runs when the box allows the expanded form (device-side decision, geo.cuh),
-// else exits; j-splits of tiles_per_split 512-j tiles, partials in the sum_finalize layout.
-struct GaussTcLaunch {
-    const float *x, *y, *b;
-    const uint32_t *geo;
-    int64_t M, N;
-    int D;
-    float s;
-    int split;
-    int64_t tiles_per_split;           // in 256-j tiles (= 2 x the 512-j tiles of the FP32 plan)
-    double scale_sum;
-    void *out; int out_f64;
-    double *part;
-    void *scratch;                     // gauss_tc_scratch_bytes(M, N) bytes
-    int num_sms;
-    cudaEvent_t ev_start, ev_stop;     // optional: recorded around the tcgen05 kernel
-};
-size_t gauss_tc_scratch_bytes(int64_t M, int64_t N);
-int gauss_tc_rows_per_unit();
-cudaError_t launch_gauss_tc(const GaussTcLaunch &a, cudaStream_t st, int *ctas, int *kernels);
 
 // Gaussian Sum at the HBM-bound edge (edge_kernel.cu): N <= sum_edge_max_n(), D <= 4, E = 1,
 // x 16-byte aligned; J = the PACK_GAUSS_AUTO direct records (geo = nullptr).

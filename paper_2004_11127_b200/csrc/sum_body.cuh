@@ -62,7 +62,6 @@ struct SumParams {
     float *out_grad;
     double *part;
     const RangeUnit *units;   // block-sparse ranges: one unit per (cluster, row tile)
-    int direct_only;          // MODE 0: exit when the expanded form applies (gauss_tc.cu runs)
     int64_t n_work;           // work units; the persistent grid walks w = blockIdx.x, + gridDim.x, ...
     unsigned *tile_done;      // split > 1, row tiles only: per-row-tile arrival counters (all zero
                               // between calls); the last CTA of a row tile merges its partials
@@ -447,7 +446,6 @@ sum_kernel(const SumParams p) {
     JRing<kStages> ring;
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
-        if (MODE == 0 && p.direct_only && geo.expanded) return;   // gauss_tc.cu took this call
         ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
         if (geo.expanded) sum_body<MODE, D, E, R, true, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
         else sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);

@@ -44,7 +44,6 @@ static cudaError_t run_smm(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.s = a.s;
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = nullptr;
-    p.direct_only = a.direct_only;
     p.tile_done = nullptr;
     p.n_work = (a.M + R - 1) / R * a.split;
     if (p.n_work == 0) { *ctas = 0; return cudaSuccess; }

@@ -8,5 +8,5 @@ All generators draw in fp64 with numpy ``default_rng(seed)`` (PCG64) and return 
 """
 from .inputs import (  # noqa: F401
     CONFIGS, Config, config, seeds,
-    uniform3, gmm3, signal, cotangent, mnist784, lattice_nodes, points,
+    uniform3, uniform3_rows, signal_rows, gmm3, signal, cotangent, mnist784, lattice_nodes, points,
 )

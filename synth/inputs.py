@@ -53,6 +53,11 @@ CONFIGS = {
     # Cedge: the memory-bound low-N, high-M edge; N in {1, 2, 4, 8, 16, 32}
     6: Config(6, "Cedge Gaussian Sum M=2^28 N=8 D=3 E=1 sigma=0.5 (HBM-bound)", "gauss", "sum",
               1 << 28, 8, 3, 1, 0.5),
+    # the j-shard regime of SURVEY.md 8(e) (M << N; north star (d)): y, b sharded over ranks
+    7: Config(7, "Cj Gaussian Sum M=1e4 N=1e8 D=3 E=1 sigma=0.5 (j-sharded)", "gauss", "sum",
+              10_000, 100_000_000, 3, 1, 0.5),
+    8: Config(8, "Cj LSE M=1e4 N=1e8 D=3 eps=0.05 (j-sharded)", "sqdist", "lse",
+              10_000, 100_000_000, 3, 1, 0.05),
 }
 
 
@@ -67,6 +72,20 @@ def seeds(cid: int) -> dict:
 def uniform3(n: int, seed: int, D: int = 3) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return rng.random((n, D)).astype(np.float32)
+
+
+def uniform3_rows(n: int, seed: int, lo: int, hi: int, D: int = 3) -> np.ndarray:
+    """Rows [lo, hi) of uniform3(n, seed, D), drawn without generating the others (PCG64
+    advance: each float64 consumes one 64-bit output), so a j-shard makes only its slice."""
+    assert 0 <= lo <= hi <= n
+    rng = np.random.default_rng(seed)
+    rng.bit_generator.advance(lo * D)
+    return rng.random((hi - lo, D)).astype(np.float32)
+
+
+def signal_rows(n: int, seed: int, lo: int, hi: int, E: int = 1) -> np.ndarray:
+    """Rows [lo, hi) of signal(n, seed, E) (the U[0,1) signal), as uniform3_rows."""
+    return uniform3_rows(n, seed, lo, hi, E)
 
 
 def gmm3(n: int, seed: int, D: int = 3, ncomp: int = 32, std: float = 0.04) -> np.ndarray:

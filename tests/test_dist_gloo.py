@@ -85,7 +85,15 @@ def _worker(rank, world, port, q):
         a_s = dist_eval("gauss", "sum", x, ys, bs, mode="jshard", scale=0.5, fns=fns, out_dtype="float64")
         a_l = jshard_eval("sqdist", "lse", x, ys, None, scale=0.05, fns=fns)
         d_k, j_k = jshard_eval("sqdist", "argkmin", x, ys, K=4, j_offset=jlo, fns=fns)
-        q.put((rank, a_i.numpy(), a_s.numpy(), a_l.numpy(), d_k.numpy(), j_k.numpy()))
+        # bench.py's j-shard inputs: each rank draws only its slice of y (PCG64 advance)
+        assert np.array_equal(synth.uniform3_rows(N, 5, jlo, jhi), synth.uniform3(N, 5)[jlo:jhi])
+        # bench.py's N > 1 parity sample: seeded rows of each rank's shard, gathered in rank order
+        import bench
+        full = torch.arange(M * 2, dtype=torch.float32).reshape(M, 2)
+        rows, vals = bench.shard_parity_sample(dist, world, rank, lo, full[lo:hi].contiguous(), per=5)
+        plan = bench.gather_rows(dist, world, None, torch.tensor([[float(rank), float(hi - lo)]], dtype=torch.float64))
+        q.put((rank, a_i.numpy(), a_s.numpy(), a_l.numpy(), d_k.numpy(), j_k.numpy(), rows, vals,
+               plan.numpy()))
     finally:
         dist.destroy_process_group()
 
@@ -108,7 +116,14 @@ def test_ishard_jshard_world2():
     a_ref, _ = oracle.gauss_sum(x, y, b, sigma=0.5)
     l_ref, _ = oracle.lse(x, y, None, eps=0.05)
     d_ref, j_ref = oracle.argkmin(x, y, 4)
-    for rank, a_i, a_s, a_l, d_k, j_k in res:
+    full = np.arange(M * 2, dtype=np.float64).reshape(M, 2)
+    for rank, a_i, a_s, a_l, d_k, j_k, rows, vals, plan in res:
+        assert len(rows) == 5 * world and len(set(rows.tolist())) == 5 * world
+        for r in range(world):                                        # 5 rows from each shard
+            lo, hi = M * r // world, M * (r + 1) // world
+            assert np.all((rows[5 * r:5 * r + 5] >= lo) & (rows[5 * r:5 * r + 5] < hi))
+        np.testing.assert_array_equal(vals, full[rows])
+        np.testing.assert_array_equal(plan[:, 0], np.arange(world))
         np.testing.assert_array_equal(a_i, a_ref)                      # i-shard: same rows, same numbers
         np.testing.assert_allclose(a_s, a_ref, rtol=1e-13)            # j-shard Sum: fp64 all-reduce
         np.testing.assert_allclose(a_l, l_ref, rtol=0, atol=1e-12)    # j-shard LSE: max-rescale merge

@@ -185,8 +185,14 @@ def test_lse(G, M, N, hkind):
     h = None if hkind == "zero" else (np.random.default_rng(33).standard_normal(N) * 3).astype(np.float32)
     a = G.eval("sqdist", "lse", dev(x), dev(y), None if h is None else dev(h), scale=0.05,
                out_dtype="float64")
-    o, _ = oracle.lse(x, y, h, eps=0.05)
-    assert_lse_parity(host(a), o, rel=True, what=f"lse {M}x{N} h={hkind}")
+    if h is None:
+        # h = 0, eps = 0.05, D = 3 (the C3 recipe): the plain 1e-6 bar (R6), no floor
+        o, _ = oracle.lse(x, y, None, eps=0.05)
+        assert_lse_parity(host(a), o, what=f"lse {M}x{N} h=0")
+    else:
+        # |h| ~ 3 sigma up to ~10: rows whose dominant exponents are large get the R6b floor
+        o, _, cond = oracle.lse(x, y, h, eps=0.05, cond=True)
+        assert_lse_parity(host(a), o, rel=True, cond=cond, what=f"lse {M}x{N} h={hkind}")
 
 
 @pytest.mark.parametrize("D", [1, 2, 5, 8])
@@ -368,43 +374,6 @@ def _rows(M, n, seed):
     return np.sort(np.concatenate([r, [0, M - 1]]))
 
 
-def test_config2_full_size_sampled(G):
-    c = synth.config(2); sd = synth.seeds(2)
-    x = synth.uniform3(c.M, sd["x"]); y = synth.uniform3(c.N, sd["y"]); b = synth.signal(c.N, sd["b"])
-    s, gr = G.eval("gauss_sum_gradx", "sum", dev(x), dev(y), dev(b), None, scale=c.scale)
-    rows = _rows(c.M, 512, 7)
-    os_, dens = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
-    og, deng = oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
-    assert_sum_parity(host(s)[rows], os_, dens, what="C2 sum")
-    assert_sum_parity(host(gr)[rows], og, deng, what="C2 grad")
-    # separate-kernel path gives the same numbers up to rounding
-    s2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=c.scale)
-    assert_sum_parity(host(s2)[rows], os_, dens, what="C2 sum (separate)")
-
-
-def test_config3_full_size_sampled(G):
-    c = synth.config(3); sd = synth.seeds(3)
-    x = synth.uniform3(c.M, sd["x"]); y = synth.gmm3(c.N, sd["y"])
-    a = G.eval("sqdist", "lse", dev(x), dev(y), None, scale=c.scale, out_dtype="float64")
-    rows = _rows(c.M, 256, 8)
-    o, _ = oracle.lse(x, y, None, eps=c.scale, rows=rows)
-    assert_lse_parity(host(a)[rows], o, what="C3 lse")
-    # all rows: max_j F <= LSE <= max_j F + log N, with max_j F from the GPU's own ArgKMin K=1
-    d, _ = G.eval("sqdist", "argkmin", dev(x), dev(y), K=1)
-    fmax = -host(d)[:, 0].astype(np.float64) / c.scale
-    A = host(a)
-    assert np.all(A >= fmax - 1e-5) and np.all(A <= fmax + math.log(c.N) + 1e-5)
-
-
-def test_config5_full_size_sampled(G):
-    c = synth.config(5); sd = synth.seeds(5)
-    x = synth.uniform3(c.M, sd["x"]); y = synth.uniform3(c.N, sd["y"]); b = synth.signal(c.N, sd["b"])
-    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=c.scale)
-    rows = _rows(c.M, 64, 9)
-    o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
-    assert_sum_parity(host(a)[rows], o, den, what="C5 sum")
-
-
 # ------------------------------------------------------------------------------------------------
 # ArgKMin, large D: tcgen05 3xTF32 screening + exact fp64 re-rank
 # ------------------------------------------------------------------------------------------------
@@ -439,18 +408,6 @@ def test_argkmin_tensor_path_fallback_certificate(G):
     assert host(j)[0].tolist() == list(range(10))
     assert host(j)[69].tolist() == list(range(10))
     argk_check(host(d), host(j), od, oj, 10, what="fallback")
-
-
-def test_config4_full_size_sampled(G):
-    c = synth.config(4); sd = synth.seeds(4)
-    x = synth.mnist784(c.M, sd["x"]); y = synth.mnist784(c.N, sd["y"])
-    d, j = G.eval("sqdist", "argkmin", dev(x), dev(y), K=c.K)
-    plan = G.last_plan()
-    assert plan["path"] == 1 and 0 <= plan["fallback_rows"] <= c.M // 100   # R17 certificate: rare rescans
-    rows = _rows(c.M, 300, 10)
-    od, oj = oracle.argkmin(x, y, c.K + 1, rows=rows)
-    n_idx, n_dist = argk_check(host(d)[rows], host(j)[rows], od, oj, c.K, what="C4")
-    assert n_idx >= 0.95 * len(rows) * c.K
 
 
 # ------------------------------------------------------------------------------------------------
@@ -577,21 +534,15 @@ def test_gauss_sum_tiny_n(G, N):
     (3000, 4100, 1, False, 7),       # forced split, D = 1
     (20000, 20000, 3, True, 3),
 ])
-def test_gauss_tc_path(G, monkeypatch, M, N, D, signed, split):
-    """Opt-in Gaussian Sum with the exponent on the tensor cores (gauss_tc.cu, path 3) against the
-    oracle, and the default FP32 expanded kernel (path 2) on the same inputs."""
+def test_gauss_expanded_path_shapes(G, M, N, D, signed, split):
+    """Gaussian Sum in the default FP32 expanded form (path 2) against the oracle on ragged,
+    degenerate, long-j and forced-split shapes (tiny N or M take the direct form, no bbox)."""
     x = synth.uniform3(M, 91)[:, :D].copy(); y = synth.uniform3(N, 92)[:, :D].copy()
     b = synth.signal(N, 93, signed=signed)
-    monkeypatch.setenv("GENRED_GAUSS_TC", "1")                 # opt-in path
-    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split, out_dtype="float64")
-    plan = G.last_plan()
-    assert plan["path"] == 3, plan
     o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
-    assert_sum_parity(host(a), o, den, what=f"gauss tc {M}x{N} D{D}")
-    monkeypatch.setenv("GENRED_GAUSS_TC", "0")
     a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=split, out_dtype="float64")
-    assert G.last_plan()["path"] == (2 if N > 64 and M > 16 else 0)   # tiny N or M: direct form, no bbox
-    assert_sum_parity(host(a2), o, den, what="gauss fp32 expanded")
+    assert G.last_plan()["path"] == (2 if N > 64 and M > 16 else 0)
+    assert_sum_parity(host(a2), o, den, what=f"gauss fp32 expanded {M}x{N} D{D}")
 
 
 @pytest.mark.parametrize("formula", ["gauss_gradx", "gauss_sum_gradx"])

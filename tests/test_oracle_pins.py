@@ -145,6 +145,39 @@ def test_lattice_lse(shape, eps):
     np.testing.assert_allclose(a, a_cf, rtol=1e-13, atol=1e-12)
 
 
+@pytest.mark.parametrize("shape,sigma", [((7, 6, 5), 0.5), ((5, 5, 4), 1.1)])
+def test_lattice_signed_b_denominator(shape, sigma):
+    """P3 with SIGNED separable weights b_j = w1(k1) w2(k2) w3(k3), w_d(k) in +-{1/4 .. 4}:
+    a_i = prod_d sum_k w_d(k) e_dk, and the R4 denominator S_i = sum_j |b_j| e_ij = prod_d
+    sum_k |w_d(k)| e_dk (|prod w| = prod |w|): pins O1/O2's denominators as sums of |terms|,
+    not |sum of terms| (signed terms cancel in a_i, never in S_i)."""
+    rng = np.random.default_rng(31)
+    nodes = [np.sort(rng.uniform(-0.2, 1.2, n)).astype(np.float32).astype(np.float64) for n in shape]
+    w = [rng.choice([0.25, 0.5, 1.0, 2.0, 4.0], size=n) * rng.choice([-1.0, 1.0], size=n) for n in shape]
+    for d in range(3):
+        w[d][0], w[d][-1] = abs(w[d][0]), -abs(w[d][-1])        # both signs on every axis
+    grids = np.meshgrid(*nodes, indexing="ij")
+    y = np.stack([q.reshape(-1) for q in grids], 1).astype(np.float32)
+    wg = np.meshgrid(*w, indexing="ij")
+    b = np.prod(np.stack([q.reshape(-1) for q in wg], 1), axis=1).astype(np.float32)
+    x = rng.uniform(-0.3, 1.3, (48, 3)).astype(np.float32)
+    X = x.astype(np.float64)
+    s2 = sigma * sigma
+    e = [np.exp(-(X[:, d:d + 1] - nodes[d][None, :]) ** 2 / s2) for d in range(3)]
+    S = np.stack([(w[d][None, :] * e[d]).sum(1) for d in range(3)], 1)
+    Sabs = np.stack([(np.abs(w[d])[None, :] * e[d]).sum(1) for d in range(3)], 1)
+    a, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+    assert np.all(np.abs(a[:, 0] - S.prod(1)) <= 1e-13 * Sabs.prod(1))
+    np.testing.assert_allclose(den[:, 0], Sabs.prod(1), rtol=1e-13)
+    assert np.any(np.abs(S.prod(1)) < 0.5 * Sabs.prod(1))       # the case really cancels
+    # gradient: |T_d| with |w| and |x - g| in the d-th factor, |w| in the others
+    Tabs = np.stack([(np.abs(w[d])[None, :] * (2 / s2) * np.abs(X[:, d:d + 1] - nodes[d][None, :])
+                      * e[d]).sum(1) for d in range(3)], 1)
+    G, gden = oracle.gauss_gradx(x, y, b, None, sigma=sigma)
+    gden_cf = np.stack([Tabs[:, d] * np.prod(np.delete(Sabs, d, axis=1), axis=1) for d in range(3)], 1)
+    np.testing.assert_allclose(gden, gden_cf, rtol=1e-13)
+
+
 def test_lattice_centre_gradient_is_zero():
     """P3: x at the centre of a symmetric lattice with symmetric weights -> grad = 0."""
     g1 = np.array([-1.0, -0.5, 0.0, 0.5, 1.0], np.float32)
