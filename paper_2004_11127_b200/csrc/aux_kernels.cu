@@ -133,10 +133,17 @@ __global__ void __launch_bounds__(256) pack_kernel(int kind, const float *__rest
                 rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;   // w = -|y'|^2
                 for (int e = 0; e < E; ++e)
                     rec[2 * D + 2 + 2 * e + h] = valid ? (b ? bs[jj * E + e] : 1.0f) : 0.0f;
-                if (raw && E == 1 && kGradBY) {                       // b y' (expanded form only)
-                    const float bj = valid ? (b ? bs[jj] : 1.0f) : 0.0f;
-                    for (int d = 0; d < D; ++d)
-                        rec[2 * D + 4 + 2 * d + h] = geo.expanded ? bj * rec[2 * d + h] : 0.0f;
+                if (raw && E == 1 && kGradBY && geo.expanded) {
+                    // gradient records (expanded form): the j factor 2^w is folded into the
+                    // signal, b' = b 2^(-|y'|^2) (fp64, one rounding), and the records carry
+                    // b' y' -- the pair loop's exponent is then u = 2 x'.y' alone (no w term)
+                    const double bj = valid ? (b ? (double)bs[jj] : 1.0) : 0.0;
+                    const float bp = (float)(bj * exp2(-w));
+                    rec[2 * D + h] = 0.0f;
+                    rec[2 * D + 2 + h] = bp;
+                    for (int d = 0; d < D; ++d) rec[2 * D + 4 + 2 * d + h] = bp * rec[2 * d + h];
+                } else if (raw && E == 1 && kGradBY) {
+                    for (int d = 0; d < D; ++d) rec[2 * D + 4 + 2 * d + h] = 0.0f;   // direct form
                 }
                 continue;
             }
@@ -272,10 +279,16 @@ __global__ void pack_ranges_kernel(int kind, const float *__restrict__ y, const 
             if (gauto) rec[2 * D + h] = geo.expanded ? (float)(-w) : 0.0f;
             for (int e = 0; e < E; ++e)
                 rec[boff + 2 * e + h] = valid ? (b ? b[j * E + e] : 1.0f) : 0.0f;
-            if (kind == PACK_GAUSS_AUTO_RAW && E == 1 && kGradBY) {   // b y' (expanded form only)
-                const float bj = valid ? (b ? b[j] : 1.0f) : 0.0f;
-                for (int d = 0; d < D; ++d)
-                    rec[boff + 2 + 2 * d + h] = geo.expanded ? bj * rec[2 * d + h] : 0.0f;
+            if (kind == PACK_GAUSS_AUTO_RAW && E == 1 && kGradBY) {   // b' = b 2^w, b' y' (as pack_kernel)
+                if (geo.expanded) {
+                    const double bj = valid ? (b ? (double)b[j] : 1.0) : 0.0;
+                    const float bp = (float)(bj * exp2(-w));
+                    rec[2 * D + h] = 0.0f;
+                    rec[boff + h] = bp;
+                    for (int d = 0; d < D; ++d) rec[boff + 2 + 2 * d + h] = bp * rec[2 * d + h];
+                } else {
+                    for (int d = 0; d < D; ++d) rec[boff + 2 + 2 * d + h] = 0.0f;
+                }
             }
         }
         const int used = boff + 2 * E + ((kind == PACK_GAUSS_AUTO_RAW && E == 1 && kGradBY) ? 2 * D : 0);

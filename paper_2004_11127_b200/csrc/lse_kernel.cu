@@ -35,6 +35,11 @@ constexpr float kSumMax = 65536.0f;
 #ifndef GENRED_LSE_MINB
 #define GENRED_LSE_MINB 2
 #endif
+// Row-pair packing (as the gradient modes, sum_body.cuh GENRED_GRAD_RP): the packed lanes hold
+// two ROWS, the record's -y_d is a broadcast scalar operand, one j at a time.
+#ifndef GENRED_LSE_RP
+#define GENRED_LSE_RP 1
+#endif
 constexpr int kSub = GENRED_LSE_SUB;  // record pairs per sub-chunk (2 kSub j)
 constexpr int kPromote = 64 / kSub;   // sub-chunks per fp64 promotion (128 j)
 static_assert(kSplitGrain % kSub == 0, "j-splits must hold whole sub-chunks");
@@ -153,6 +158,94 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
         s32[r] = make_float2(0.f, 0.f);
     }
 
+    constexpr bool RP = GENRED_LSE_RP && (R % 2 == 0);
+    if constexpr (RP) {
+    // ---- row-pair mode: lanes = rows (2q, 2q + 1) -------------------------------------------
+    constexpr int RQ = R / 2;
+    float2 X2[RQ][D], NM2[RQ], S32[RQ];
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+#pragma unroll
+        for (int d = 0; d < D; ++d) X2[q][d] = make_float2(xr[2 * q][d], xr[2 * q + 1][d]);
+        NM2[q] = make_float2(-m[2 * q], -m[2 * q + 1]);
+        S32[q] = make_float2(0.f, 0.f);
+    }
+    for (int k = 0; k < nt; ++k) {
+        const float *tile = ring.acquire(k);
+        const int nsc = (k == nt - 1 ? last_np : Cfg::PAIRS) / kSub;     // sub-chunks in this tile
+        for (int sc = 0; sc < nsc; ++sc) {
+            const float *base = tile + sc * kSub * RS;
+            float2 cs[RQ];
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) cs[q] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int pq = 0; pq < kSub; ++pq) {
+                float f[RS];
+#pragma unroll
+                for (int u = 0; u < RS / 4; ++u) {
+                    const float4 v = lds128(base + pq * RS + 4 * u);
+                    f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+                }
+#pragma unroll
+                for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                    for (int q = 0; q < RQ; ++q) {
+                        float2 dd = add2(X2[q][0], dup2(f[h]));              // x - y (raw, R6)
+                        float2 q2 = mul2(dd, dd);
+#pragma unroll
+                        for (int d = 1; d < D; ++d) {
+                            dd = add2(X2[q][d], dup2(f[2 * d + h]));
+                            q2 = fma2(dd, dd, q2);
+                        }
+                        const float2 hm = HZ ? NM2[q] : add2(NM2[q], dup2(f[2 * D + h]));   // h'_hi - m
+                        const float2 t = fma2(q2, negc2, hm);
+                        const float2 e = make_float2(ex2(t.x), ex2(t.y));
+                        cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                if (!(fmaxf(cs[q].x, cs[q].y) <= kSumMax)) {           // rare: per-row rescale
+#pragma unroll
+                    for (int l = 0; l < 2; ++l) {
+                        const int r = 2 * q + l;
+                        const float c = l ? cs[q].y : cs[q].x;
+                        if (c <= kSumMax) {
+                            if (l) S32[q].y += c; else S32[q].x += c;
+                            continue;
+                        }
+                        float xrow[D];
+#pragma unroll
+                        for (int d = 0; d < D; ++d) xrow[d] = l ? X2[q][d].y : X2[q][d].x;
+                        const float sl = l ? S32[q].y : S32[q].x;
+                        const LseRescale rs = lse_rescale<D, HZ, RS>(base, xrow, negc, m[r], s64[r],
+                                                                     make_float2(sl, 0.f));
+                        m[r] = rs.m;
+                        s64[r] = rs.s64;
+                        if (l) { S32[q].y = rs.c1; NM2[q].y = -rs.m; } else { S32[q].x = rs.c1; NM2[q].x = -rs.m; }
+                    }
+                } else {
+                    S32[q] = add2(S32[q], cs[q]);
+                }
+            }
+            if ((sc + 1) % kPromote == 0) {
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) {
+                    s64[2 * q] += (double)S32[q].x;
+                    s64[2 * q + 1] += (double)S32[q].y;
+                    S32[q] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+        ring.release(k);
+    }
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {                 // the (at most) partial last promotion
+        s32[2 * q] = make_float2(S32[q].x, 0.f);
+        s32[2 * q + 1] = make_float2(S32[q].y, 0.f);
+    }
+    } else {
     for (int k = 0; k < nt; ++k) {
         const float *tile = ring.acquire(k);
         const int nsc = (k == nt - 1 ? last_np : Cfg::PAIRS) / kSub;     // sub-chunks in this tile
@@ -218,6 +311,7 @@ __global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const Ls
         }
         ring.release(k);
     }
+    }   // RP
 
 #pragma unroll
     for (int r = 0; r < R; ++r) {

@@ -11,14 +11,31 @@
 
 namespace genred {
 
-// Gradient modes with D + E <= 4 (fused Sum+grad, M = N = 1e5, records carrying b y'): 4 rows per
-// thread, 4 record pairs per iteration, 2 CTAs/SM (128 registers) measured 11.47 pairs/clk/SM;
-// 2 rows / 2 pairs / 3 CTAs 10.78; 4 / 4 / 3 CTAs (80 registers, spilling) 11.23; 4 / 8 11.10.
+// Gradient modes with D + E <= 4 (fused Sum+grad, records carrying b' and b' y'), row-pair mode
+// (GENRED_GRAD_RP): 4 rows per thread and 8 record pairs per iteration at 3 CTAs/SM (80
+// registers; the fp64 tile sums spill to local memory once per 512 j, outside the pair loop)
+// measured 13.34 pairs/clk/SM at M = N = 1e5 and 13.91 at 4e5, against 13.03 / 13.41 at 2 CTAs/SM
+// and 12.42 / 12.94 with 4 record pairs per iteration (B200, round 2).  The j-packed loop of
+// round 1 (4 rows, 4 pairs, 2 CTAs/SM) measured 11.45 / 11.93.  The direct form shares the
+// kernel: 8.92 -> 8.77 pairs/clk/SM at 3 CTAs/SM (4e5, sigma = 0.05).
 #ifndef GENRED_GRAD_R
 #define GENRED_GRAD_R 4
 #endif
 #ifndef GENRED_GRAD_MINB
-#define GENRED_GRAD_MINB 2
+#define GENRED_GRAD_MINB 3
+#endif
+// Row-pair packing of the expanded gradient modes (E = 1, records carrying b' and b' y'): the
+// packed FFMA2 lanes hold two ROWS and the j-record value is a broadcast scalar operand, instead
+// of two j's against a per-row broadcast.  Every FFMA2 then reads one fresh scalar + two register
+// pairs (not three pairs), and the row-pair's exponential is reused by the 1 + D accumulations.
+#ifndef GENRED_GRAD_RP
+#define GENRED_GRAD_RP 1
+#endif
+#ifndef GENRED_SUM_RPD
+#define GENRED_SUM_RPD 1
+#endif
+#ifndef GENRED_GRAD_RP_QOUT
+#define GENRED_GRAD_RP_QOUT 0
 #endif
 // Record pairs per pair-loop iteration of the Sum modes: 4 measured 15.16 pairs/clk/SM against
 // 14.98 for 2 and 15.01 for 8 (Gaussian Sum, M = N = 1e6).
@@ -26,7 +43,7 @@ namespace genred {
 #define GENRED_SUM_HH 4
 #endif
 #ifndef GENRED_GRAD_HH
-#define GENRED_GRAD_HH 4
+#define GENRED_GRAD_HH 8
 #endif
 
 template <int MODE, int D, int E>
@@ -133,6 +150,22 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         s0[r] = make_float2(0.f, 0.f);
         s064[r] = 0.0;
     }
+    // row-pair mode (GENRED_GRAD_RP): X2[q][d] = (2x'_{2q,d}, 2x'_{2q+1,d}); S0p / Sp the fp32
+    // tile sums of e b' and e b' y'_d for the two rows of pair q (lanes x, y)
+    constexpr bool RP = GENRED_GRAD_RP && XP && Cfg::BY && !SMM && (R % 2 == 0);
+    // the same row-pair packing for the direct form of the Gaussian Sum (raw x - y, R18e)
+    constexpr bool RPD = GENRED_SUM_RPD && RAWD && MODE == 0 && E == 1 && !SMM && (R % 2 == 0);
+    constexpr int RQ = (RP || RPD) ? R / 2 : 1;
+    float2 X2[RQ][D], S0p[RQ], Sp[RQ][D];
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) {
+        S0p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            X2[q][d] = (RP || RPD) ? make_float2(xr[2 * q][d], xr[(2 * q + 1) % R][d]) : make_float2(0.f, 0.f);
+            Sp[q][d] = make_float2(0.f, 0.f);
+        }
+    }
 #pragma unroll
     for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -148,6 +181,62 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         // record pairs of this tile: whole tiles, except the range's last one (a multiple of
         // kSplitGrain, so of HH)
         const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
+        if constexpr (RP) {
+        for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+        for (int hh = 0; hh < HH; ++hh) {
+            float f[RS];
+#pragma unroll
+            for (int q = 0; q < RS / 4; ++q) {
+                const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int hq = 0; hq < 2 * RQ; ++hq) {     // the record pair's two j's x the row pairs
+                const int h = GENRED_GRAD_RP_QOUT ? hq % 2 : hq / RQ;
+                const int q = GENRED_GRAD_RP_QOUT ? hq / 2 : hq % RQ;
+                {
+                    float2 u = mul2(X2[q][0], dup2(f[h]));                          // 2 x'.y'
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(X2[q][d], dup2(f[2 * d + h]), u);
+                    const float2 ex = make_float2(ex2(u.x), ex2(u.y));
+                    S0p[q] = fma2(ex, dup2(f[BOFF + h]), S0p[q]);                   // e b'
+#pragma unroll
+                    for (int d = 0; d < D; ++d)
+                        Sp[q][d] = fma2(ex, dup2(f[Cfg::BYOFF + 2 * d + h]), Sp[q][d]);   // e b' y'_d
+                }
+            }
+        }
+        }
+        } else if constexpr (RPD) {
+        for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+        for (int hh = 0; hh < HH; ++hh) {
+            float f[RS];
+#pragma unroll
+            for (int q = 0; q < RS / 4; ++q) {
+                const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) {
+                    float2 dd = add2(X2[q][0], dup2(f[h]));                       // x - y, raw
+                    float2 qq = mul2(dd, dd);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) {
+                        dd = add2(X2[q][d], dup2(f[2 * d + h]));
+                        qq = fma2(dd, dd, qq);
+                    }
+                    const float2 t = mul2(qq, negs2);                               // -s^2 |x - y|^2
+                    const float2 ex = make_float2(ex2(t.x), ex2(t.y));
+                    S0p[q] = fma2(ex, dup2(f[BOFF + h]), S0p[q]);                   // e b
+                }
+            }
+        }
+        }
+        } else {
         for (int pp2 = SMM ? ct : 0; pp2 < np; pp2 += SMM ? kThreads : HH) {
 #pragma unroll
         for (int hh = 0; hh < HH; ++hh) {
@@ -259,8 +348,34 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
             }
         }
         }
+        }   // RP
         ring.release(k);
         // promote the tile's fp32 partials to fp64 (every 512 j)
+        if constexpr (RPD) {
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                acc64[2 * q][0] += (double)S0p[q].x;
+                acc64[2 * q + 1][0] += (double)S0p[q].y;
+                S0p[q] = make_float2(0.f, 0.f);
+            }
+        }
+        if constexpr (RP) {
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                const int r0 = 2 * q, r1 = 2 * q + 1;
+                double &a0 = OWN_S0 ? s064[r0] : acc64[r0][0];
+                double &a1 = OWN_S0 ? s064[r1] : acc64[r1][0];
+                a0 += (double)S0p[q].x;
+                a1 += (double)S0p[q].y;
+                S0p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    acc64[r0][NS + d] += (double)Sp[q][d].x;
+                    acc64[r1][NS + d] += (double)Sp[q][d].y;
+                    Sp[q][d] = make_float2(0.f, 0.f);
+                }
+            }
+        }
 #pragma unroll
         for (int r = 0; r < R; ++r) {
 #pragma unroll
@@ -315,13 +430,26 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
         const int64_t i = SMM ? row0 + r : row0 + r * (kConsumerWarps * 32) + ct;
         if (i >= row_end || (SMM && ct != 0)) continue;
         if constexpr (XP) {
-            const double fac = exp2(-xsq[r]);                  // row factor 2^(-|x'|^2)
+            // row factor 2^(-|x'|^2); in the row-pair mode x' is re-read from X2 (= 2 x', exact),
+            // so neither xr nor xsq stays live through the pair loop
+            double xs2 = 0.0;
+            if constexpr (RP) {
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const double h = 0.5 * (double)((r & 1) ? X2[r >> 1][d].y : X2[r >> 1][d].x);
+                    xs2 += h * h;
+                }
+            } else {
+                xs2 = xsq[r];
+            }
+            const double fac = exp2(-xs2);
             if constexpr (NG > 0) {
                 // sum_j w_ij (x'_i - y'_j) = x'_i S0_i - S_i  (the kernel's d' convention)
                 const double S0 = OWN_S0 ? s064[r] : acc64[r][0];
 #pragma unroll
                 for (int c = 0; c < NG; ++c)
-                    acc64[r][NS + c] = 0.5 * (double)xr[r][c] * S0 - acc64[r][NS + c];
+                    acc64[r][NS + c] = 0.5 * (double)(RP ? ((r & 1) ? X2[r >> 1][c].y : X2[r >> 1][c].x) : xr[r][c]) * S0
+                                       - acc64[r][NS + c];
             }
 #pragma unroll
             for (int c = 0; c < C; ++c) acc64[r][c] *= fac;
