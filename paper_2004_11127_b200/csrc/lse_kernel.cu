@@ -32,8 +32,11 @@ constexpr float kSumMax = 65536.0f;
 #ifndef GENRED_LSE_SUB
 #define GENRED_LSE_SUB 16
 #endif
+// 3 CTAs/SM (80 registers; the spills are outside the pair loop) with the row-pair loop:
+// C3-like LSE (1e6 x 1e6, eps = 0.05) 13.42 -> 13.60 pairs/clk/SM; the j-packed loop of round 1
+// at 2 CTAs/SM measured 12.98 (B200, round 2).
 #ifndef GENRED_LSE_MINB
-#define GENRED_LSE_MINB 2
+#define GENRED_LSE_MINB 3
 #endif
 // Row-pair packing (as the gradient modes, sum_body.cuh GENRED_GRAD_RP): the packed lanes hold
 // two ROWS, the record's -y_d is a broadcast scalar operand, one j at a time.
@@ -113,8 +116,11 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
     return o;
 }
 
+template <int D, int R>
+constexpr int lse_min_blocks() { return (D <= 3 && R % 2 == 0) ? GENRED_LSE_MINB : 2; }
+
 template <int D, int R, bool HZ>
-__global__ void __launch_bounds__(kThreads, GENRED_LSE_MINB) lse_kernel(const LseParams p) {
+__global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>()) lse_kernel(const LseParams p) {
     using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -531,7 +537,7 @@ static int occ_lse() {
     return n > 0 ? n : 1;
 }
 
-// Rows per thread that stay spill-free within 112 registers.
+// Rows per thread (D <= 3: 4 rows at 80 registers, 3 CTAs/SM; else 2 at 2 CTAs/SM).
 template <int D>
 #ifndef GENRED_LSE_R4
 #define GENRED_LSE_R4 1

@@ -32,7 +32,7 @@ namespace genred {
 #define GENRED_GRAD_RP 1
 #endif
 #ifndef GENRED_SUM_RPD
-#define GENRED_SUM_RPD 1
+#define GENRED_SUM_RPD 0
 #endif
 #ifndef GENRED_GRAD_RP_QOUT
 #define GENRED_GRAD_RP_QOUT 0

@@ -527,6 +527,28 @@ def test_gauss_sum_tiny_n(G, N):
     assert_sum_parity(host(a3), o3, den3, what=f"gauss tiny N={N} unaligned x")
 
 
+@pytest.mark.parametrize("case", ["mixed_rows", "wide_y", "far_offset"])
+def test_gauss_sum_tiny_n_rows_and_offsets(G, case):
+    """Edge kernel (tiny N): rows spread beyond the unit cube, a wide y, and clouds far from the
+    origin against the oracle; a row's result does not depend on the tile it falls in (x shifted
+    by 4 rows: bitwise the same rows)."""
+    M, N, sigma = 200_003, 8, 0.5
+    rng = np.random.default_rng(7)
+    x = rng.uniform(-0.5, 1.5, (M, 3)).astype(np.float32)     # some rows outside |x'|^2 <= 6
+    y = synth.uniform3(N, 8); b = synth.signal(N, 9, signed=True)
+    if case == "wide_y":
+        y[0] = [4.0, -3.0, 2.0]
+    if case == "far_offset":
+        x = (x + 1000.0).astype(np.float32); y = (y + 1000.0).astype(np.float32)
+    a = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=sigma, out_dtype="float64"))
+    assert G.last_plan()["path"] == 0
+    rows = np.r_[np.arange(0, M, 173), M - 1]
+    o, den = oracle.gauss_sum(x, y, b, sigma=sigma, rows=rows)
+    assert_sum_parity(a[rows], o, den, what=f"edge per-row form {case}")
+    a4 = host(G.eval("gauss", "sum", dev(x[4:]), dev(y), dev(b), scale=sigma, out_dtype="float64"))
+    np.testing.assert_array_equal(a4, a[4:])
+
+
 @pytest.mark.parametrize("M,N,D,signed,split", [
     (1000, 777, 3, False, 0),        # ragged row tile and j tile
     (128, 256, 3, True, 1),          # exactly one tile
