@@ -506,12 +506,14 @@ def main() -> None:
                                          K=c.K, out=out, out_dtype=w["out_dtype"], out_grad=out_grad,
                                          out_idx=out_idx, j_offset=0)
 
+    call = genred.bound_call(step_args, stream, local)   # ctypes arguments converted once
+
     def step():
         if world > 1:                                   # X1: y (and b) broadcast once per step
             dist.broadcast(yd, src=0)
             if bd is not None:
                 dist.broadcast(bd, src=0)
-        genred.eval_args(step_args, stream=stream, device=local)
+        call()
 
     def barrier():
         torch.cuda.synchronize(dev)
@@ -534,12 +536,26 @@ def main() -> None:
         return float(t.item())
 
     # ---------------- device-resident timed region ----------------
+    # Per-kernel CUDA events (genred_profile) time the dominant kernel for the roofline.  For
+    # steps of >= 5 ms they are recorded inside the timed region itself; for launch-bound steps
+    # (C1: ~6 us of device time per call) two extra events per call would inflate the step they
+    # measure, so the timed region runs without them and the same K steps are then re-run with
+    # them (the "kernel_timing" key says which).
     for _ in range(args.warmup):
         step()
     barrier()
+    # the decision times the LAST warm-up step only (the first call allocates scratch)
+    w0, w1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    w0.record(stream)
+    step()
+    w1.record(stream)
+    barrier()
+    inline_prof = max_over_ranks(w0.elapsed_time(w1)) >= 5.0
     plan = genred.last_plan(local)
-    sampler = ClockSampler(local).start()
-    genred.profile(True, local)
+    sampler = ClockSampler(local)
+    if not os.environ.get("BENCH_NO_SAMPLER"):
+        sampler.start()
+    genred.profile(inline_prof, local)
     l0 = genred.launch_count(local)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
@@ -549,9 +565,18 @@ def main() -> None:
     torch.cuda.synchronize(dev)
     clocks = sampler.stop()
     launches = genred.launch_count(local) - l0
+    if not inline_prof:
+        barrier()
+        genred.profile(True, local)
+        for _ in range(args.steps):
+            step()
+        torch.cuda.synchronize(dev)
     kms = genred.profile_read(local)
     genred.profile(False, local)
     barrier()
+    kernel_timing = ("CUDA events around the main kernel inside the timed region" if inline_prof else
+                     "CUDA events around the main kernel over a second pass of the same K steps "
+                     "(the timed region runs without per-kernel events: the step is launch-bound)")
     ms_total = max_over_ranks(ev0.elapsed_time(ev1))
     launches = int(sum_over_ranks(launches))
     ms_step = ms_total / args.steps
@@ -600,6 +625,8 @@ def main() -> None:
                     "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
                                   f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
                     "pairs_per_launch": Ml * N}
+
+    roofline["kernel_timing"] = kernel_timing
 
     # ---------------- end-to-end: host buffers through the C ABI (H2D + D2H inside) ----------------
     e2e = None

@@ -26,6 +26,11 @@
  *     faults surface at the caller's next synchronisation.
  *   - NaN / Inf inputs propagate under IEEE semantics and are not checked.
  *   - A context is used by one host thread at a time; distinct contexts are independent.
+ *   - Calls on one context must be STREAM-SERIALISED: its scratch arena and its split-merge
+ *     arrival counters (one per row tile, zero at rest, reset by the merging CTA) are shared by
+ *     every call, so two calls in flight at once on different streams -- or concurrent replays
+ *     of a captured graph -- would interleave on them and give wrong results.  For concurrency
+ *     use one context per stream.
  *   - CUDA graphs: once a context's scratch arena has grown to the largest problem (one warm-up
  *     call), device-mode genred_eval neither synchronises nor allocates, so it can be captured
  *     on `stream`.  Captured launches use that arena: while the graph lives, calls on the same
@@ -192,6 +197,18 @@ int64_t genred_launch_count(const genred_ctx *ctx);
  * launch order; it returns the number written (or -1 on a CUDA error). */
 genred_status genred_profile(genred_ctx *ctx, int32_t enable);
 int32_t       genred_profile_read(genred_ctx *ctx, float *ms, int32_t max);
+
+/* Planner switches of a context (defaults read once from the environment at genred_create, so a
+ * call does not scan the environment).  Names:
+ *   "small_fused"  1 (default; env GENRED_SMALL_FUSED): problems with max(M, N) <= 4096, E = 1,
+ *                  D <= 4 run as ONE kernel (CTAs build their own direct-form j-records, split
+ *                  partials merged through distributed shared memory in a cluster, or by the last
+ *                  CTA); 0 keeps the pack + pair-loop kernels (which may take the expanded form).
+ *   "fused_merge"  1 (default; env GENRED_FUSED_MERGE): the last CTA of a row tile merges the
+ *                  split partials inside the pair-loop kernel when they are few; 0 always launches
+ *                  the finalize kernel.
+ * Returns GENRED_E_INVALID for an unknown name; affects later calls on this context only. */
+genred_status genred_set_option(genred_ctx *ctx, const char *name, int64_t value);
 
 #ifdef __cplusplus
 }

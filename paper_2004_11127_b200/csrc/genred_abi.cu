@@ -38,6 +38,8 @@ struct genred_ctx {
     float geo_s = 0.f;
     unsigned *tile_done = nullptr;                             // split-merge arrival counters (zero at rest)
     int64_t tile_done_cap = 0;
+    bool small_fused = true;                                   // genred_set_option("small_fused")
+    bool fused_merge = true;                                   // genred_set_option("fused_merge")
     bool profiling = false;
     std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
     int nprof = 0;
@@ -552,6 +554,43 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // direct form costs nothing and the bounding-box pass over y (a full read of y) is skipped.
         const bool no_box = tiny_n || M <= kDirectMaxM;
         if (no_box) geo = nullptr;
+        // Small problems in ONE launch (C1-like, launch-latency bound; sum_small_kernel): the CTAs
+        // build their own direct-form j-records in shared memory (no pack kernel, no bounding
+        // box), and the split partials are merged in the same kernel.  Option "small_fused" = 0
+        // keeps the pack + pair-loop path (which may take the expanded form).
+        {
+            const int64_t tile_rows = (int64_t)kConsumerWarps * 32 * pl.R;
+            // split <= 8: the split's CTAs form a cluster and merge through distributed shared
+            // memory; else the last-CTA merge through global partials (as sum_kernel)
+            const bool merge_ok = pl.split == 1 || (pl.split <= 8 && kSmallCluster) ||
+                (pl.split <= 32 && ctx->fused_merge && std::min<int64_t>(tile_rows, M) * C * pl.split <= 16384);
+            if (!smm && !tiny_n && E == 1 && D <= 4 && std::max(M, N) <= kFusedBoxMax &&
+                pl.pairs_per_split <= kSmallMaxPairs && merge_ok && ctx->small_fused) {
+                SumLaunch L;
+                L.num_sms = ctx->num_sms;
+                L.mode = mode; L.D = D; L.E = E; L.R = pl.R; L.x = a->x; L.J = nullptr; L.g = a->g; L.M = M;
+                L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv; L.s = sc;
+                L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
+                L.out_grad = a->out_grad; L.part = part; L.geo = nullptr; L.units = nullptr; L.n_units = 0;
+                if (pl.split > 8 || (pl.split > 1 && !kSmallCluster)) {
+                    s = ensure_tile_done(ctx, pl.itiles, st);
+                    if (s != GENRED_OK) return s;
+                    L.tile_done = ctx->tile_done;
+                }
+                int ctas = 0;
+                prof_event(ctx, true, st);
+                e = launch_sum_small(L, a->y, a->b, N, st, &ctas);
+                prof_event(ctx, false, st);
+                if (e != cudaSuccess) return cuda_fail(ctx, e, "small sum kernel");
+                ctx->launches += 1;
+                ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = (int32_t)tile_rows;
+                ctx->plan.ctas = ctas; ctx->plan.kernels = 1; ctx->plan.path = 0;
+                ctx->plan.tile_j = (int32_t)(2 * pl.pairs_per_split);
+                ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
+                ctx->geo_dev = nullptr;
+                return GENRED_OK;
+            }
+        }
         // small problems: the box is reduced inside the pack kernel (one launch fewer)
         const bool boxed_pack = mode != 3 && !no_box && std::max(M, N) <= kFusedBoxMax;
         if (mode != 3 && !no_box && !boxed_pack) {
@@ -589,8 +628,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // and the fused merge must give bitwise its result (i-shards of one problem may take
         // either path).
         const int64_t tile_rows = (int64_t)kConsumerWarps * 32 * pl.R;
-        const char *fmv = getenv("GENRED_FUSED_MERGE");          // "0": always the finalize kernel
-        const bool fused_merge = pl.split > 1 && pl.split <= 32 && !smm && !(fmv && atoi(fmv) == 0) &&
+        const bool fused_merge = pl.split > 1 && pl.split <= 32 && !smm && ctx->fused_merge &&
                                  std::min<int64_t>(tile_rows, M) * C * pl.split <= 16384;
         if (fused_merge) {
             s = ensure_tile_done(ctx, pl.itiles, st);
@@ -811,6 +849,8 @@ genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
     cudaSetDevice(cuda_device);
     int major = 0, minor = 0;
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
+    if (const char *v = getenv("GENRED_SMALL_FUSED")) ctx->small_fused = atoi(v) != 0;
+    if (const char *v = getenv("GENRED_FUSED_MERGE")) ctx->fused_merge = atoi(v) != 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
     cudaSetDevice(prev);
@@ -968,6 +1008,14 @@ genred_status genred_profile(genred_ctx *ctx, int32_t enable) {
     }
     if (prev != ctx->device) cudaSetDevice(prev);
     return GENRED_OK;
+}
+
+genred_status genred_set_option(genred_ctx *ctx, const char *name, int64_t value) {
+    if (!ctx || !name) return GENRED_E_INVALID;
+    const std::string n(name);
+    if (n == "small_fused") { ctx->small_fused = value != 0; return GENRED_OK; }
+    if (n == "fused_merge") { ctx->fused_merge = value != 0; return GENRED_OK; }
+    return fail(ctx, GENRED_E_INVALID, "unknown option '" + n + "'");
 }
 
 int32_t genred_profile_read(genred_ctx *ctx, float *ms, int32_t max) {

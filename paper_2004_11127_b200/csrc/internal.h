@@ -114,6 +114,15 @@ struct SumLaunch {
     int num_sms = 148;        // persistent grid: at most num_sms x occupancy CTAs
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
+// Small problems in one launch (sum_small_kernel, sum_body.cuh): E = 1, D <= 4, j-splits of at
+// most kSmallMaxPairs record pairs (the CTA's records live in shared memory); a.J is unused.
+constexpr int64_t kSmallMaxPairs = 512;
+#ifndef GENRED_SMALL_CLUSTER
+#define GENRED_SMALL_CLUSTER 1
+#endif
+constexpr bool kSmallCluster = GENRED_SMALL_CLUSTER != 0;   // split <= 8: merge through DSMEM
+cudaError_t launch_sum_small(const SumLaunch &a, const float *y, const float *b, int64_t N,
+                             cudaStream_t st, int *ctas);
 // Small-M mode (sum_smm.cu): CTAs of R = sum_smm_rows(mode) rows whose threads split j; grid =
 // ceil(M / R) * split, split-major.  E = 1, D <= 4 only (sum_smm_supported).
 bool sum_smm_supported(int mode, int D, int E);

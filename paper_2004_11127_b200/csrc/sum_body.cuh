@@ -82,6 +82,8 @@ struct SumParams {
     int64_t n_work;           // work units; the persistent grid walks w = blockIdx.x, + gridDim.x, ...
     unsigned *tile_done;      // split > 1, row tiles only: per-row-tile arrival counters (all zero
                               // between calls); the last CTA of a row tile merges its partials
+    double *part_smem = nullptr;   // sum_small_kernel with a cluster merge: this CTA's partials go
+                                   // to its own shared memory, [local row][C], not to `part`
 };
 
 // Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
@@ -99,8 +101,17 @@ constexpr bool kPolyShare = false;
 // themselves (thread t takes pairs t, t + 256, ...); at the end the CTA reduces its fp64 partials
 // with warp shuffles (fixed butterfly order) and a fixed-order sum over the 8 warps, and thread 0
 // runs the epilogue for the R rows.  Used when M is too small to fill the GPU with row tiles.
-template <int MODE, int D, int E, int R, bool XP, bool SMM>
-__device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &ring, int nt, int last_np,
+// A JRing stand-in whose tiles are already resident in shared memory (sum_small_kernel builds the
+// CTA's j-records there itself): acquire returns the tile, release is a no-op.
+struct SmemTiles {
+    const float *base;
+    int tile_floats;
+    __device__ __forceinline__ const float *acquire(int k) const { return base + k * tile_floats; }
+    __device__ __forceinline__ void release(int) const {}
+};
+
+template <int MODE, int D, int E, int R, bool XP, bool SMM, class Ring>
+__device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt, int last_np,
                                          int64_t row0, int64_t row_end, int sp, const Geo &geo) {
     using Cfg = SumCfg<MODE, D, E>;
     constexpr int RS = Cfg::RS, NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C, BOFF = Cfg::BOFF;
@@ -458,6 +469,11 @@ __device__ __forceinline__ void sum_body(const SumParams &p, JRing<kStages> &rin
 #pragma unroll
             for (int c = 0; c < NG; ++c) acc64[r][NS + c] *= (double)p.s;
         }
+        if (p.part_smem) {                                 // cluster merge (sum_small_kernel)
+#pragma unroll
+            for (int c = 0; c < C; ++c) p.part_smem[(i - row0) * C + c] = acc64[r][c];
+            continue;
+        }
         if (p.split > 1) {
             double *dst = p.part + ((int64_t)sp * p.M + i) * C;
 #pragma unroll
@@ -586,5 +602,109 @@ sum_kernel(const SumParams p) {
     }
 }
 
+
+// Small problems in ONE launch (max(M, N) <= kFusedBoxMax, C1-like; launch-latency bound): each
+// CTA builds the direct-form j-records of its own j-split in shared memory straight from y and b
+// (the pack kernel's direct layout: -y raw, w = 0, b; zero records past N), so there is no pack
+// launch and no bounding box (the direct form on raw differences, reading R18e, needs none), runs
+// the unchanged pair loop on them, and the last CTA of each row tile merges the split partials
+// (sum_tile_merge).  The pair arithmetic is that of sum_kernel's direct form.
+// Cluster merge (CL = split <= 8): the split's CTAs of one row tile form a thread-block cluster;
+// each leaves its fp64 partials in its own shared memory, and after a cluster barrier CTA q of
+// the cluster merges rows q, q + S, ... reading every CTA's partials through distributed shared
+// memory in split order 0..S-1 (the finalize kernel's order and arithmetic), then writes the
+// outputs.  No global partials, no arrival counters, no threadfence round trips.
+__device__ __forceinline__ void cluster_barrier() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+__device__ __forceinline__ double ld_dsmem_f64(const double *local, uint32_t rank) {
+    uint32_t a = smem_u32(local), ra;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(ra) : "r"(a), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(ra) : "memory");
+    return v;
+}
+
+template <int MODE, int D, int E, int R>
+__device__ __forceinline__ void sum_cluster_merge(const SumParams &p, const double *part_s, int rank,
+                                                  int64_t row0) {
+    using Cfg = SumCfg<MODE, D, E>;
+    constexpr int NS = Cfg::NS, NG = Cfg::NG, C = Cfg::C;
+    const int64_t rows = min(p.M, row0 + (int64_t)(kConsumerWarps * 32 * R)) - row0;
+    for (int64_t t = (int64_t)rank * blockDim.x + threadIdx.x; t < rows * C; t += (int64_t)p.split * blockDim.x) {
+        const int64_t i = row0 + t / C;
+        const int c = (int)(t % C);
+        double acc = 0.0;
+        for (int q = 0; q < p.split; ++q) acc += ld_dsmem_f64(part_s + t, (uint32_t)q);
+        if (c < NS) {
+            const double v = acc * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i * NS + c] = v;
+            else ((float *)p.out)[i * NS + c] = (float)v;
+        } else if constexpr (NG > 0) {
+            double v = acc * p.scale_grad;
+            if (E == 1 && p.g) v *= (double)__ldg(p.g + i);
+            const int dc = c - NS;
+            if (MODE == 2) p.out_grad[i * D + dc] = (float)v;
+            else if (p.out_f64) ((double *)p.out)[i * D + dc] = v;
+            else ((float *)p.out)[i * D + dc] = (float)v;
+        }
+    }
+}
+
+template <int MODE, int D, int E, int R>
+__global__ void __launch_bounds__(kThreads, 2)
+sum_small_kernel(SumParams p, const float *__restrict__ y, const float *__restrict__ b, int64_t N,
+                 int cluster_merge) {
+    using Cfg = SumCfg<MODE, D, E>;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    // [cluster partials: kThreads R rows x C fp64][j-records]
+    double *part_s = reinterpret_cast<double *>(smem_raw);
+    float *recs = reinterpret_cast<float *>(smem_raw + (cluster_merge ? kThreads * R * Cfg::C * 8 : 0));
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t q0 = (int64_t)sp * p.pairs_per_split;
+    const int npc = (int)max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    // this thread's x rows: prefetched into L1 now, so the pair loop's loads do not add a second
+    // memory round trip after the j-records'
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + threadIdx.x;
+        if (i < p.M) asm volatile("prefetch.global.L1 [%0];" ::"l"(p.x + i * D));
+    }
+    // one pass: thread t builds whole record pairs t, t + 256, ... (zeros past N and in the pad)
+    for (int pp = threadIdx.x; pp < npc; pp += kThreads) {
+        float rec[Cfg::RS];
+#pragma unroll
+        for (int k = 0; k < Cfg::RS; ++k) rec[k] = 0.0f;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int64_t j = 2 * (q0 + pp) + h;
+            if (j >= N) continue;                          // zero record: contributes nothing
+#pragma unroll
+            for (int d = 0; d < D; ++d) rec[2 * d + h] = -__ldg(y + j * D + d);
+#pragma unroll
+            for (int e = 0; e < E; ++e) rec[Cfg::BOFF + 2 * e + h] = b ? __ldg(b + j * E + e) : 1.0f;
+        }
+        float4 *dst = reinterpret_cast<float4 *>(recs + pp * Cfg::RS);
+#pragma unroll
+        for (int q = 0; q < Cfg::RS / 4; ++q) dst[q] = make_float4(rec[4 * q], rec[4 * q + 1], rec[4 * q + 2], rec[4 * q + 3]);
+    }
+    __syncthreads();
+    const int nt = (npc + Cfg::PAIRS - 1) / Cfg::PAIRS;
+    const int last_np = npc - (nt > 0 ? nt - 1 : 0) * Cfg::PAIRS;
+    SmemTiles ring{recs, Cfg::TILE_FLOATS};
+    Geo geo{};
+    geo.expanded = false;
+    if (cluster_merge) p.part_smem = part_s;
+    sum_body<MODE, D, E, R, false, false>(p, ring, nt, last_np, row0, p.M, sp, geo);
+    if (cluster_merge) {
+        cluster_barrier();                             // every CTA's partials are in its smem
+        sum_cluster_merge<MODE, D, E, R>(p, part_s, sp, row0);
+        cluster_barrier();                             // no CTA leaves while others read its smem
+    } else if (p.tile_done) {
+        sum_tile_merge<MODE, D, E, R>(p, itile, row0, p.M);
+    }
+}
 
 }  // namespace genred

@@ -140,6 +140,81 @@ static int occ_sum_d(int D, int E, int R) {
     return 1;
 }
 
+template <int MODE, int D, int R>
+static cudaError_t run_sum_small(const SumLaunch &a, const float *y, const float *b, int64_t N,
+                                 cudaStream_t st, int *ctas) {
+    using Cfg = SumCfg<MODE, D, 1>;
+    SumParams p;
+    p.x = a.x; p.J = nullptr; p.g = a.g; p.M = a.M; p.split = a.split;
+    p.pairs_per_split = a.pairs_per_split; p.npv = a.npv; p.s = a.s;
+    p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
+    p.out_grad = a.out_grad; p.part = a.part; p.geo = nullptr; p.units = nullptr;
+    p.tile_done = a.split > 1 ? a.tile_done : nullptr;
+    const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
+    const int64_t itiles = (a.M + rows - 1) / rows;
+    p.n_work = itiles * a.split;
+    *ctas = (int)p.n_work;
+    if (p.n_work == 0) return cudaSuccess;
+    // cluster merge through distributed shared memory for split <= 8 (portable cluster size)
+    const int cl = (a.split > 1 && a.split <= 8 && kSmallCluster) ? 1 : 0;
+    const int smem = (int)(a.pairs_per_split * Cfg::RS * 4) + (cl ? kThreads * R * Cfg::C * 8 : 0);
+    auto kern = sum_small_kernel<MODE, D, 1, R>;
+    if (smem > 48 * 1024) {
+        const cudaError_t e = smem_opt_in((const void *)kern, smem);
+        if (e != cudaSuccess) return e;
+    }
+    if (!cl) {
+        kern<<<(unsigned)p.n_work, kThreads, smem, st>>>(p, y, b, N, 0);
+        return cudaGetLastError();
+    }
+    p.tile_done = nullptr;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.n_work);
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = (unsigned)a.split;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const cudaError_t e = cudaLaunchKernelEx(&cfg, kern, p, y, b, N, 1);
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+template <int MODE, int D>
+static cudaError_t run_sum_small_r(const SumLaunch &a, const float *y, const float *b, int64_t N,
+                                   cudaStream_t st, int *ctas) {
+    constexpr int RM = sum_rmax<MODE, D, 1>();
+    return a.R == 1 ? run_sum_small<MODE, D, 1>(a, y, b, N, st, ctas) : run_sum_small<MODE, D, RM>(a, y, b, N, st, ctas);
+}
+
+template <int MODE>
+static cudaError_t run_sum_small_d(const SumLaunch &a, const float *y, const float *b, int64_t N,
+                                   cudaStream_t st, int *ctas) {
+    switch (a.D) {
+        case 1: return run_sum_small_r<MODE, 1>(a, y, b, N, st, ctas);
+        case 2: return run_sum_small_r<MODE, 2>(a, y, b, N, st, ctas);
+        case 3: return run_sum_small_r<MODE, 3>(a, y, b, N, st, ctas);
+        case 4: return run_sum_small_r<MODE, 4>(a, y, b, N, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_sum_small(const SumLaunch &a, const float *y, const float *b, int64_t N,
+                             cudaStream_t st, int *ctas) {
+    if (a.E != 1 || a.pairs_per_split > kSmallMaxPairs) return cudaErrorInvalidValue;
+    switch (a.mode) {
+        case 0: return run_sum_small_d<0>(a, y, b, N, st, ctas);
+        case 1: return run_sum_small_d<1>(a, y, b, N, st, ctas);
+        case 2: return run_sum_small_d<2>(a, y, b, N, st, ctas);
+        case 3: return run_sum_small_d<3>(a, y, b, N, st, ctas);
+    }
+    return cudaErrorInvalidValue;
+}
+
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     switch (a.mode) {
         case 0: return run_sum_d<0>(a, st, ctas);

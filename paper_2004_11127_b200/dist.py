@@ -4,7 +4,10 @@ SURVEY.md Sec. 8(e).  Eq. (1) shards along either axis:
 
 * ``ishard_eval`` (default, north star (d)): rank r owns rows [rM/G, (r+1)M/G) of x; y and b are
   broadcast once from ``src`` (collective X1) and every rank runs libgenred on its rows.  No
-  reduction is needed; per-row arithmetic is identical to the single-GPU run (same j-tiling).
+  reduction is needed.  Per-row arithmetic is bitwise that of the single-GPU run only when every
+  shard runs the same j-split (pass the same ``split_j`` to all ranks: the automatic planner
+  chooses it from the local M) and the same form (shards of a problem with max(M, N) > 4096 all
+  take the pair-loop kernels; the one-launch small-problem path takes the direct form).
 * ``jshard_eval`` (M << N): rank r owns [rN/G, (r+1)N/G) of y and b; every rank reduces all M rows
   over its slice and the monoid states are merged:
     Sum      fp64 partials -> all_reduce(SUM)                                        (X3)

@@ -109,6 +109,8 @@ def load():
         lib.genred_profile.restype = I32
         lib.genred_profile_read.argtypes = [P, P, I32]
         lib.genred_profile_read.restype = I32
+        lib.genred_set_option.argtypes = [P, ctypes.c_char_p, I64]
+        lib.genred_set_option.restype = I32
         if lib.genred_abi_version() != ABI_VERSION:
             raise RuntimeError("libgenred ABI version mismatch")
         _lib = lib
@@ -284,6 +286,30 @@ def prepare(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float 
     else:
         res = out
     return a, res, keep
+
+
+def set_option(name: str, value: int, device: int | None = None) -> None:
+    """genred_set_option on the device's context ("small_fused", "fused_merge")."""
+    ctx = context(device)
+    st = load().genred_set_option(ctx, name.encode(), int(value))
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+
+
+def bound_call(args: Args, stream, device: int | None = None):
+    """A zero-argument callable repeating genred_eval(ctx, args, stream) with every ctypes
+    argument converted once (the benchmark's timed loops: launch-latency-bound shapes)."""
+    fn = load().genred_eval
+    ctx = context(device)
+    ref = ctypes.byref(args)
+    sptr = ctypes.c_void_p(stream.cuda_stream) if args.memory == MEM_DEVICE else None
+    err = load().genred_last_error
+
+    def call():
+        st = fn(ctx, ref, sptr)
+        if st:
+            raise GenredError(st, err(ctx).decode())
+    return call
 
 
 def eval_args(args: Args, stream=None, device: int | None = None) -> None:

@@ -33,6 +33,22 @@ def dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).cuda()
 
 
+def option(G, monkeypatch, name, value):
+    """genred_set_option on the test context for this test only (restored to 1 afterwards)."""
+    G.set_option(name, value)
+    _RESTORE.append(name)
+
+
+_RESTORE = []
+
+
+@pytest.fixture(autouse=True)
+def _restore_options(G):
+    yield
+    while _RESTORE:
+        G.set_option(_RESTORE.pop(), 1)
+
+
 def host(t):
     return t.detach().cpu().numpy()
 
@@ -527,6 +543,47 @@ def test_gauss_sum_tiny_n(G, N):
     assert_sum_parity(host(a3), o3, den3, what=f"gauss tiny N={N} unaligned x")
 
 
+@pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
+@pytest.mark.parametrize("M,N,D,split", [(1000, 1000, 3, 0), (1000, 1000, 3, 1), (300, 4096, 2, 0),
+                                         (4096, 77, 1, 0), (777, 3001, 4, 5), (65, 1500, 3, 0),
+                                         (2000, 1000, 3, 32)])
+def test_small_problem_one_launch(G, monkeypatch, formula, M, N, D, split):
+    """max(M, N) <= 4096 (C1-like): ONE kernel (sum_small_kernel: the CTAs build their own
+    direct-form j-records, last-CTA split merge) against the oracle, against the two-launch path
+    on the same inputs, and bitwise run to run."""
+    rng = np.random.default_rng(M + N + D + split)
+    x = rng.random((M, D)).astype(np.float32); y = rng.random((N, D)).astype(np.float32)
+    b = rng.standard_normal((N, 1)).astype(np.float32)
+    args = (formula, "sum", dev(x), dev(y), dev(b))
+    r1 = G.eval(*args, scale=0.5, split_j=split)
+    plan = G.last_plan()
+    if plan["kernels"] != 1:       # not eligible (the last-CTA merge would read > 16 K partials)
+        assert plan["split_j"] > 8, plan
+    else:
+        assert plan["path"] == 0, plan
+    r1b = G.eval(*args, scale=0.5, split_j=split)
+    option(G, monkeypatch, "small_fused", 0)
+    r2 = G.eval(*args, scale=0.5, split_j=split)
+    assert G.last_plan()["kernels"] >= 2
+    if (M, N) == (1000, 1000):
+        assert plan["kernels"] == 1, plan                  # C1: one launch
+    outs = lambda r: [host(t) for t in (r if isinstance(r, tuple) else (r,))]
+    for a1, a1b in zip(outs(r1), outs(r1b)):
+        np.testing.assert_array_equal(a1, a1b)
+    if formula == "sqdist":
+        o, den = oracle.sqdist_sum(x, y, b)
+        assert_sum_parity(outs(r1)[0], o, den, what=f"small sqdist {M}x{N}")
+        return
+    ores = []
+    if formula in ("gauss", "gauss_sum_gradx"):
+        ores.append(oracle.gauss_sum(x, y, b, sigma=0.5))
+    if formula in ("gauss_gradx", "gauss_sum_gradx"):
+        ores.append(oracle.gauss_gradx(x, y, b, None, sigma=0.5))
+    for a1, a2, (o, den) in zip(outs(r1), outs(r2), ores):
+        assert_sum_parity(a1, o, den, what=f"small {formula} {M}x{N} D={D} split={split}")
+        assert_sum_parity(a2, o, den, what=f"two-launch {formula} {M}x{N}")
+
+
 @pytest.mark.parametrize("case", ["mixed_rows", "wide_y", "far_offset"])
 def test_gauss_sum_tiny_n_rows_and_offsets(G, case):
     """Edge kernel (tiny N): rows spread beyond the unit cube, a wide y, and clouds far from the
@@ -558,9 +615,11 @@ def test_gauss_sum_tiny_n_rows_and_offsets(G, case):
     (3000, 4100, 1, False, 7),       # forced split, D = 1
     (20000, 20000, 3, True, 3),
 ])
-def test_gauss_expanded_path_shapes(G, M, N, D, signed, split):
+def test_gauss_expanded_path_shapes(G, monkeypatch, M, N, D, signed, split):
     """Gaussian Sum in the default FP32 expanded form (path 2) against the oracle on ragged,
-    degenerate, long-j and forced-split shapes (tiny N or M take the direct form, no bbox)."""
+    degenerate, long-j and forced-split shapes (tiny N or M take the direct form, no bbox).  The
+    one-launch small-problem path is switched off here (it always takes the direct form)."""
+    option(G, monkeypatch, "small_fused", 0)
     x = synth.uniform3(M, 91)[:, :D].copy(); y = synth.uniform3(N, 92)[:, :D].copy()
     b = synth.signal(N, 93, signed=signed)
     o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
@@ -571,9 +630,10 @@ def test_gauss_expanded_path_shapes(G, M, N, D, signed, split):
 
 @pytest.mark.parametrize("formula", ["gauss_gradx", "gauss_sum_gradx"])
 @pytest.mark.parametrize("case", ["expanded", "far_offset", "direct", "E2_g"])
-def test_gradient_expanded_and_direct_paths(G, formula, case):
+def test_gradient_expanded_and_direct_paths(G, monkeypatch, formula, case):
     """Gradient in the expanded form uses x' S0 - S (sum of w y'): checked against the oracle on
-    both sides of the device-side path decision."""
+    both sides of the device-side path decision (the one-launch small path switched off)."""
+    option(G, monkeypatch, "small_fused", 0)
     M, N, sigma, E = 2500, 3100, 0.5, 1
     x = synth.gmm3(M, 71); y = synth.gmm3(N, 72)
     if case == "far_offset":
@@ -1021,11 +1081,14 @@ def test_randomized_hard_inputs(G, seed):
 @pytest.mark.parametrize("formula,E,g", [("gauss", 1, False), ("gauss", 2, False),
                                          ("gauss_gradx", 1, True), ("gauss_sum_gradx", 1, True),
                                          ("gauss_sum_gradx", 2, True)])
-@pytest.mark.parametrize("M,N,split", [(1000, 1000, 0), (2500, 3100, 5), (700, 20000, 0)])
+@pytest.mark.parametrize("M,N,split", [(1000, 1000, 0), (2500, 3100, 5), (700, 20000, 0), (64, 20000, 64)])
 def test_fused_split_merge_bitwise(G, monkeypatch, formula, E, g, M, N, split):
     """The last-CTA split merge inside the pair-loop kernel (DESIGN a7/a8) sums the partials in
     the finalize kernel's order: bitwise equal to the two-kernel path, one launch fewer, and the
-    arrival counters are back at zero after every call (repeated calls are bitwise equal)."""
+    arrival counters are back at zero after every call (repeated calls are bitwise equal).  Above
+    32 splits the merge is never fused (the finalize kernel sums lane-strided there).  (The
+    one-launch small-problem path is switched off: it takes the direct form.)"""
+    option(G, monkeypatch, "small_fused", 0)
     x = synth.uniform3(M, 501); y = synth.uniform3(N, 502)
     b = synth.signal(N, 503, E=E, signed=True)
     gg = dev(synth.cotangent(M, 504, E=E)) if g else None
@@ -1035,19 +1098,51 @@ def test_fused_split_merge_bitwise(G, monkeypatch, formula, E, g, M, N, split):
         r = r if isinstance(r, tuple) else (r,)
         return [host(t) for t in r], G.last_plan()
 
-    monkeypatch.setenv("GENRED_FUSED_MERGE", "0")
+    option(G, monkeypatch, "fused_merge", 0)
     ref, p0 = run()
-    monkeypatch.setenv("GENRED_FUSED_MERGE", "1")
+    option(G, monkeypatch, "fused_merge", 1)
     got, p1 = run()
     again, _ = run()
     assert p0["split_j"] == p1["split_j"] > 1, (p0, p1)
     fused = p1["kernels"] == p0["kernels"] - 1         # tiles with <= 16 K partials merge in-kernel
     assert fused or p1["kernels"] == p0["kernels"], (p0, p1)
     if (M, N) == (1000, 1000):
-        assert fused and p1["kernels"] == 2, p1        # C1: pack (+ box) and the pair loop
+        assert fused and p1["kernels"] == 2, p1        # pack (+ box) and the pair loop
+    if split > 32:
+        assert not fused, (p0, p1)
     for a, c, d in zip(ref, got, again):
         np.testing.assert_array_equal(a, c)
         np.testing.assert_array_equal(c, d)
     if formula == "gauss":
         o, den = oracle.gauss_sum(x, y, b, sigma=0.5)
         assert_sum_parity(got[0], o, den, what=f"fused merge {M}x{N}")
+
+
+def test_fused_merge_fresh_context_nonblocking_stream(G, monkeypatch):
+    """the split-merge arrival counters of a NEW context are zeroed on the caller's
+    stream (cudaMemsetAsync), so the first call on a fresh non-blocking stream merges correctly:
+    bitwise equal to the default context's result, and again on the second call."""
+    import ctypes
+    option(G, monkeypatch, "small_fused", 0)
+    M, N = 2500, 3100
+    x = dev(synth.uniform3(M, 601)); y = dev(synth.uniform3(N, 602)); b = dev(synth.signal(N, 603))
+    ref = host(G.eval("gauss", "sum", x, y, b, scale=0.5, split_j=5))
+    lib = G.load()
+    h = ctypes.c_void_p()
+    assert lib.genred_create(0, ctypes.byref(h)) == G.OK
+    assert lib.genred_set_option(h, b"small_fused", 0) == G.OK
+    assert lib.genred_set_option(h, b"no_such_option", 0) == G.E_INVALID
+    try:
+        st = torch.cuda.Stream()                              # non-blocking w.r.t. the legacy stream
+        for _ in range(2):
+            out = torch.full((M, 1), float("nan"), device="cuda")
+            args, _, keep = G.prepare("gauss", "sum", x, y, b, None, scale=0.5, out=out, split_j=5)
+            with torch.cuda.stream(st):
+                assert lib.genred_eval(h, ctypes.byref(args), ctypes.c_void_p(st.cuda_stream)) == G.OK
+            st.synchronize()
+            plan = G.Plan()
+            lib.genred_last_plan(h, ctypes.byref(plan))
+            assert plan.kernels == 2 and plan.split_j == 5       # pack + pair loop with the fused merge
+            np.testing.assert_array_equal(host(out), ref)
+    finally:
+        lib.genred_destroy(h)
