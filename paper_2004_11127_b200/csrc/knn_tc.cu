@@ -367,22 +367,69 @@ __device__ __forceinline__ float rna_tf32(float v) {
     return __uint_as_float(r);
 }
 
+// Also does the call's initialisation (folded in to spare stream operations): with `init` (the
+// x call, which runs first) it sets every row threshold to 3.4e38 and zeroes the max-norm word
+// and the fallback counters that the later kernels of this call accumulate into.
+struct SplitInit {
+    unsigned int *row_thr; int64_t M;           // per-row K'-th-best thresholds -> 0x7f7f7f7f
+    unsigned int *maxnorm; int *fb_count;        // -> 0
+    unsigned int *fb_done; int fb_cap;           // -> 0
+};
+
 __global__ void split_kernel(const float *__restrict__ src, int64_t rows, int D, int Dp,
                              float *__restrict__ hi, float *__restrict__ lo, float *__restrict__ nrm,
-                             unsigned int *maxnorm_bits) {
-    // one warp per row
-    const int64_t w = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+                             unsigned int *maxnorm_bits, SplitInit init) {
+    const int64_t gt = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t gs = (int64_t)gridDim.x * blockDim.x;
+    if (init.row_thr) {
+        for (int64_t k = gt; k < init.M; k += gs) init.row_thr[k] = 0x7f7f7f7fu;
+        if (gt == 0) { *init.maxnorm = 0u; *init.fb_count = 0; }
+        for (int64_t k = gt; k < init.fb_cap; k += gs) init.fb_done[k] = 0u;
+    }
+    // one warp per row; float4 loads and stores when rows are 16-byte multiples (D % 4 == 0)
+    const int64_t w = gt >> 5;
     const int lane = threadIdx.x & 31;
-    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t nw = gs >> 5;
+    const bool vec = (D & 3) == 0 && (((uintptr_t)src) & 15) == 0;
     for (int64_t i = w; i < rows; i += nw) {
         double s = 0.0;
-        for (int k = lane; k < Dp; k += 32) {
-            const float v = k < D ? src[i * D + k] : 0.0f;
-            const float h = rna_tf32(v);
-            const float l = rna_tf32(v - h);
-            hi[i * Dp + k] = h;
-            lo[i * Dp + k] = l;
-            s += (double)v * (double)v;
+        if (vec) {
+            // all of a lane's float4 of the row (up to 7 x 32: D <= 896 in one pass) are loaded
+            // before any is converted: ~3.5 KB per warp in flight instead of 512 B
+            constexpr int U = 7;
+            const float4 *s4 = reinterpret_cast<const float4 *>(src + i * D);
+            float4 *h4 = reinterpret_cast<float4 *>(hi + i * Dp);
+            float4 *l4 = reinterpret_cast<float4 *>(lo + i * Dp);
+            for (int base = 0; base < Dp / 4; base += 32 * U) {
+                float4 v[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = base + lane + 32 * u;
+                    v[u] = k < D / 4 ? __ldg(s4 + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int k = base + lane + 32 * u;
+                    if (k >= Dp / 4) break;
+                    float4 h, l;
+                    h.x = rna_tf32(v[u].x); h.y = rna_tf32(v[u].y); h.z = rna_tf32(v[u].z); h.w = rna_tf32(v[u].w);
+                    l.x = rna_tf32(v[u].x - h.x); l.y = rna_tf32(v[u].y - h.y);
+                    l.z = rna_tf32(v[u].z - h.z); l.w = rna_tf32(v[u].w - h.w);
+                    h4[k] = h;
+                    l4[k] = l;
+                    s += (double)v[u].x * (double)v[u].x + (double)v[u].y * (double)v[u].y +
+                         (double)v[u].z * (double)v[u].z + (double)v[u].w * (double)v[u].w;
+                }
+            }
+        } else {
+            for (int k = lane; k < Dp; k += 32) {
+                const float v = k < D ? src[i * D + k] : 0.0f;
+                const float h = rna_tf32(v);
+                const float l = rna_tf32(v - h);
+                hi[i * Dp + k] = h;
+                lo[i * Dp + k] = l;
+                s += (double)v * (double)v;
+            }
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
@@ -468,37 +515,88 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
         }
     }
     __syncwarp();
-    // exact fp64 distances of the K' candidates (direct differences, never expanded)
-    for (int k = 0; k < KP; ++k) {
-        const int32_t j = s_j[wl][k];
-        double s = 0.0;
-        if (j >= 0) {
+    // exact fp64 distances (direct differences, never expanded) of the candidates that can still
+    // be in the top K: d~_(k) <= d~_(K) + 2 delta (a candidate above that has a true distance >
+    // d~_(K) + delta >= the true distance of each of the K best screened ones, so it cannot be
+    // among the K nearest); all candidates' y rows are read together (one load of x, up to K'
+    // independent loads of y per step: the rows are scattered, so memory-level parallelism, not
+    // arithmetic, sets this kernel's time)
+    {
+        const float ymax = __uint_as_float(*maxnorm_bits);
+        const double xnorm = sqrt((double)xn[i]);
+        const double delta = 3.0 * D * ldexp(1.0, -23) * xnorm * ymax +
+                             ldexp(1.0, -22) * ((double)xn[i] + (double)ymax * ymax);
+        const double dK = (double)s_d[wl][K - 1];
+        int32_t jj[KP];
+        bool use[KP];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) {
+            jj[k] = s_j[wl][k];
+            use[k] = jj[k] >= 0 && (k < K || (double)s_d[wl][k] <= dK + 2.0 * delta);
+        }
+        double acc[KP];
+#pragma unroll
+        for (int k = 0; k < KP; ++k) acc[k] = 0.0;
+        if ((D & 3) == 0 && ((((uintptr_t)x) | ((uintptr_t)y)) & 15) == 0) {
+            const float4 *x4 = reinterpret_cast<const float4 *>(x + i * D);
+            for (int c = lane; c < D / 4; c += 32) {
+                const float4 xv = __ldg(x4 + c);
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    if (!use[k]) continue;
+                    const float4 yv = __ldg(reinterpret_cast<const float4 *>(y + (int64_t)jj[k] * D) + c);
+                    const double d0 = (double)xv.x - (double)yv.x, d1 = (double)xv.y - (double)yv.y;
+                    const double d2 = (double)xv.z - (double)yv.z, d3 = (double)xv.w - (double)yv.w;
+                    acc[k] = fma(d3, d3, fma(d2, d2, fma(d1, d1, fma(d0, d0, acc[k]))));
+                }
+            }
+        } else {
             for (int c = lane; c < D; c += 32) {
-                const double dv = (double)x[i * D + c] - (double)y[(int64_t)j * D + c];
-                s = fma(dv, dv, s);
+                const double xv = (double)x[i * D + c];
+#pragma unroll
+                for (int k = 0; k < KP; ++k) {
+                    if (!use[k]) continue;
+                    const double dv = xv - (double)y[(int64_t)jj[k] * D + c];
+                    acc[k] = fma(dv, dv, acc[k]);
+                }
             }
         }
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-        if (lane == 0) s_e[wl][k] = j >= 0 ? s : INFINITY;
+        for (int k = 0; k < KP; ++k) {
+            double v = acc[k];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0) s_e[wl][k] = use[k] ? v : INFINITY;
+        }
     }
     __syncwarp();
-    if (lane == 0) {
-        // sort candidates by (exact d, j) and emit K
-        double ed[KP];
-        int32_t ej[KP];
-        for (int k = 0; k < KP; ++k) { ed[k] = s_e[wl][k]; ej[k] = s_j[wl][k]; }
-        for (int a = 1; a < KP; ++a) {
-            const double vd = ed[a]; const int32_t vj = ej[a];
-            int b = a;
-            while (b > 0 && (vd < ed[b - 1] || (vd == ed[b - 1] && (uint32_t)vj < (uint32_t)ej[b - 1]))) {
-                ed[b] = ed[b - 1]; ej[b] = ej[b - 1]; --b;
+    // emit the K best by (exact d, j): lane k < K' computes candidate k's rank (the number of
+    // candidates before it in that order; (d, j) pairs are distinct) and writes it to slot rank
+    // if rank < K -- all lanes at once instead of a serial sort on lane 0; unused slots (fewer
+    // than K candidates) get the (+inf, -1) padding
+    {
+        const double myd = lane < KP ? s_e[wl][lane] : INFINITY;
+        const int32_t myj = lane < KP ? s_j[wl][lane] : -1;
+        const uint32_t myju = (uint32_t)myj;                  // -1 (no candidate) sorts last
+        int rank = 0;
+        bool valid = lane < KP && myj >= 0 && myd < INFINITY;
+        if (valid) {
+#pragma unroll
+            for (int k = 0; k < KP; ++k) {
+                const double od = s_e[wl][k];
+                const uint32_t oj = (uint32_t)s_j[wl][k];
+                if (s_j[wl][k] >= 0 && (od < myd || (od == myd && oj < myju))) ++rank;
             }
-            ed[b] = vd; ej[b] = vj;
         }
-        for (int k = 0; k < K; ++k) {
-            dist[i * K + k] = ej[k] >= 0 ? (float)ed[k] : INFINITY;
-            idx[i * K + k] = ej[k] >= 0 ? (int64_t)ej[k] + j_offset : -1;
+        const unsigned vmask = __ballot_sync(0xffffffffu, valid);
+        const int nvalid = __popc(vmask);
+        if (valid && rank < K) {
+            dist[i * K + rank] = (float)myd;
+            idx[i * K + rank] = (int64_t)myj + j_offset;
+        }
+        for (int k = nvalid + lane; k < K; k += 32) {
+            dist[i * K + k] = INFINITY;
+            idx[i * K + k] = -1;
         }
     }
 }
@@ -774,9 +872,10 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     int *fb_count = (int *)s;
 
     int kernels = 0;
-    if ((e = cudaMemsetAsync(ymax, 0, 64, st)) != cudaSuccess) return e;
-    tc::split_kernel<<<(unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16), 256, 0, st>>>(a.x, M, D, Dp, xhi, xlo, xn, nullptr);
-    tc::split_kernel<<<(unsigned)std::min<int64_t>((N + 7) / 8, 148 * 16), 256, 0, st>>>(a.y, N, D, Dp, yhi, ylo, yn, ymax);
+    // the x split also initialises row_thr, ymax, fb_count and fb_done (no memset launches)
+    tc::SplitInit ini{row_thr, M, ymax, fb_count, fb_done, tc::FB_CAP};
+    tc::split_kernel<<<(unsigned)std::min<int64_t>((M + 7) / 8, 148 * 16), 256, 0, st>>>(a.x, M, D, Dp, xhi, xlo, xn, nullptr, ini);
+    tc::split_kernel<<<(unsigned)std::min<int64_t>((N + 7) / 8, 148 * 16), 256, 0, st>>>(a.y, N, D, Dp, yhi, ylo, yn, ymax, tc::SplitInit{});
     kernels += 2;
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
 
@@ -790,7 +889,6 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     p.M = M; p.N = N; p.Dp = Dp; p.nk = Dp / tc::BK; p.n_rtiles = n_rtiles; p.n_ttiles = n_ttiles;
     p.n_groups = n_groups; p.group = group; p.xn = xn; p.yn = yn; p.pd = pd; p.pj = pj;
     p.row_thr = row_thr;
-    if ((e = cudaMemsetAsync(row_thr, 0x7f, (size_t)M * 4, st)) != cudaSuccess) return e;   // 3.4e38
     const int n_units = n_groups * ((n_rtiles + CL - 1) / CL);
     const int grid = std::min(n_units, a.num_sms / CL) * CL;
     if (a.ev_start) cudaEventRecord(a.ev_start, st);
@@ -798,7 +896,6 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     if (a.ev_stop) cudaEventRecord(a.ev_stop, st);
     if (e != cudaSuccess) return e;
     kernels += 1;
-    if ((e = cudaMemsetAsync(fb_count, 0, 4, st)) != cudaSuccess) return e;
     const unsigned rgrid = (unsigned)((M + 3) / 4);
     if (KP == 16)
         tc::rerank_kernel<16><<<rgrid, 128, 0, st>>>(pd, pj, n_groups, a.x, a.y, xn, ymax, M, N, D, K,
@@ -806,7 +903,6 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
     else
         tc::rerank_kernel<32><<<rgrid, 128, 0, st>>>(pd, pj, n_groups, a.x, a.y, xn, ymax, M, N, D, K,
                                                      a.dist, a.idx, a.j_offset, fb_count, fb_rows);
-    if ((e = cudaMemsetAsync(fb_done, 0, tc::FB_CAP * 4, st)) != cudaSuccess) return e;
     tc::fallback_kernel<<<tc::FB_GRID, tc::FB_THREADS, 0, st>>>(a.x, a.y, N, D, K, fb_count, fb_rows,
                                                                 fb_pd, fb_pj, fb_done, a.dist, a.idx,
                                                                 a.j_offset);
