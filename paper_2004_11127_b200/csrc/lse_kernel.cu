@@ -117,7 +117,7 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
 }
 
 template <int D, int R>
-constexpr int lse_min_blocks() { return (D <= 3 && R % 2 == 0) ? GENRED_LSE_MINB : 2; }
+constexpr int lse_min_blocks() { return (D <= 3 && R % 2 == 0) ? (R > 4 ? 2 : GENRED_LSE_MINB) : 2; }
 
 template <int D, int R, bool HZ>
 __global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>()) lse_kernel(const LseParams p) {
@@ -542,9 +542,12 @@ template <int D>
 #ifndef GENRED_LSE_R4
 #define GENRED_LSE_R4 1
 #endif
-constexpr int lse_rmax() { return (D <= 3 && GENRED_LSE_R4) ? 4 : 2; }
+#ifndef GENRED_LSE_RBIG
+#define GENRED_LSE_RBIG 4
+#endif
+constexpr int lse_rmax() { return (D <= 3 && GENRED_LSE_R4) ? GENRED_LSE_RBIG : 2; }
 
-int lse_rows_per_thread_max(int D) { return (D <= 3 && GENRED_LSE_R4) ? 4 : 2; }
+int lse_rows_per_thread_max(int D) { return (D <= 3 && GENRED_LSE_R4) ? GENRED_LSE_RBIG : 2; }
 
 template <int D>
 static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {

@@ -12,10 +12,10 @@
 namespace genred {
 
 // Gradient modes with D + E <= 4 (fused Sum+grad, records carrying b' and b' y'), row-pair mode
-// (GENRED_GRAD_RP): 4 rows per thread and 8 record pairs per iteration at 3 CTAs/SM (80
+// (GENRED_GRAD_RP): 4 rows per thread and 16 record pairs per iteration at 3 CTAs/SM (80
 // registers; the fp64 tile sums spill to local memory once per 512 j, outside the pair loop)
-// measured 13.34 pairs/clk/SM at M = N = 1e5 and 13.91 at 4e5, against 13.03 / 13.41 at 2 CTAs/SM
-// and 12.42 / 12.94 with 4 record pairs per iteration (B200, round 2).  The j-packed loop of
+// measured 13.46 pairs/clk/SM at M = N = 1e5 and 14.07 at 4e5 (8 pairs: 13.34 / 13.91; 2 CTAs/SM:
+// 13.03 / 13.41; 4 pairs: 12.42 / 12.94; 6 or 8 rows per thread spill in the loop: 13.22 / 11.82).  The j-packed loop of
 // round 1 (4 rows, 4 pairs, 2 CTAs/SM) measured 11.45 / 11.93.  The direct form shares the
 // kernel: 8.92 -> 8.77 pairs/clk/SM at 3 CTAs/SM (4e5, sigma = 0.05).
 #ifndef GENRED_GRAD_R
@@ -43,7 +43,12 @@ namespace genred {
 #define GENRED_SUM_HH 4
 #endif
 #ifndef GENRED_GRAD_HH
-#define GENRED_GRAD_HH 8
+#define GENRED_GRAD_HH 16
+#endif
+// Row-pair gradient loop: fp32 tile sums promoted to fp64 every GENRED_GRAD_PROMO tiles of 512 j
+// (R18: every <= 1024 pairs); each promotion costs conversions on the MUFU pipe.
+#ifndef GENRED_GRAD_PROMO
+#define GENRED_GRAD_PROMO 2
 #endif
 
 template <int MODE, int D, int E>
@@ -371,6 +376,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
             }
         }
         if constexpr (RP) {
+            if (GENRED_GRAD_PROMO > 1 && (k + 1) % GENRED_GRAD_PROMO != 0 && k != nt - 1) continue;
 #pragma unroll
             for (int q = 0; q < RQ; ++q) {
                 const int r0 = 2 * q, r1 = 2 * q + 1;
