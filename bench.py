@@ -439,6 +439,8 @@ def main() -> None:
     ap.add_argument("--one-device", action="store_true", help="testing only: every rank uses cuda:0")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--edge-n", type=int, default=0, help="config 6 (Cedge): N (default 8)")
+    ap.add_argument("--shape", default="", help="testing only: M,N override of the config's sizes "
+                    "(the line's config.workload then names the override)")
     args = ap.parse_args()
     if not args.config:
         args.config = 7 if args.mode == "jshard" else 5
@@ -451,6 +453,12 @@ def main() -> None:
         synth.CONFIGS[6] = dataclasses.replace(synth.CONFIGS[6], N=args.edge_n,
                                                name=f"Cedge Gaussian Sum M=2^28 N={args.edge_n} D=3 E=1 sigma=0.5 (HBM-bound)")
 
+    if args.shape:
+        import dataclasses
+        Mo, No = (int(float(v)) for v in args.shape.split(","))
+        c0 = synth.CONFIGS[args.config]
+        synth.CONFIGS[args.config] = dataclasses.replace(c0, M=Mo, N=No,
+                                                         name=f"{c0.name} [test override M={Mo} N={No}]")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))

@@ -59,3 +59,46 @@ def test_reference_arm_under_torchrun_two_ranks():
     assert len(lines) == 1, out.stdout
     d = json.loads(lines[0])
     assert d["impl"] == "reference" and d["n_gpus"] == 2 and d["value"] > 0
+
+
+def _torchrun(args, port, timeout=900):
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py")] + args
+    out = subprocess.run(cmd, cwd=ROOT, capture_output=True, text=True, timeout=timeout)
+    assert out.returncode == 0, out.stderr[-3000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout[-3000:]
+    return json.loads(lines[0])
+
+
+@pytest.mark.gpu
+def test_device_arm_two_ranks_verifies_itself():
+    """N > 1 (2 gloo ranks sharing cuda:0, testing only): the line carries its own parity sample
+    (128 rows of each shard gathered to rank 0) and every rank's plan."""
+    d = _torchrun(["--gpus", "2", "--config", "2", "--dist-backend", "gloo", "--one-device",
+                   "--steps", "3", "--warmup", "3", "--shape", "20000,20000"], 29581)
+    assert d["n_gpus"] == 2 and d["config"]["parallelism"] == "ishard2"
+    assert len(d["per_rank"]) == 2 and [r["rank"] for r in d["per_rank"]] == [0, 1]
+    assert d["per_rank"][0]["row_lo"] == 0 and d["per_rank"][1]["row_hi"] == 20000
+    cb = d["cpu_baseline"]
+    assert "of each of the 2 shards" in cb["sample"] and cb["max_r4_err_vs_gpu"] <= 1e-5
+    assert cb["cpu_model"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("config", [7, 8])
+def test_jshard_mode_json(config):
+    """--mode jshard (1 rank here, 2 gloo ranks below): the public dist.jshard_eval path, with
+    the merged rows checked against the oracle over all of y."""
+    d = _run(["--mode", "jshard", "--config", str(config), "--steps", "3", "--warmup", "3",
+              "--shape", "3000,2000000"])
+    assert d["config"]["combine"] and d["roofline"]["bound"] == "alu" and d["value"] > 0
+    err = d["cpu_baseline"].get("max_r4_err_vs_gpu", d["cpu_baseline"].get("max_abs_err_vs_gpu"))
+    assert err is not None and err <= (1e-5 if config == 7 else 1e-6)
+    d2 = _torchrun(["--gpus", "2", "--mode", "jshard", "--config", str(config), "--dist-backend",
+                    "gloo", "--one-device", "--steps", "2", "--warmup", "2", "--shape", "3000,2000000"],
+                   29582 + config)
+    assert d2["config"]["parallelism"] == "jshard2" and len(d2["per_rank"]) == 2
+    assert d2["per_rank"][1]["j_hi"] == 2000000
+    err2 = d2["cpu_baseline"].get("max_r4_err_vs_gpu", d2["cpu_baseline"].get("max_abs_err_vs_gpu"))
+    assert err2 <= (1e-5 if config == 7 else 1e-6)

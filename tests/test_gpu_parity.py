@@ -546,7 +546,7 @@ def test_gauss_sum_tiny_n(G, N):
 @pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
 @pytest.mark.parametrize("M,N,D,split", [(1000, 1000, 3, 0), (1000, 1000, 3, 1), (300, 4096, 2, 0),
                                          (4096, 77, 1, 0), (777, 3001, 4, 5), (65, 1500, 3, 0),
-                                         (2000, 1000, 3, 32)])
+                                         (2000, 1000, 3, 32), (2048, 2000, 3, 4), (4096, 4096, 2, 8)])
 def test_small_problem_one_launch(G, monkeypatch, formula, M, N, D, split):
     """max(M, N) <= 4096 (C1-like): ONE kernel (sum_small_kernel: the CTAs build their own
     direct-form j-records, last-CTA split merge) against the oracle, against the two-launch path
