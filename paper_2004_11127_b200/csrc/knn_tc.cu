@@ -459,7 +459,25 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
     float kth = INFINITY;
 #pragma unroll
     for (int k = 0; k < KP; ++k) { bd[k] = INFINITY; bj[k] = -1; }
-    for (int g = lane; g < n_groups; g += 32) {
+    if (n_groups <= 32) {
+        // one group per lane: the main kernel leaves each group's list sorted by (d, j) (kp_insert
+        // order), so the lane takes it as is -- no insertion
+        if (lane < n_groups) {
+            const float4 *gd4 = reinterpret_cast<const float4 *>(pd + ((int64_t)lane * M + i) * KP);
+            const int4 *gj4 = reinterpret_cast<const int4 *>(pj + ((int64_t)lane * M + i) * KP);
+#pragma unroll
+            for (int q = 0; q < KP / 4; ++q) {
+                const float4 dv = gd4[q];
+                const int4 jv = gj4[q];
+                bd[4 * q] = dv.x; bd[4 * q + 1] = dv.y; bd[4 * q + 2] = dv.z; bd[4 * q + 3] = dv.w;
+                bj[4 * q] = jv.x; bj[4 * q + 1] = jv.y; bj[4 * q + 2] = jv.z; bj[4 * q + 3] = jv.w;
+            }
+#pragma unroll
+            for (int k = 0; k < KP; ++k)
+                if (bj[k] < 0) bd[k] = INFINITY;
+        }
+    }
+    for (int g = lane; n_groups > 32 && g < n_groups; g += 32) {
         const float *gd = pd + ((int64_t)g * M + i) * KP;
         const int32_t *gj = pj + ((int64_t)g * M + i) * KP;
         for (int k = 0; k < KP; ++k) {
