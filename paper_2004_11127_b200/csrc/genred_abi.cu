@@ -150,7 +150,7 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
     if (it != ctx->occ.end()) return it->second;
     int n = 1;
     if (kind == 0) n = sum_occupancy(a, b, c, R);
-    else if (kind == 1) n = lse_occupancy(a, R);
+    else if (kind == 1) n = lse_occupancy(a, R, b != 0);
     else if (kind == 3) n = softmax_grad_occupancy(a, R);
     else n = argk_occupancy(a, b, R);
     ctx->occ[key] = n;
@@ -660,7 +660,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
 
     if (red == GENRED_LSE) {
         if (a->n_ranges > 0) return eval_ranges(ctx, a, st, 4, lse_rows_per_thread_max(D));
-        Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, 0, 0, true);
+        Plan pl = make_plan(ctx, a, 1, lse_rows_per_thread_max(D), D, a->b == nullptr ? 1 : 0, 0, true);
         // small M: CTAs of a few rows whose threads split j (see the Sum path)
         const bool smm = a->split_j <= 0 && M <= kSmmMaxM && N > kDirectMaxN;
         if (smm) {

@@ -151,7 +151,7 @@ cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
 // ceil(M / R) * split, split-major, 2 CTAs per SM.
 int lse_smm_rows(int D);
 cudaError_t launch_lse_smm(const LseLaunch &a, cudaStream_t st, int *ctas);
-int lse_occupancy(int D, int R);
+int lse_occupancy(int D, int R, bool hz);
 int lse_rows_per_thread_max(int D);
 
 struct ArgkLaunch {

@@ -36,12 +36,15 @@ constexpr float kSumMax = 65536.0f;
 // C3-like LSE (1e6 x 1e6, eps = 0.05) 13.42 -> 13.60 pairs/clk/SM; the j-packed loop of round 1
 // at 2 CTAs/SM measured 12.98 (B200, round 2).
 #ifndef GENRED_LSE_MINB
-#define GENRED_LSE_MINB 3
+#define GENRED_LSE_MINB 4
 #endif
 // Row-pair packing (as the gradient modes, sum_body.cuh GENRED_GRAD_RP): the packed lanes hold
 // two ROWS, the record's -y_d is a broadcast scalar operand, one j at a time.
 #ifndef GENRED_LSE_RP
 #define GENRED_LSE_RP 1
+#endif
+#ifndef GENRED_LSE_SCALAR_ACC
+#define GENRED_LSE_SCALAR_ACC 0
 #endif
 constexpr int kSub = GENRED_LSE_SUB;  // record pairs per sub-chunk (2 kSub j)
 constexpr int kPromote = 64 / kSub;   // sub-chunks per fp64 promotion (128 j)
@@ -117,10 +120,14 @@ __device__ __noinline__ LseRescale lse_rescale(const float *base, const float (&
 }
 
 template <int D, int R>
-constexpr int lse_min_blocks() { return (D <= 3 && R % 2 == 0) ? (R > 4 ? 2 : GENRED_LSE_MINB) : 2; }
+constexpr int lse_min_blocks(bool hz) {
+    // h = 0: 4 CTAs/SM (64 registers, spills outside the pair loop) measured 13.81 pairs/clk/SM
+    // against 13.61 at 3; with h the 3-CTA build is faster (12.03 against 11.78)
+    return (D <= 3 && R % 2 == 0) ? (R > 4 ? 2 : (hz ? GENRED_LSE_MINB : 3)) : 2;
+}
 
 template <int D, int R, bool HZ>
-__global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>()) lse_kernel(const LseParams p) {
+__global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>(HZ)) lse_kernel(const LseParams p) {
     using Cfg = LseCfg<D, HZ>;
     constexpr int RS = Cfg::RS;
     extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -206,7 +213,12 @@ __global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>()) lse_kernel(c
                         const float2 hm = HZ ? NM2[q] : add2(NM2[q], dup2(f[2 * D + h]));   // h'_hi - m
                         const float2 t = fma2(q2, negc2, hm);
                         const float2 e = make_float2(ex2(t.x), ex2(t.y));
-                        cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
+                        if (GENRED_LSE_SCALAR_ACC && HZ) {
+                            cs[q].x += e.x;
+                            cs[q].y += e.y;
+                        } else {
+                            cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
+                        }
                     }
                 }
             }
@@ -527,12 +539,12 @@ static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
 }
 
 template <int D, int R>
-static int occ_lse() {
+static int occ_lse(bool hz) {
     using Cfg = LseCfg<D, false>;
-    auto kern = lse_kernel<D, R, false>;
+    auto kern = hz ? lse_kernel<D, R, true> : lse_kernel<D, R, false>;
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::SMEM);
     int n = 0;
-    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, Cfg::SMEM) != cudaSuccess)
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, kern, kThreads, hz ? LseCfg<D, true>::SMEM : Cfg::SMEM) != cudaSuccess)
         return 1;
     return n > 0 ? n : 1;
 }
@@ -570,8 +582,8 @@ cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
     return cudaErrorInvalidValue;
 }
 
-int lse_occupancy(int D, int R) {
-#define GENRED_OCC(DD) if (D == DD) return R == 1 ? occ_lse<DD, 1>() : occ_lse<DD, lse_rmax<DD>()>();
+int lse_occupancy(int D, int R, bool hz) {
+#define GENRED_OCC(DD) if (D == DD) return R == 1 ? occ_lse<DD, 1>(hz) : occ_lse<DD, lse_rmax<DD>()>(hz);
     GENRED_OCC(1) GENRED_OCC(2) GENRED_OCC(3) GENRED_OCC(4)
     GENRED_OCC(5) GENRED_OCC(6) GENRED_OCC(7) GENRED_OCC(8)
 #undef GENRED_OCC

@@ -47,6 +47,9 @@ namespace genred {
 #endif
 // Row-pair gradient loop: fp32 tile sums promoted to fp64 every GENRED_GRAD_PROMO tiles of 512 j
 // (R18: every <= 1024 pairs); each promotion costs conversions on the MUFU pipe.
+#ifndef GENRED_GRAD_STAGES
+#define GENRED_GRAD_STAGES 4
+#endif
 #ifndef GENRED_GRAD_PROMO
 #define GENRED_GRAD_PROMO 2
 #endif
@@ -67,7 +70,10 @@ struct SumCfg {
     static constexpr int C = NS + NG;
     static constexpr bool GRAD = NG > 0;
     static constexpr bool EXP = MODE != 3;
-    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
+    // ring depth: the row-pair gradient kernels (GENRED_GRAD_STAGES) may run 4 CTAs/SM, whose
+    // smem budget holds 3 stages of their 16 KB tiles
+    static constexpr int STAGES = ((MODE == 1 || MODE == 2) && E == 1 && D <= 3) ? GENRED_GRAD_STAGES : kStages;
+    static constexpr int SMEM = JRing<STAGES>::smem_bytes(TILE_FLOATS);
 };
 
 struct SumParams {
@@ -593,7 +599,7 @@ sum_kernel(const SumParams p) {
     const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
     const uint32_t last_bytes = (uint32_t)last_np * Cfg::RS * 4u;   // a partial last tile is copied partially
 
-    JRing<kStages> ring;
+    JRing<Cfg::STAGES> ring;
     if constexpr (MODE != 3) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
         ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);

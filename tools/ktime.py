@@ -24,8 +24,11 @@ def run(case: str) -> None:
     dist = parts[6] if len(parts) > 6 else "u"
     M, N, scale = int(float(M)), int(float(N)), float(scale)
     x = torch.from_numpy(synth.uniform3(M, 1)).cuda()
-    y = torch.from_numpy(synth.gmm3(N, 2) if dist == "gmm" else synth.uniform3(N, 2)).cuda()
+    y = torch.from_numpy(synth.gmm3(N, 2) if dist.startswith("gmm") else synth.uniform3(N, 2)).cuda()
     b = torch.from_numpy(synth.signal(N, 3)).cuda() if red == "sum" else None
+    if red == "lse" and "h" in dist:                      # LSE with a bias h ~ N(0, 1)
+        import numpy as np
+        b = torch.from_numpy(np.random.default_rng(4).standard_normal(N).astype(np.float32)).cuda()
     kw = dict(scale=scale)
     if red == "lse":
         kw["out_dtype"] = "float64"
