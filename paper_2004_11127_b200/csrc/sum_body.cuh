@@ -42,6 +42,12 @@ namespace genred {
 #ifndef GENRED_SUM_HH
 #define GENRED_SUM_HH 4
 #endif
+// Gaussian Sum / SqDist Sum, D <= 3, 4 rows per thread: 4 CTAs/SM (64 registers) measured 15.42
+// pairs/clk/SM (expanded form, 2e6^2) and 13.40 (direct form, sigma = 0.05) against 15.34 / 13.21
+// at 3 CTAs/SM (round 2).
+#ifndef GENRED_SUM_MINB
+#define GENRED_SUM_MINB 4
+#endif
 #ifndef GENRED_GRAD_HH
 #define GENRED_GRAD_HH 16
 #endif
@@ -516,7 +522,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
 template <int MODE, int D, int E, int R, bool SMM>
 constexpr int sum_min_blocks() {
     if (SMM) return 2;
-    if ((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) return 3;
+    if ((MODE == 0 || MODE == 3) && E == 1 && D <= 3 && R == 4) return GENRED_SUM_MINB;
     if ((MODE == 1 || MODE == 2) && D + E <= 4 && E == 1 && R == GENRED_GRAD_R) return GENRED_GRAD_MINB;
     return 2;
 }

@@ -159,8 +159,11 @@ static cudaError_t run_sum_small(const SumLaunch &a, const float *y, const float
     const int cl = (a.split > 1 && a.split <= 8 && kSmallCluster) ? 1 : 0;
     const int smem = (int)(a.pairs_per_split * Cfg::RS * 4) + (cl ? kThreads * R * Cfg::C * 8 : 0);
     auto kern = sum_small_kernel<MODE, D, 1, R>;
-    if (smem > 48 * 1024) {
-        const cudaError_t e = smem_opt_in((const void *)kern, smem);
+    // the size varies per call: opt in once to the largest this instance can ask for
+    // (smem_opt_in caches per kernel, so a smaller first request would stick)
+    constexpr int kSmemMax = (int)(kSmallMaxPairs * Cfg::RS * 4) + kThreads * R * Cfg::C * 8;
+    if (kSmemMax > 48 * 1024) {
+        const cudaError_t e = smem_opt_in((const void *)kern, kSmemMax);
         if (e != cudaSuccess) return e;
     }
     if (!cl) {
