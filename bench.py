@@ -12,10 +12,17 @@ broadcasts y and b from rank 0 and every rank reduces its M/N rows (strong scali
 
 Timing: W warm-up steps; then K steps bracketed by barrier + cuda synchronize, CUDA events on
 the launching stream, max over ranks.  Inputs (280 MB) exceed the 126 MB L2, so no flush.
-Extra keys: roofline (dominant kernel, live CUDA-event timing through genred_profile),
-cpu_baseline (the fp64 oracle on a bounded row sample, rank 0 at N=1), e2e (host buffers through
-the C ABI's host mode, H2D + D2H inside the timed region), clocks (NVML sampled during the timed
-region), gpu_launches (libgenred kernels launched in the timed region, all ranks).
+Extra keys: roofline (dominant kernel, live CUDA-event timing through genred_profile: inside the
+timed region for steps >= 5 ms, else over a second pass of the same K steps -- kernel_timing),
+cpu_baseline (the fp64 oracle on a bounded row sample; at N > 1 on 128 seeded rows of EACH shard
+gathered to rank 0, with max_r4_err_vs_gpu), per_rank (N > 1: every rank's plan and kernel time),
+e2e (host buffers through the C ABI's host mode, H2D + D2H inside the timed region), clocks (NVML
+sampled during the timed region), gpu_launches (libgenred kernels launched in the timed region,
+all ranks).  NCCL runs with NCCL_DEBUG=INFO, NCCL_DEBUG_SUBSYS=INIT (communicator rank counts).
+
+``--mode jshard`` (configs 7, 8: M = 1e4 against N = 1e8, Gaussian Sum / LSE): the j-shard path of
+SURVEY.md 8(e) -- each rank draws its slice of y, a step is the public dist.jshard_eval (local
+reduction + fp64 all-reduce, or (m, s) all-gather + genred_combine_lse).
 
 ``--impl reference``: there is no reference implementation (PAPER.md only); the reference arm
 is the fp64 oracle (oracle/) timed on this host's cores on a bounded row sample of the same

@@ -34,6 +34,19 @@ __global__ void __launch_bounds__(256,3) k_ffma2_3reg(float* out, float s){
   }
   float t=0; for(int k=0;k<6;k++) t+=a[k].x+a[k].y+c[k].x; if(t==1.2345f) out[0]=t;
 }
+// FFMA2 with a broadcast SCALAR first operand and two register pairs (the row-pair loops'
+// accumulation pattern: acc_k = fma2(e_k pair, scalar, acc_k))
+__global__ void __launch_bounds__(256,3) k_ffma2_scalar(float* out, float s){
+  float2 a[6], c[6]; float b[6];
+  for(int k=0;k<6;k++){ a[k]=make_float2(threadIdx.x*1e-4f+k, k*0.5f); b[k]=s*k; c[k]=make_float2(s, s*0.5f*k);}
+  for(int i=0;i<IT;i++){
+    #pragma unroll
+    for(int k=0;k<6;k++) a[k]=__ffma2_rn(c[k], make_float2(b[k],b[k]), a[k]);
+    #pragma unroll
+    for(int k=0;k<6;k++) c[k]=__ffma2_rn(a[k], make_float2(b[(k+1)%6],b[(k+1)%6]), c[k]);
+  }
+  float t=0; for(int k=0;k<6;k++) t+=a[k].x+a[k].y+c[k].x; if(t==1.2345f) out[0]=t;
+}
 // FFMA2 with an immediate third operand: a_k = fma(a_k, b_k, imm)
 __global__ void __launch_bounds__(256,3) k_ffma2_imm(float* out, float s){
   float2 a[8], b[8];
@@ -92,6 +105,7 @@ int main(){
   run("mufu",k_mufu2,8,n,"ex2");
   run("ffma2_3reg",k_ffma2_3reg,24,n,"lane-fma");
   run("ffma2_imm",k_ffma2_imm,16,n,"lane-fma");
+  run("ffma2_scalar+2pairs",k_ffma2_scalar,24,n,"lane-fma");
   run("ffma_3reg",k_ffma_3reg,16,n,"lane-fma");
   run("mix 4ffma2:2mufu",k_mix,8,n,"ex2");
   return 0;
