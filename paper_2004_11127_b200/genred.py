@@ -109,8 +109,9 @@ def load():
         lib.genred_profile.restype = I32
         lib.genred_profile_read.argtypes = [P, P, I32]
         lib.genred_profile_read.restype = I32
-        lib.genred_set_option.argtypes = [P, ctypes.c_char_p, I64]
-        lib.genred_set_option.restype = I32
+        if hasattr(lib, "genred_set_option"):          # (older builds of the library lack it)
+            lib.genred_set_option.argtypes = [P, ctypes.c_char_p, I64]
+            lib.genred_set_option.restype = I32
         if lib.genred_abi_version() != ABI_VERSION:
             raise RuntimeError("libgenred ABI version mismatch")
         _lib = lib
