@@ -160,6 +160,10 @@ int occupancy(genred_ctx *ctx, int kind, int a, int b, int c, int R) {
 constexpr int64_t kDirectMaxN = 64;          // Gaussian Sum: N at or below -> direct form, no bbox
 constexpr int64_t kDirectMaxM = 16;          // Gaussian Sum: M at or below -> direct form, no bbox
 constexpr int64_t kMinSplitPairs = 64;       // shortest record-pair j-split (128 j)
+#ifndef GENRED_MIN_WAVES
+#define GENRED_MIN_WAVES 4
+#endif
+constexpr int64_t kMinWaves = GENRED_MIN_WAVES;  // Sum / LSE row-tile kernels: waves of CTAs to aim for
 constexpr int64_t kMaxSplitSmm = 2048;       // small-M mode: j-splits (CTAs of a few rows each)
 constexpr int64_t kSmmMaxM = 64;             // small-M mode for M at or below
 constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
@@ -222,6 +226,28 @@ Plan make_plan(genred_ctx *ctx, const genred_args *a, int kind, int rmax, int oc
         } else {
             // (pair splits: a smaller per-split penalty lets small M spread over many splits)
             S = choose_split(itiles, total, grain, min_units, slots, &eff, cap, pair_splits ? 2e-4 : 0.002);
+            if (pair_splits && kind == 0 && kMinWaves > 0 && itiles * S < kMinWaves * slots) {
+                // At least kMinWaves waves of CTAs: with one (or two) waves the kernel ends with the
+                // slowest SM, while later waves let faster SMs take more CTAs.  Measured at 1e5^2
+                // (`profiles/r02_split_sweep.txt`): the Gaussian Sum goes 14.28 (6 splits, 1 wave)
+                // -> 14.96 (27) pairs/clk/SM, the fused Sum + grad 13.30 (6) -> 13.79 (27), and
+                // 3e5^2 14.99 -> 15.24.  Take the best wave efficiency over [S_min, 2 S_min]
+                // (ties: fewer splits), if the j-axis allows it.  Sum family only: an LSE CTA
+                // restarts its running max per split (more lazy rescales) and measured slower
+                // with more splits (1e5^2: 12.94 -> 12.74).
+                const int64_t smax = std::min<int64_t>(cap, std::max<int64_t>(1, total / min_units));
+                const int64_t s_lo = (kMinWaves * slots + itiles - 1) / itiles;
+                double e_best = 0.0;
+                int S_best = S;
+                for (int64_t S2 = s_lo; S2 <= std::min<int64_t>(smax, 2 * s_lo); ++S2) {
+                    const int64_t per = ((total + S2 - 1) / S2 + grain - 1) / grain * grain;
+                    if ((total + per - 1) / per != S2) continue;
+                    const int64_t U = itiles * S2, waves = (U + slots - 1) / slots;
+                    const double e2 = (double)U / (double)(waves * slots);
+                    if (e2 > e_best + 1e-9) { e_best = e2; S_best = (int)S2; }
+                }
+                if (e_best >= 0.9) { S = S_best; eff = e_best; }
+            }
         }
         // fewer rows/thread costs issue slots; rows past M in the last row tile are wasted work
         const double util = (double)a->M / (double)(itiles * rows);
