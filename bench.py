@@ -448,6 +448,8 @@ def main() -> None:
     ap.add_argument("--edge-n", type=int, default=0, help="config 6 (Cedge): N (default 8)")
     ap.add_argument("--shape", default="", help="testing only: M,N override of the config's sizes "
                     "(the line's config.workload then names the override)")
+    ap.add_argument("--scale", type=float, default=0.0, help="override sigma / eps (e.g. 0.05: the "
+                    "Gaussian Sum's direct form, reading R18e); config.workload names the override")
     args = ap.parse_args()
     if not args.config:
         args.config = 7 if args.mode == "jshard" else 5
@@ -466,6 +468,11 @@ def main() -> None:
         c0 = synth.CONFIGS[args.config]
         synth.CONFIGS[args.config] = dataclasses.replace(c0, M=Mo, N=No,
                                                          name=f"{c0.name} [test override M={Mo} N={No}]")
+    if args.scale:
+        import dataclasses
+        c0 = synth.CONFIGS[args.config]
+        synth.CONFIGS[args.config] = dataclasses.replace(c0, scale=args.scale,
+                                                         name=f"{c0.name} [scale override {args.scale}]")
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
@@ -631,6 +638,10 @@ def main() -> None:
                     "peak_basis": "HBM copy bandwidth (MEASURED_PEAKS.json)",
                     "bytes_per_launch": nbytes}
     else:
+        # the Gaussian Sum's form is decided on the device (bounding box, reading R18b): the
+        # direct form on raw differences runs 8 FP32 lane-ops per pair instead of 4 (same peak)
+        if w["formula"] == "gauss" and plan.get("path") == 0 and not w.get("hbm"):
+            w = dict(w, fp32=8)
         peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
         achieved = Ml * N / (kmean * 1e-3)
         roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
@@ -728,6 +739,7 @@ def main() -> None:
                              "inputs re-read from HBM/L2 each step; no flush",
                        "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"],
                        "ctas": plan["ctas"], "K": c.K if argk else None,
+                       "form": {0: "direct", 1: "tensor", 2: "expanded"}.get(plan.get("path")),
                        "fallback_rows": plan.get("fallback_rows")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,
