@@ -38,6 +38,9 @@ constexpr float kSumMax = 65536.0f;
 #ifndef GENRED_LSE_MINB
 #define GENRED_LSE_MINB 4
 #endif
+#ifndef GENRED_LSE_MINB_BIG
+#define GENRED_LSE_MINB_BIG 2
+#endif
 // Row-pair packing (as the gradient modes, sum_body.cuh GENRED_GRAD_RP): the packed lanes hold
 // two ROWS, the record's -y_d is a broadcast scalar operand, one j at a time.
 #ifndef GENRED_LSE_RP
@@ -123,7 +126,7 @@ template <int D, int R>
 constexpr int lse_min_blocks(bool hz) {
     // h = 0: 4 CTAs/SM (64 registers, spills outside the pair loop) measured 13.81 pairs/clk/SM
     // against 13.61 at 3; with h the 3-CTA build is faster (12.03 against 11.78)
-    return (D <= 3 && R % 2 == 0) ? (R > 4 ? 2 : (hz ? GENRED_LSE_MINB : 3)) : 2;
+    return (D <= 3 && R % 2 == 0) ? (R > 4 ? GENRED_LSE_MINB_BIG : (hz ? GENRED_LSE_MINB : 3)) : 2;
 }
 
 template <int D, int R, bool HZ>
