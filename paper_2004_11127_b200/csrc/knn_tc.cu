@@ -391,6 +391,7 @@ __global__ void split_kernel(const float *__restrict__ src, int64_t rows, int D,
     const int lane = threadIdx.x & 31;
     const int64_t nw = gs >> 5;
     const bool vec = (D & 3) == 0 && (((uintptr_t)src) & 15) == 0;
+    float wmax = 0.0f;                                  // this warp's largest |row| (lane 0)
     for (int64_t i = w; i < rows; i += nw) {
         double s = 0.0;
         if (vec) {
@@ -435,7 +436,18 @@ __global__ void split_kernel(const float *__restrict__ src, int64_t rows, int D,
         for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
         if (lane == 0) {
             nrm[i] = (float)s;
-            if (maxnorm_bits) atomicMax(maxnorm_bits, __float_as_uint((float)sqrt(s) * 1.0000002f));
+            wmax = fmaxf(wmax, (float)sqrt(s) * 1.0000002f);
+        }
+    }
+    // one atomicMax per CTA (not per row: same-address atomics serialise in L2)
+    if (maxnorm_bits) {
+        __shared__ float smax[32];
+        if (lane == 0) smax[threadIdx.x >> 5] = wmax;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            float m = 0.0f;
+            for (int k = 0; k < (int)(blockDim.x >> 5); ++k) m = fmaxf(m, smax[k]);
+            atomicMax(maxnorm_bits, __float_as_uint(m));
         }
     }
 }
@@ -552,39 +564,61 @@ __global__ void rerank_kernel(const float *__restrict__ pd, const int32_t *__res
             jj[k] = s_j[wl][k];
             use[k] = jj[k] >= 0 && (k < K || (double)s_d[wl][k] <= dK + 2.0 * delta);
         }
-        double acc[KP];
-#pragma unroll
-        for (int k = 0; k < KP; ++k) acc[k] = 0.0;
-        if ((D & 3) == 0 && ((((uintptr_t)x) | ((uintptr_t)y)) & 15) == 0) {
+        constexpr int CV = 7;                          // float4 per lane per row: D <= 896 in one pass
+        if ((D & 3) == 0 && D / 4 <= 32 * CV && ((((uintptr_t)x) | ((uintptr_t)y)) & 15) == 0) {
+            // candidate-major: a lane's CV float4 of one candidate row are requested together (one
+            // memory latency per candidate instead of one per float4: the scattered y rows made
+            // this kernel latency-bound)
             const float4 *x4 = reinterpret_cast<const float4 *>(x + i * D);
-            for (int c = lane; c < D / 4; c += 32) {
-                const float4 xv = __ldg(x4 + c);
+            float4 xv[CV];
 #pragma unroll
-                for (int k = 0; k < KP; ++k) {
-                    if (!use[k]) continue;
-                    const float4 yv = __ldg(reinterpret_cast<const float4 *>(y + (int64_t)jj[k] * D) + c);
-                    const double d0 = (double)xv.x - (double)yv.x, d1 = (double)xv.y - (double)yv.y;
-                    const double d2 = (double)xv.z - (double)yv.z, d3 = (double)xv.w - (double)yv.w;
-                    acc[k] = fma(d3, d3, fma(d2, d2, fma(d1, d1, fma(d0, d0, acc[k]))));
+            for (int u = 0; u < CV; ++u) {
+                const int c = lane + 32 * u;
+                xv[u] = c < D / 4 ? __ldg(x4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+            }
+            for (int k = 0; k < KP; ++k) {
+                if (!use[k]) {                             // warp-uniform
+                    if (lane == 0) s_e[wl][k] = INFINITY;
+                    continue;
                 }
+                const float4 *y4 = reinterpret_cast<const float4 *>(y + (int64_t)jj[k] * D);
+                float4 yv[CV];
+#pragma unroll
+                for (int u = 0; u < CV; ++u) {
+                    const int c = lane + 32 * u;
+                    yv[u] = c < D / 4 ? __ldg(y4 + c) : make_float4(0.f, 0.f, 0.f, 0.f);
+                }
+                double v = 0.0;
+#pragma unroll
+                for (int u = 0; u < CV; ++u) {
+                    const double d0 = (double)xv[u].x - (double)yv[u].x, d1 = (double)xv[u].y - (double)yv[u].y;
+                    const double d2 = (double)xv[u].z - (double)yv[u].z, d3 = (double)xv[u].w - (double)yv[u].w;
+                    v = fma(d3, d3, fma(d2, d2, fma(d1, d1, fma(d0, d0, v))));
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) s_e[wl][k] = v;
             }
         } else {
+            double acc[KP];
+#pragma unroll
+            for (int k = 0; k < KP; ++k) acc[k] = 0.0;
             for (int c = lane; c < D; c += 32) {
-                const double xv = (double)x[i * D + c];
+                const double xs = (double)x[i * D + c];
 #pragma unroll
                 for (int k = 0; k < KP; ++k) {
                     if (!use[k]) continue;
-                    const double dv = xv - (double)y[(int64_t)jj[k] * D + c];
+                    const double dv = xs - (double)y[(int64_t)jj[k] * D + c];
                     acc[k] = fma(dv, dv, acc[k]);
                 }
             }
-        }
 #pragma unroll
-        for (int k = 0; k < KP; ++k) {
-            double v = acc[k];
+            for (int k = 0; k < KP; ++k) {
+                double v = acc[k];
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-            if (lane == 0) s_e[wl][k] = use[k] ? v : INFINITY;
+                for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+                if (lane == 0) s_e[wl][k] = use[k] ? v : INFINITY;
+            }
         }
     }
     __syncwarp();
