@@ -46,9 +46,6 @@ constexpr float kSumMax = 65536.0f;
 #ifndef GENRED_LSE_RP
 #define GENRED_LSE_RP 1
 #endif
-#ifndef GENRED_LSE_SCALAR_ACC
-#define GENRED_LSE_SCALAR_ACC 0
-#endif
 constexpr int kSub = GENRED_LSE_SUB;  // record pairs per sub-chunk (2 kSub j)
 constexpr int kPromote = 64 / kSub;   // sub-chunks per fp64 promotion (128 j)
 static_assert(kSplitGrain % kSub == 0, "j-splits must hold whole sub-chunks");
@@ -216,12 +213,7 @@ __global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>(HZ)) lse_kernel
                         const float2 hm = HZ ? NM2[q] : add2(NM2[q], dup2(f[2 * D + h]));   // h'_hi - m
                         const float2 t = fma2(q2, negc2, hm);
                         const float2 e = make_float2(ex2(t.x), ex2(t.y));
-                        if (GENRED_LSE_SCALAR_ACC && HZ) {
-                            cs[q].x += e.x;
-                            cs[q].y += e.y;
-                        } else {
-                            cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
-                        }
+                        cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
                     }
                 }
             }

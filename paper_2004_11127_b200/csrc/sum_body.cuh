@@ -31,12 +31,6 @@ namespace genred {
 #ifndef GENRED_GRAD_RP
 #define GENRED_GRAD_RP 1
 #endif
-#ifndef GENRED_SUM_RPD
-#define GENRED_SUM_RPD 0
-#endif
-#ifndef GENRED_GRAD_RP_QOUT
-#define GENRED_GRAD_RP_QOUT 0
-#endif
 // Record pairs per pair-loop iteration of the Sum modes: 4 measured 15.16 pairs/clk/SM against
 // 14.98 for 2 and 15.01 for 8 (Gaussian Sum, M = N = 1e6).
 #ifndef GENRED_SUM_HH
@@ -181,16 +175,16 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
     // row-pair mode (GENRED_GRAD_RP): X2[q][d] = (2x'_{2q,d}, 2x'_{2q+1,d}); S0p / Sp the fp32
     // tile sums of e b' and e b' y'_d for the two rows of pair q (lanes x, y)
     constexpr bool RP = GENRED_GRAD_RP && XP && Cfg::BY && !SMM && (R % 2 == 0);
-    // the same row-pair packing for the direct form of the Gaussian Sum (raw x - y, R18e)
-    constexpr bool RPD = GENRED_SUM_RPD && RAWD && MODE == 0 && E == 1 && !SMM && (R % 2 == 0);
-    constexpr int RQ = (RP || RPD) ? R / 2 : 1;
+    // (the same packing for the direct-form Gaussian Sum measured 1.7% slower at 3 CTAs/SM and
+    // +0.4% at 4: not used)
+    constexpr int RQ = RP ? R / 2 : 1;
     float2 X2[RQ][D], S0p[RQ], Sp[RQ][D];
 #pragma unroll
     for (int q = 0; q < RQ; ++q) {
         S0p[q] = make_float2(0.f, 0.f);
 #pragma unroll
         for (int d = 0; d < D; ++d) {
-            X2[q][d] = (RP || RPD) ? make_float2(xr[2 * q][d], xr[(2 * q + 1) % R][d]) : make_float2(0.f, 0.f);
+            X2[q][d] = RP ? make_float2(xr[2 * q][d], xr[(2 * q + 1) % R][d]) : make_float2(0.f, 0.f);
             Sp[q][d] = make_float2(0.f, 0.f);
         }
     }
@@ -221,8 +215,7 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
             }
 #pragma unroll
             for (int hq = 0; hq < 2 * RQ; ++hq) {     // the record pair's two j's x the row pairs
-                const int h = GENRED_GRAD_RP_QOUT ? hq % 2 : hq / RQ;
-                const int q = GENRED_GRAD_RP_QOUT ? hq / 2 : hq % RQ;
+                const int h = hq / RQ, q = hq % RQ;
                 {
                     float2 u = mul2(X2[q][0], dup2(f[h]));                          // 2 x'.y'
 #pragma unroll
@@ -232,34 +225,6 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
 #pragma unroll
                     for (int d = 0; d < D; ++d)
                         Sp[q][d] = fma2(ex, dup2(f[Cfg::BYOFF + 2 * d + h]), Sp[q][d]);   // e b' y'_d
-                }
-            }
-        }
-        }
-        } else if constexpr (RPD) {
-        for (int pp2 = 0; pp2 < np; pp2 += HH) {
-#pragma unroll
-        for (int hh = 0; hh < HH; ++hh) {
-            float f[RS];
-#pragma unroll
-            for (int q = 0; q < RS / 4; ++q) {
-                const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
-                f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
-            }
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-#pragma unroll
-                for (int q = 0; q < RQ; ++q) {
-                    float2 dd = add2(X2[q][0], dup2(f[h]));                       // x - y, raw
-                    float2 qq = mul2(dd, dd);
-#pragma unroll
-                    for (int d = 1; d < D; ++d) {
-                        dd = add2(X2[q][d], dup2(f[2 * d + h]));
-                        qq = fma2(dd, dd, qq);
-                    }
-                    const float2 t = mul2(qq, negs2);                               // -s^2 |x - y|^2
-                    const float2 ex = make_float2(ex2(t.x), ex2(t.y));
-                    S0p[q] = fma2(ex, dup2(f[BOFF + h]), S0p[q]);                   // e b
                 }
             }
         }
@@ -379,14 +344,6 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
         }   // RP
         ring.release(k);
         // promote the tile's fp32 partials to fp64 (every 512 j)
-        if constexpr (RPD) {
-#pragma unroll
-            for (int q = 0; q < RQ; ++q) {
-                acc64[2 * q][0] += (double)S0p[q].x;
-                acc64[2 * q + 1][0] += (double)S0p[q].y;
-                S0p[q] = make_float2(0.f, 0.f);
-            }
-        }
         if constexpr (RP) {
             if (GENRED_GRAD_PROMO > 1 && (k + 1) % GENRED_GRAD_PROMO != 0 && k != nt - 1) continue;
 #pragma unroll
