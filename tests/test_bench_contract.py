@@ -102,3 +102,16 @@ def test_jshard_mode_json(config):
     assert d2["per_rank"][1]["j_hi"] == 2000000
     err2 = d2["cpu_baseline"].get("max_r4_err_vs_gpu", d2["cpu_baseline"].get("max_abs_err_vs_gpu"))
     assert err2 <= (1e-5 if config == 7 else 1e-6)
+
+
+@pytest.mark.gpu
+def test_bench_reports_the_form_the_device_chose():
+    """config.form follows the device's bounding-box decision (reading R18b): sigma = 0.5 on the
+    unit cube takes the expanded form, sigma = 0.05 the direct one (8 FP32 lane-ops per pair in
+    the roofline's basis)."""
+    d = _run(["--config", "5", "--shape", "200000,200000", "--steps", "3", "--warmup", "3", "--no-e2e"])
+    assert d["config"]["form"] == "expanded" and "128/4 FP32" in d["roofline"]["peak_basis"]
+    d = _run(["--config", "5", "--shape", "200000,200000", "--scale", "0.05", "--steps", "3", "--warmup", "3",
+              "--no-e2e"])
+    assert d["config"]["form"] == "direct" and "128/8 FP32" in d["roofline"]["peak_basis"]
+    assert d["cpu_baseline"]["max_r4_err_vs_gpu"] <= 1e-5
