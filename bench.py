@@ -65,15 +65,17 @@ def measured_peaks() -> dict:
 def workload(cid: int) -> dict:
     """Per-config step definition: formula, algorithmic FP32 lane-ops and exps per pair (D=3)."""
     c = synth.config(cid)
-    if cid in (1, 5):  # expanded form: u = 2x'.y' - |y'|^2 (3 FFMA) + acc (1 FFMA) = 4 lane-ops
-        return dict(cfg=c, formula="gauss", reduction="sum", fp32=4, mufu=1, out_dtype="float32")
+    if cid in (1, 5):  # expanded form: u = 2x'.y' - |y'|^2 (3 FFMA) + acc (1 FFMA) = 4 lane-ops;
+        #                and 1/8 of the exponentials on the FP32 pipe (degree-5 polynomial: 8 lane-ops
+        #                each): MUFU 7/8 and FP32 4 + 8/8 = 5 per pair
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=5, mufu=7 / 8, out_dtype="float32")
     if cid == 2:   # Sum + gradient, one fused pass, expanded form: u (3 FFMA) + S0 += e b (1 FFMA)
         #            + S += e (b y') (3 FFMA, b y' packed with the j-records) = 7 lane-ops; the peak
         #            is the MUFU's either way (min(16/1, 128/7) = 16 pairs/clk/SM)
         return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=7, mufu=1,
                     out_dtype="float32")
     if cid == 7:   # j-sharded Gaussian Sum (M << N): as C5 per rank, fp64 partials all-reduced
-        return dict(cfg=c, formula="gauss", reduction="sum", fp32=4, mufu=1, out_dtype="float64")
+        return dict(cfg=c, formula="gauss", reduction="sum", fp32=5, mufu=7 / 8, out_dtype="float64")
     if cid == 8:   # j-sharded LSE: as C3 per rank, (m, s) states all-gathered and combined
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
     if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
@@ -359,7 +361,7 @@ def run_jshard(args, rank: int, world: int, local: int, w: dict) -> None:
                 "frac": achieved / peak, "traffic": None,
                 "kernel": f"{w['formula']}/{w['reduction']} pair loop (one rank's j-slice)",
                 "kernel_ms": kmean, "share_of_step": kmean / ms_step if world == 1 else None,
-                "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
+                "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']:g} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
                               f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
                 "pairs_per_launch": M * (hi - lo)}
     mine = [float(rank), float(lo), float(hi), float(plan["split_j"]), float(plan["rows_per_cta"]),
@@ -503,7 +505,10 @@ def main() -> None:
             dist.destroy_process_group()
         return
     M, N = c.M, c.N
-    lo, hi = M * rank // world, M * (rank + 1) // world
+    # i-shard rows: boundaries on the 1024-row tile (dist.ISHARD_ALIGN), so the shards' rows are
+    # bitwise the unsharded ones for the same j-split
+    from paper_2004_11127_b200.dist import ISHARD_ALIGN, shard_range
+    lo, hi = shard_range(M, world, rank, align=ISHARD_ALIGN)
     x, y, b = make_inputs(w, args.dist)
     xl = np.ascontiguousarray(x[lo:hi])
     dev = torch.device("cuda", local)
@@ -641,14 +646,14 @@ def main() -> None:
         # the Gaussian Sum's form is decided on the device (bounding box, reading R18b): the
         # direct form on raw differences runs 8 FP32 lane-ops per pair instead of 4 (same peak)
         if w["formula"] == "gauss" and plan.get("path") == 0 and not w.get("hbm"):
-            w = dict(w, fp32=8)
+            w = dict(w, fp32=8, mufu=1)                      # (no polynomial share in the direct form)
         peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
         achieved = Ml * N / (kmean * 1e-3)
         roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
                     "frac": achieved / peak, "traffic": traffic,
                     "kernel": f"{w['formula']}/{w['reduction']} pair loop", "kernel_ms": kmean,
                     "share_of_step": kmean / ms_step if world == 1 else None,
-                    "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
+                    "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']:g} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
                                   f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
                     "pairs_per_launch": Ml * N}
 

@@ -97,10 +97,17 @@ struct SumParams {
                                    // to its own shared memory, [local row][C], not to `part`
 };
 
-// Moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73) pairs/clk/SM against
-// 14.90 with every exp on MUFU (M = N = 1e6, B200): the packed FFMA2s of the expanded form read
-// three register pairs and already load the FP32 pipe close to the MUFU time, so the share is off.
-constexpr bool kPolyShare = false;
+// (Round 1, at 3 CTAs/SM: moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73)
+// pairs/clk/SM against 14.90 with every exp on MUFU; at 4 CTAs/SM the 1/8 share pays, above.)
+// Expanded Gaussian Sum: a share of the exponentials on the FP32 pipe (ex2_poly2: degree-5
+// polynomial + exponent add, 2.3e-7 relative, u in [-24, 6] by the box bound).  At 4 CTAs/SM
+// (FP32 pipe ~48% busy, MUFU 97%) one eighth (mode 3: the last row of a thread, every other
+// record pair) measured 16.66 pairs/clk/SM against 15.43 without (2e6^2); 1/16 16.21, 3/16 15.93,
+// 1/4 15.05 (round 2).  At 3 CTAs/SM in round 1 the share had measured slower.
+#ifndef GENRED_POLY_MODE
+#define GENRED_POLY_MODE 3
+#endif
+constexpr bool kPolyShare = GENRED_POLY_MODE != 0;
 
 // The pair loop + epilogue.  XP selects the expanded form of the Gaussian Sum (MODE 0 only):
 //   exp(-|x-y|^2/sigma^2) = 2^(-|x'|^2) * 2^(u),  u = 2 x'.y' - |y'|^2,  x' = s (x - c)
@@ -256,8 +263,17 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
 #pragma unroll
                     for (int d = 1; d < D; ++d) u = fma2(dup2(xr[r][d]), ny[d], u);   // 2x'.y' - |y'|^2
                     float2 ex;
-                    // FP32-pipe exp2 share (kPolyShare, off: see DESIGN.md Sec. 6 measurements)
-                    if (POLY && r == R - 1 && hh == 0) ex = ex2_poly2(u);
+                    // FP32-pipe exp2 share (GENRED_POLY_MODE above)
+                    // share of the exponentials on the FP32 pipe: mode 1 = 1/(R HH), 2 = 1/R,
+                    // 3 = 1/(2R), 4 = 3/(4R), 5 = 1/(2R) spread over two rows
+                    const bool poly = POLY &&
+                        (GENRED_POLY_MODE == 1 ? (r == R - 1 && hh == 0) :
+                         GENRED_POLY_MODE == 2 ? (r == R - 1) :
+                         GENRED_POLY_MODE == 3 ? (r == R - 1 && (hh & 1) == 0) :
+                         GENRED_POLY_MODE == 4 ? (r == R - 1 && hh != HH - 1) :
+                         GENRED_POLY_MODE == 5 ? ((r == R - 1 && hh == 0) || (r == R - 2 && hh == HH / 2)) :
+                         GENRED_POLY_MODE == 6 ? (hh == 0) : false);
+                    if (poly) ex = ex2_poly2(u);
                     else ex = make_float2(ex2(u.x), ex2(u.y));
                     if constexpr (NG == 0) {
 #pragma unroll

@@ -6,8 +6,10 @@ SURVEY.md Sec. 8(e).  Eq. (1) shards along either axis:
   broadcast once from ``src`` (collective X1) and every rank runs libgenred on its rows.  No
   reduction is needed.  Per-row arithmetic is bitwise that of the single-GPU run only when every
   shard runs the same j-split (pass the same ``split_j`` to all ranks: the automatic planner
-  chooses it from the local M) and the same form (shards of a problem with max(M, N) > 4096 all
-  take the pair-loop kernels; the one-launch small-problem path takes the direct form).
+  chooses it from the local M), the shard boundaries are multiples of ``ISHARD_ALIGN`` rows
+  (``shard_range(M, G, r, align=ISHARD_ALIGN)``) and every shard takes the same form (shards of a
+  problem with max(M, N) > 4096 all take the pair-loop kernels; the one-launch small-problem path
+  takes the direct form).
 * ``jshard_eval`` (M << N): rank r owns [rN/G, (r+1)N/G) of y and b; every rank reduces all M rows
   over its slice and the monoid states are merged:
     Sum      fp64 partials -> all_reduce(SUM)                                        (X3)
@@ -23,9 +25,20 @@ import torch
 import torch.distributed as dist
 
 
-def shard_range(n: int, world: int, rank: int) -> tuple:
-    """Contiguous balanced shard [lo, hi) of n items for `rank` of `world`."""
-    return n * rank // world, n * (rank + 1) // world
+# Row tile of the Sum / LSE row-tile kernels (8 warps x 32 threads x 4 rows).  A row's arithmetic
+# depends on its slot in its row tile (the expanded Gaussian Sum evaluates the exponentials of the
+# last row slot of a thread on the FP32 pipe for every other record pair), so i-shards whose
+# boundaries are multiples of it compute their rows bitwise as the unsharded call does (given the
+# same j-split).
+ISHARD_ALIGN = 1024
+
+
+def shard_range(n: int, world: int, rank: int, align: int = 1) -> tuple:
+    """Contiguous shard [lo, hi) of n items for `rank` of `world`, balanced to within `align` items,
+    with every boundary but the last a multiple of `align`."""
+    def b(r):
+        return n if r >= world else min(n, (n * r // world) // align * align)
+    return b(rank), b(rank + 1)
 
 
 def _default_fns():

@@ -110,8 +110,8 @@ def test_bench_reports_the_form_the_device_chose():
     unit cube takes the expanded form, sigma = 0.05 the direct one (8 FP32 lane-ops per pair in
     the roofline's basis)."""
     d = _run(["--config", "5", "--shape", "200000,200000", "--steps", "3", "--warmup", "3", "--no-e2e"])
-    assert d["config"]["form"] == "expanded" and "128/4 FP32" in d["roofline"]["peak_basis"]
+    assert d["config"]["form"] == "expanded" and "16/0.875 MUFU, 128/5 FP32" in d["roofline"]["peak_basis"]
     d = _run(["--config", "5", "--shape", "200000,200000", "--scale", "0.05", "--steps", "3", "--warmup", "3",
               "--no-e2e"])
-    assert d["config"]["form"] == "direct" and "128/8 FP32" in d["roofline"]["peak_basis"]
+    assert d["config"]["form"] == "direct" and "16/1 MUFU, 128/8 FP32" in d["roofline"]["peak_basis"]
     assert d["cpu_baseline"]["max_r4_err_vs_gpu"] <= 1e-5

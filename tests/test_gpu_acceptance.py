@@ -48,11 +48,13 @@ def host(t):
 
 
 def shard_rows(M, G_, per, seed):
-    """`per` seeded rows from each of the G_ contiguous i-shards [rM/G, (r+1)M/G) (8(e))."""
+    """`per` seeded rows from each of the G_ contiguous i-shards of bench.py's partition
+    (dist.shard_range on the 1024-row tile, 8(e))."""
+    from paper_2004_11127_b200.dist import ISHARD_ALIGN, shard_range
     rng = np.random.default_rng(seed)
     out = []
     for r in range(G_):
-        lo, hi = M * r // G_, M * (r + 1) // G_
+        lo, hi = shard_range(M, G_, r, align=ISHARD_ALIGN)
         out.append(np.sort(rng.choice(np.arange(lo, hi), size=per, replace=False)))
     return np.concatenate(out)
 
@@ -255,19 +257,22 @@ def test_c5_lattice_200x200x250(G):
 
 @pytest.mark.parametrize("split", [1, 3])
 def test_ishard_bitwise_across_1_2_4_8(G, split):
-    """8(e): with the same (forced) j-split every i-shard computes its rows with exactly the
+    """8(e): with the same (forced) j-split and shard boundaries on the 1024-row tile
+    (dist.ISHARD_ALIGN, as bench.py partitions) every i-shard computes its rows with exactly the
     unsharded arithmetic, so the outputs are bitwise equal for G = 1, 2, 4, 8 (each shard run as
     its own call, as a rank would)."""
     M, N = 1_000_003, 200_000
     x = synth.uniform3(M, 151); y = synth.uniform3(N, 152); b = synth.signal(N, 153)
     yd, bd = dev(y), dev(b)
+    from paper_2004_11127_b200.dist import ISHARD_ALIGN, shard_range
     full = host(G.eval("gauss", "sum", dev(x), yd, bd, scale=0.5, split_j=split))
     for Gn in (2, 4, 8):
-        parts = [host(G.eval("gauss", "sum", dev(x[M * r // Gn:M * (r + 1) // Gn]), yd, bd, scale=0.5,
-                             split_j=split)) for r in range(Gn)]
+        rg = [shard_range(M, Gn, r, align=ISHARD_ALIGN) for r in range(Gn)]
+        parts = [host(G.eval("gauss", "sum", dev(x[lo:hi]), yd, bd, scale=0.5, split_j=split)) for lo, hi in rg]
         np.testing.assert_array_equal(np.concatenate(parts), full, err_msg=f"G={Gn}")
     lf = host(G.eval("sqdist", "lse", dev(x[:300_000]), yd, None, scale=0.05, out_dtype="float64", split_j=split))
     for Gn in (2, 4, 8):
-        parts = [host(G.eval("sqdist", "lse", dev(x[300_000 * r // Gn:300_000 * (r + 1) // Gn]), yd, None,
-                             scale=0.05, out_dtype="float64", split_j=split)) for r in range(Gn)]
+        rg = [shard_range(300_000, Gn, r, align=ISHARD_ALIGN) for r in range(Gn)]
+        parts = [host(G.eval("sqdist", "lse", dev(x[lo:hi]), yd, None, scale=0.05, out_dtype="float64",
+                             split_j=split)) for lo, hi in rg]
         np.testing.assert_array_equal(np.concatenate(parts), lf, err_msg=f"lse G={Gn}")

@@ -845,12 +845,12 @@ def test_ishard_rows_bitwise_equal_to_single_gpu(G):
     M, N = 5000, 20000
     x = synth.uniform3(M, 141); y = synth.uniform3(N, 142); b = synth.signal(N, 143)
     full = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.5, split_j=2))
-    for lo, hi in ((0, 1250), (1250, 3333), (3333, 5000)):
+    for lo, hi in ((0, 1024), (1024, 3072), (3072, 5000)):       # boundaries on the row tile
         part = host(G.eval("gauss", "sum", dev(x[lo:hi]), dev(y), dev(b), scale=0.5, split_j=2))
         np.testing.assert_array_equal(part, full[lo:hi])
     lf = host(G.eval("sqdist", "lse", dev(x), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
-    lp = host(G.eval("sqdist", "lse", dev(x[1000:2000]), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
-    np.testing.assert_array_equal(lp, lf[1000:2000])
+    lp = host(G.eval("sqdist", "lse", dev(x[1024:2048]), dev(y), None, scale=0.05, out_dtype="float64", split_j=3))
+    np.testing.assert_array_equal(lp, lf[1024:2048])
 
 
 @pytest.mark.parametrize("with_h", [False, True])
