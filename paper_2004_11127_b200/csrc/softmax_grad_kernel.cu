@@ -15,6 +15,10 @@
 #include "device.cuh"
 #include "internal.h"
 
+// 3 CTAs/SM (80 registers): 8.06 -> 8.18 pairs/clk/SM at 4e5^2 (4: spills, 5.48; round 2)
+#ifndef GENRED_SM_MINB
+#define GENRED_SM_MINB 3
+#endif
 #ifndef GENRED_SM_UNROLL
 #define GENRED_SM_UNROLL 2
 #endif
@@ -47,7 +51,7 @@ struct SmParams {
 };
 
 template <int D, int R>
-__global__ void __launch_bounds__(kThreads, 2) softmax_grad_kernel(const SmParams p) {
+__global__ void __launch_bounds__(kThreads, GENRED_SM_MINB) softmax_grad_kernel(const SmParams p) {
     using Cfg = SmCfg<D>;
     constexpr int RS = Cfg::RS, C = 1 + D;
     extern __shared__ __align__(128) unsigned char smem_raw[];
