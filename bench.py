@@ -74,6 +74,9 @@ def workload(cid: int) -> dict:
         #            is the MUFU's either way (min(16/1, 128/7) = 16 pairs/clk/SM)
         return dict(cfg=c, formula="gauss_sum_gradx", reduction="sum", fp32=7, mufu=1,
                     out_dtype="float32")
+    if cid == 9:   # the x-gradient alone (GAUSS_GRADX), expanded form: u (3) + S0 += e b' (1) +
+        #            S += e (b' y') (3) = 7 lane-ops, as the fused kernel (the Sum column is S0)
+        return dict(cfg=c, formula="gauss_gradx", reduction="sum", fp32=7, mufu=1, out_dtype="float32")
     if cid == 7:   # j-sharded Gaussian Sum (M << N): as C5 per rank, fp64 partials all-reduced
         return dict(cfg=c, formula="gauss", reduction="sum", fp32=5, mufu=7 / 8, out_dtype="float64")
     if cid == 8:   # j-sharded LSE: as C3 per rank, (m, s) states all-gathered and combined
@@ -186,6 +189,8 @@ def cpu_baseline(w: dict, x, y, b, rows: np.ndarray, gpu_rows=None) -> dict:
     elif w["formula"] == "gauss_sum_gradx":
         o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
         oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
+    elif w["formula"] == "gauss_gradx":
+        o, den = oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
     else:
         o, den = oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
     dt = time.perf_counter() - t0
@@ -234,6 +239,8 @@ def run_reference(args, rank: int, world: int) -> None:
             oracle.lse(x, y, None, eps=c.scale, rows=rows)
         elif w["formula"] == "gauss_sum_gradx":
             oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
+            oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
+        elif w["formula"] == "gauss_gradx":
             oracle.gauss_gradx(x, y, b, None, sigma=c.scale, rows=rows)
         else:
             oracle.gauss_sum(x, y, b, sigma=c.scale, rows=rows)
@@ -519,7 +526,8 @@ def main() -> None:
         bd = torch.from_numpy(b).to(dev) if rank == 0 else torch.empty(b.shape, dtype=torch.float32, device=dev)
     Ml = hi - lo
     argk = w["reduction"] == "argkmin"
-    out_shape = (Ml,) if w["reduction"] == "lse" else ((Ml, c.K) if argk else (Ml, c.E))
+    out_shape = (Ml,) if w["reduction"] == "lse" else ((Ml, c.K) if argk else
+                                                       ((Ml, c.D) if w["formula"] == "gauss_gradx" else (Ml, c.E)))
     out = torch.empty(out_shape, dtype=getattr(torch, w["out_dtype"]), device=dev)
     out_idx = torch.empty((Ml, c.K), dtype=torch.int64, device=dev) if argk else None
     out_grad = torch.empty((Ml, c.D), dtype=torch.float32, device=dev) \

@@ -53,6 +53,9 @@ CONFIGS = {
     # Cedge: the memory-bound low-N, high-M edge; N in {1, 2, 4, 8, 16, 32}
     6: Config(6, "Cedge Gaussian Sum M=2^28 N=8 D=3 E=1 sigma=0.5 (HBM-bound)", "gauss", "sum",
               1 << 28, 8, 3, 1, 0.5),
+    # the north star's "gradient form" alone: C2's shape with the x-gradient only (GAUSS_GRADX)
+    9: Config(9, "C2g Gaussian grad_x only M=N=1e5 D=3 E=1 sigma=0.5", "gauss_gradx", "sum",
+              100_000, 100_000, 3, 1, 0.5),
     # the j-shard regime of SURVEY.md 8(e) (M << N; north star (d)): y, b sharded over ranks
     7: Config(7, "Cj Gaussian Sum M=1e4 N=1e8 D=3 E=1 sigma=0.5 (j-sharded)", "gauss", "sum",
               10_000, 100_000_000, 3, 1, 0.5),
