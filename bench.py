@@ -587,6 +587,7 @@ def main() -> None:
     barrier()
     inline_prof = max_over_ranks(w0.elapsed_time(w1)) >= 5.0
     plan = genred.last_plan(local)
+    tiles = genred.last_tiles(local) if plan.get("path") == 3 else (0, 0)
     sampler = ClockSampler(local)
     if not os.environ.get("BENCH_NO_SAMPLER"):
         sampler.start()
@@ -656,13 +657,23 @@ def main() -> None:
         if w["formula"] == "gauss" and plan.get("path") == 0 and not w.get("hbm"):
             w = dict(w, fp32=8, mufu=1)                      # (no polynomial share in the direct form)
         peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
+        basis_extra = ""
+        if w["formula"] == "gauss" and plan.get("path") == 3:
+            # tile-centred form (R18j): centred tiles run the expanded mix, the others the direct
+            # one; the ceiling is the pair-weighted harmonic mix of the two
+            f_loc = tiles[0] / max(tiles[1], 1)
+            p_dir = alu_peak_pairs(8, 1, mhz_max)
+            peak = 1.0 / (f_loc / peak + (1.0 - f_loc) / p_dir)
+            basis_extra = (f"; tile-centred form: {tiles[0]} of {tiles[1]} tiles centred (expanded mix), "
+                           f"the rest direct (16/1 MUFU, 128/8 FP32), harmonic mix")
         achieved = Ml * N / (kmean * 1e-3)
         roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",
                     "frac": achieved / peak, "traffic": traffic,
                     "kernel": f"{w['formula']}/{w['reduction']} pair loop", "kernel_ms": kmean,
                     "share_of_step": kmean / ms_step if world == 1 else None,
                     "peak_basis": f"min({MUFU_PER_CLK_SM}/{w['mufu']:g} MUFU, {FP32_PER_CLK_SM}/{w['fp32']} FP32)"
-                                  f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)",
+                                  f" pairs/clk/SM x {SMS} SMs x {mhz_max:.0f} MHz (sm_max_mhz, MEASURED_PEAKS.json)"
+                                  + basis_extra,
                     "pairs_per_launch": Ml * N}
 
     roofline["kernel_timing"] = kernel_timing
@@ -752,7 +763,8 @@ def main() -> None:
                              "inputs re-read from HBM/L2 each step; no flush",
                        "split_j": plan["split_j"], "rows_per_cta": plan["rows_per_cta"],
                        "ctas": plan["ctas"], "K": c.K if argk else None,
-                       "form": {0: "direct", 1: "tensor", 2: "expanded"}.get(plan.get("path")),
+                       "form": {0: "direct", 1: "tensor", 2: "expanded",
+                                3: f"tile-centred ({tiles[0]} of {tiles[1]} tiles)"}.get(plan.get("path")),
                        "fallback_rows": plan.get("fallback_rows")},
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clocks,
             "gpu_launches": launches,

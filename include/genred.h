@@ -179,12 +179,20 @@ typedef struct {
     int32_t tile_j;          /* j-records per shared-memory stage */
     int32_t kernels;         /* kernels launched by the last call */
     int32_t path;            /* 0 = FP32/MUFU small-D path, 1 = tcgen05 tensor path, 2 = Gaussian
-                                Sum expanded form with the FP32-pipe exp2 share (synchronises) */
+                                Sum expanded form with the FP32-pipe exp2 share (synchronises),
+                                3 = Gaussian Sum tile-centred form (y in Hilbert order, records
+                                centred per 512-j tile; genred_last_tiles counts its tiles) */
     int64_t scratch_bytes;   /* device scratch the last call used (the context may hold more) */
     int64_t fallback_rows;   /* tensor path: rows whose 3xTF32 screening failed the margin
                                 certificate and were rescanned exactly (synchronises; else -1) */
 } genred_plan;
 genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan);
+
+/* Tile-centred form of the last call (plan.path == 3; R18j): the number of 512-j tiles
+ * and how many of them ran the tile-centred expanded form (the others, wider than the radius bound
+ * kExpandedR2Max in sigma units, ran the direct form).  Synchronises (reads the per-tile table).
+ * Other paths: both 0. */
+genred_status genred_last_tiles(const genred_ctx *ctx, int64_t *local_tiles, int64_t *tiles);
 
 /* Total kernels launched by this context since creation (evidence for the bench's
  * gpu_launches claim). */
@@ -207,6 +215,11 @@ int32_t       genred_profile_read(genred_ctx *ctx, float *ms, int32_t max);
  *   "fused_merge"  1 (default; env GENRED_FUSED_MERGE): the last CTA of a row tile merges the
  *                  split partials inside the pair-loop kernel when they are few; 0 always launches
  *                  the finalize kernel.
+ *   "local_form"   Gaussian Sum (D <= 3, row tiles): 1 (default; env GENRED_LOCAL_FORM) orders y
+ *                  along a Hilbert curve and centres the j-records per 512-j tile when
+ *                  N >= 2^18 and M >= 2^16 (the expanded form for clouds wider than the global
+ *                  box allows, R18j); 2 does so at any size above the tiny-problem paths; 0 never.
+ *                  The j-splits then cover whole tiles.
  * Returns GENRED_E_INVALID for an unknown name; affects later calls on this context only. */
 genred_status genred_set_option(genred_ctx *ctx, const char *name, int64_t value);
 

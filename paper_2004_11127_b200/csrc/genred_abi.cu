@@ -40,6 +40,9 @@ struct genred_ctx {
     int64_t tile_done_cap = 0;
     bool small_fused = true;                                   // genred_set_option("small_fused")
     bool fused_merge = true;                                   // genred_set_option("fused_merge")
+    int local_form = 1;                                        // genred_set_option("local_form")
+    const float4 *centers_dev = nullptr;                       // last tile-centred call: per-tile
+    int64_t centers_n = 0;                                     //   (centre, r^2 or -1)
     bool profiling = false;
     std::vector<cudaEvent_t> ev;                               // pairs: (start, stop) per launch
     int nprof = 0;
@@ -167,6 +170,10 @@ constexpr int64_t kMinWaves = GENRED_MIN_WAVES;  // Sum / LSE row-tile kernels: 
 constexpr int64_t kMaxSplitSmm = 2048;       // small-M mode: j-splits (CTAs of a few rows each)
 constexpr int64_t kSmmMaxM = 64;             // small-M mode for M at or below
 constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
+// Tile-centred form of the Gaussian Sum (R18j, tile_order.cu), option local_form = 1: for N and M
+// at or above these (the sort's cost, ~N, against the pair loop's M N)
+constexpr int64_t kLocalMinN = 1 << 18;
+constexpr int64_t kLocalMinM = 1 << 16;
 
 // Choose the j-split S so that itiles*S CTAs fill whole waves of `slots` concurrent CTAs.  The
 // j-axis has `total` units (512-j tiles, or record pairs split in multiples of `grain`); every
@@ -556,13 +563,28 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         const int RS = pack_record_stride(pk, D, E);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const int C = (mode == 1) ? D : (mode == 2) ? E + D : E;
+        // Tile-centred form (R18j): y in Hilbert order, records centred per 512-j tile; the device
+        // takes it where the global box rules the expanded form out (geo.cuh), tile by tile.  The
+        // j-splits then cover whole tiles.
+        const bool local = mode == 0 && !smm && D <= 3 && N > kDirectMaxN && M > kDirectMaxM &&
+                           N < ((int64_t)1 << 31) &&
+                           (ctx->local_form == 2 || (ctx->local_form == 1 && N >= kLocalMinN && M >= kLocalMinM));
+        if (local) {
+            const int64_t P = kTileJ / 2;
+            pl.pairs_per_split = (pl.pairs_per_split + P - 1) / P * P;
+            pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+        }
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * C * 8) : 0;
-        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256);
+        const size_t lbytes = local ? al256((size_t)pl.ntiles * 16) + 4 * al256((size_t)N * 4) +
+                                      al256(tile_order_temp_bytes(N)) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + 256 + lbytes);
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
         uint32_t *geo = (uint32_t *)((char *)ctx->scratch + jbytes + pbytes);
+        char *lbase = (char *)ctx->scratch + jbytes + pbytes + 256;
+        float4 *centers = local ? (float4 *)lbase : nullptr;
         // parameter folding in fp64, rounded once to fp32 (R15, R18)
         float sc = 1.0f;
         double scale_grad = 0.0;
@@ -618,15 +640,27 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             }
         }
         // small problems: the box is reduced inside the pack kernel (one launch fewer)
-        const bool boxed_pack = mode != 3 && !no_box && std::max(M, N) <= kFusedBoxMax;
+        const bool boxed_pack = mode != 3 && !no_box && std::max(M, N) <= kFusedBoxMax && !local;
         if (mode != 3 && !no_box && !boxed_pack) {
             e = launch_bbox(a->x, M, a->y, N, D, geo, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
             kernels++;
         }
         int ctas = 0;
-        e = boxed_pack ? launch_pack_boxed(pk, a->y, a->b, N, D, E, sc, npairs, J, a->x, M, geo, st)
-                       : launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
+        if (local) {
+            char *q = lbase + al256((size_t)pl.ntiles * 16);
+            const size_t nb = al256((size_t)N * 4);
+            uint32_t *keys = (uint32_t *)q, *idx = (uint32_t *)(q + nb), *keys_s = (uint32_t *)(q + 2 * nb),
+                     *perm = (uint32_t *)(q + 3 * nb);
+            int lk = 0;
+            e = launch_tile_order(a->y, a->b, N, D, E, sc, geo, keys, idx, keys_s, perm, q + 4 * nb,
+                                  tile_order_temp_bytes(N), pl.ntiles, J, centers, st, &lk);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "tile order / pack kernels");
+            kernels += lk - 1;
+        } else {
+            e = boxed_pack ? launch_pack_boxed(pk, a->y, a->b, N, D, E, sc, npairs, J, a->x, M, geo, st)
+                           : launch_pack(pk, a->y, a->b, N, D, E, sc, 0.0, npairs, J, st, geo);
+        }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         if (tiny_n && mode == 0 && E == 1 && D <= 4 && N <= sum_edge_max_n() &&
             ((uintptr_t)a->x & 15) == 0) {
@@ -648,6 +682,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.split = pl.split; L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv; L.s = sc;
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
+        L.centers = centers;
         // Few partials per row tile: the last CTA of each row tile merges them (no finalize
         // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.  Only up to 32
         // splits: above that the finalize kernel sums lane-strided (sum_finalize_warp_kernel),
@@ -676,8 +711,10 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         }
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? pl.R : kConsumerWarps * 32 * pl.R;
-        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = local ? 3 : 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
+        ctx->centers_dev = centers;
+        ctx->centers_n = local ? pl.ntiles : 0;
         ctx->geo_dev = mode != 3 ? geo : nullptr;
         ctx->geo_D = D;
         ctx->geo_s = sc;
@@ -877,6 +914,7 @@ genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
     cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, cuda_device);
     if (const char *v = getenv("GENRED_SMALL_FUSED")) ctx->small_fused = atoi(v) != 0;
     if (const char *v = getenv("GENRED_FUSED_MERGE")) ctx->fused_merge = atoi(v) != 0;
+    if (const char *v = getenv("GENRED_LOCAL_FORM")) ctx->local_form = atoi(v);
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
     cudaSetDevice(prev);
@@ -1003,8 +1041,9 @@ genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
     if (!ctx || !plan) return GENRED_E_INVALID;
     *plan = ctx->plan;
     plan->fallback_rows = -1;
-    if (ctx->plan.path == 0 && ctx->geo_dev && geo_expanded_host(ctx->geo_dev, ctx->geo_D, ctx->geo_s))
-        plan->path = 2;                                        // expanded form
+    if ((ctx->plan.path == 0 || ctx->plan.path == 3) && ctx->geo_dev &&
+        geo_expanded_host(ctx->geo_dev, ctx->geo_D, ctx->geo_s))
+        plan->path = 2;                                        // expanded form (global box)
     if (ctx->plan.path == 1 && ctx->fallback_dev) {
         int n = -1;
         if (cudaMemcpy(&n, ctx->fallback_dev, sizeof(int), cudaMemcpyDeviceToHost) != cudaSuccess) {
@@ -1017,6 +1056,20 @@ genred_status genred_last_plan(const genred_ctx *ctx, genred_plan *plan) {
 }
 
 int64_t genred_launch_count(const genred_ctx *ctx) { return ctx ? ctx->launches : 0; }
+
+genred_status genred_last_tiles(const genred_ctx *ctx, int64_t *local_tiles, int64_t *tiles) {
+    if (!ctx || !local_tiles || !tiles) return GENRED_E_INVALID;
+    *local_tiles = 0;
+    *tiles = ctx->plan.path == 3 ? ctx->centers_n : 0;
+    if (ctx->plan.path != 3 || !ctx->centers_dev || ctx->centers_n == 0) return GENRED_OK;
+    std::vector<float4> h((size_t)ctx->centers_n);
+    if (cudaMemcpy(h.data(), ctx->centers_dev, h.size() * sizeof(float4), cudaMemcpyDeviceToHost) != cudaSuccess) {
+        cudaGetLastError();
+        return GENRED_E_CUDA;
+    }
+    for (const float4 &c : h) *local_tiles += c.w >= 0.0f;
+    return GENRED_OK;
+}
 
 genred_status genred_profile(genred_ctx *ctx, int32_t enable) {
     if (!ctx) return GENRED_E_INVALID;
@@ -1041,6 +1094,11 @@ genred_status genred_set_option(genred_ctx *ctx, const char *name, int64_t value
     const std::string n(name);
     if (n == "small_fused") { ctx->small_fused = value != 0; return GENRED_OK; }
     if (n == "fused_merge") { ctx->fused_merge = value != 0; return GENRED_OK; }
+    if (n == "local_form") {
+        if (value < 0 || value > 2) return fail(ctx, GENRED_E_INVALID, "local_form is 0, 1 or 2");
+        ctx->local_form = (int)value;
+        return GENRED_OK;
+    }
     return fail(ctx, GENRED_E_INVALID, "unknown option '" + n + "'");
 }
 

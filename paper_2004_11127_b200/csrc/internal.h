@@ -112,8 +112,19 @@ struct SumLaunch {
     int64_t n_units;
     unsigned *tile_done = nullptr;  // split > 1: zeroed per-row-tile counters -> merge in the kernel
     int num_sms = 148;        // persistent grid: at most num_sms x occupancy CTAs
+    // MODE 0, tile-centred form (tile_order.cu, R18j): per 512-j tile (centre, radius^2 or -1 =
+    // direct layout); pairs_per_split is then a multiple of kTileJ / 2
+    const float4 *centers = nullptr;
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
+// Tile-centred form (tile_order.cu): Hilbert keys of y over its box (geo), a radix sort of
+// (key, j), and the per-tile pack (records + centers).  Scratch: keys/idx/keys_s/perm N words
+// each, temp = tile_order_temp_bytes(N).  *kernels = kernels launched.
+size_t tile_order_temp_bytes(int64_t N);
+cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, int E, float s,
+                              const uint32_t *geo, uint32_t *keys, uint32_t *idx, uint32_t *keys_s,
+                              uint32_t *perm, void *temp, size_t temp_bytes, int64_t ntiles, float *J,
+                              float4 *centers, cudaStream_t st, int *kernels);
 // Small problems in one launch (sum_small_kernel, sum_body.cuh): E = 1, D <= 4, j-splits of at
 // most kSmallMaxPairs record pairs (the CTA's records live in shared memory); a.J is unused.
 constexpr int64_t kSmallMaxPairs = 512;

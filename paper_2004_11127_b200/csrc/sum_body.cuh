@@ -95,6 +95,7 @@ struct SumParams {
                               // between calls); the last CTA of a row tile merges its partials
     double *part_smem = nullptr;   // sum_small_kernel with a cluster merge: this CTA's partials go
                                    // to its own shared memory, [local row][C], not to `part`
+    const float4 *centers = nullptr;   // MODE 0 tile-centred form: per 512-j tile (c_k, r_k^2 or -1)
 };
 
 // (Round 1, at 3 CTAs/SM: moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73)
@@ -491,6 +492,156 @@ __device__ __forceinline__ void sum_body(const SumParams &p, Ring &ring, int nt,
     }
 }
 
+// The tile-centred expanded form of the Gaussian Sum (MODE 0, tile_order.cu, R18j).
+// y is ordered along a Hilbert curve and each 512-j tile k carries its records around its own
+// centre c_k: y'' = s (y - c_k), w = -|y''|^2.  For a row, x'' = s (x - c_k) (from RAW x, so the
+// rounding is relative to |x - c_k|), and
+//   exp(-|x - y|^2 / sigma^2) = 2^(-|x''|^2) * 2^(u),   u = 2 x''.y'' - |y''|^2,
+// the pair loop of sum_body's expanded form (3 FFMA + exp + 1 FFMA per pair, the same FP32-pipe
+// exp2 share) with the row factor 2^(-|x''|^2) applied per tile in fp64 when the tile's fp32 sums
+// are promoted.  A row farther than r_k + 11.5 from c_k (every term of the tile below 2^-121, the
+// deep tail of reading R4c) takes x'' = 0 and factor 0, which also keeps 2^u finite (u <= 68).
+// Tiles whose radius fails |y''|^2 <= kExpandedR2Max keep the direct layout and run the direct
+// form's loop on raw differences (R18e).
+template <int D, int E, int R, class Ring>
+__device__ __forceinline__ void sum_body_local(const SumParams &p, Ring &ring, int nt, int last_np,
+                                               int64_t row0, int64_t row_end, int sp, int64_t tile0) {
+    using Cfg = SumCfg<0, D, E>;
+    constexpr int RS = Cfg::RS, BOFF = Cfg::BOFF;
+    constexpr bool POLY = kPolyShare && R == 4;
+    constexpr int HH = GENRED_SUM_HH;
+    const int ct = threadIdx.x;
+    const float2 negs2 = dup2(-(p.s * p.s));
+    float xw[R][D];                                   // raw x rows
+    double acc64[R][E];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+#pragma unroll
+        for (int d = 0; d < D; ++d) xw[r][d] = i < row_end ? __ldg(p.x + i * D + d) : 0.0f;
+#pragma unroll
+        for (int e = 0; e < E; ++e) acc64[r][e] = 0.0;
+    }
+    for (int k = 0; k < nt; ++k) {
+        const float4 cen = __ldg(p.centers + tile0 + k);
+        const float *tile = ring.acquire(k);
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
+        float2 acc[R][E];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int e = 0; e < E; ++e) acc[r][e] = make_float2(0.f, 0.f);
+        if (cen.w >= 0.0f) {
+            const float cc[3] = {cen.x, cen.y, cen.z};
+            const float lim = sqrtf(cen.w) + 11.5f;
+            float xl[R][D];                           // 2 x''
+            unsigned far = 0u;
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                float q = 0.0f;
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const float h = p.s * (xw[r][d] - cc[d]);
+                    xl[r][d] = 2.0f * h;
+                    q = fmaf(h, h, q);
+                }
+                if (q > lim * lim) {
+                    far |= 1u << r;
+#pragma unroll
+                    for (int d = 0; d < D; ++d) xl[r][d] = 0.0f;
+                }
+            }
+            for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+            for (int hh = 0; hh < HH; ++hh) {
+                float f[RS];
+#pragma unroll
+                for (int q = 0; q < RS / 4; ++q) {
+                    const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                    f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+                }
+                const float2 w = make_float2(f[2 * D], f[2 * D + 1]);              // -|y''|^2
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 u = fma2(dup2(xl[r][0]), make_float2(f[0], f[1]), w);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(dup2(xl[r][d]), make_float2(f[2 * d], f[2 * d + 1]), u);
+                    const bool poly = POLY && (r == R - 1 && (hh & 1) == 0);      // GENRED_POLY_MODE 3
+                    const float2 ex = poly ? ex2_poly2(u) : make_float2(ex2(u.x), ex2(u.y));
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+                        acc[r][e] = fma2(ex, make_float2(f[BOFF + 2 * e], f[BOFF + 2 * e + 1]), acc[r][e]);
+                }
+            }
+            }
+            ring.release(k);
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                // row factor 2^(-|x''|^2) in fp64 from the same x'' (= xl / 2, exact): 2^-n exact,
+                // 2^-f (f in [0, 1)) by MUFU.EX2 (2^-22 relative)
+                double q64 = 0.0;
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    const double hd = 0.5 * (double)xl[r][d];
+                    q64 = fma(hd, hd, q64);
+                }
+                const double n = floor(q64);
+                const double fac = ((far >> r) & 1u) ? 0.0 : ldexp((double)ex2(-(float)(q64 - n)), -(int)n);
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc64[r][e] += fac * ((double)acc[r][e].x + (double)acc[r][e].y);
+            }
+        } else {
+            for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+            for (int hh = 0; hh < HH; ++hh) {
+                float f[RS];
+#pragma unroll
+                for (int q = 0; q < RS / 4; ++q) {
+                    const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                    f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    float2 dd[D];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) dd[d] = add2(dup2(xw[r][d]), make_float2(f[2 * d], f[2 * d + 1]));
+                    float2 q = mul2(dd[0], dd[0]);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) q = fma2(dd[d], dd[d], q);         // |x - y|^2 (raw)
+                    const float2 tq = mul2(q, negs2);
+                    const float2 ex = make_float2(ex2(tq.x), ex2(tq.y));
+#pragma unroll
+                    for (int e = 0; e < E; ++e)
+                        acc[r][e] = fma2(ex, make_float2(f[BOFF + 2 * e], f[BOFF + 2 * e + 1]), acc[r][e]);
+                }
+            }
+            }
+            ring.release(k);
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+#pragma unroll
+                for (int e = 0; e < E; ++e) acc64[r][e] += (double)acc[r][e].x + (double)acc[r][e].y;
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= row_end) continue;
+        if (p.split > 1) {
+            double *dst = p.part + ((int64_t)sp * p.M + i) * E;
+#pragma unroll
+            for (int e = 0; e < E; ++e) dst[e] = acc64[r][e];
+            continue;
+        }
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            const double v = acc64[r][e] * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i * E + e] = v;
+            else ((float *)p.out)[i * E + e] = (float)v;
+        }
+    }
+}
+
 // CTAs per SM the register allocation must allow (the 16 K registers of each SM sub-partition)
 template <int MODE, int D, int E, int R, bool SMM>
 constexpr int sum_min_blocks() {
@@ -583,7 +734,16 @@ sum_kernel(const SumParams p) {
         const Geo geo = geo_decode(p.geo, D, p.s);     // same decision as the pack kernel
         ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
         if (geo.expanded) sum_body<MODE, D, E, R, true, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
-        else sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+        else {
+            bool local = false;
+            if constexpr (MODE == 0 && !SMM && D <= 3) {
+                if (p.centers && !p.units) {           // tile-centred form (R18j)
+                    sum_body_local<D, E, R>(p, ring, nt, last_np, row0, row_end, sp, q0 / Cfg::PAIRS);
+                    local = true;
+                }
+            }
+            if (!local) sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
+        }
     } else {
         ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * Cfg::RS, nt, kConsumerWarps, last_bytes);
         Geo geo{};

@@ -112,6 +112,9 @@ def load():
         if hasattr(lib, "genred_set_option"):          # (older builds of the library lack it)
             lib.genred_set_option.argtypes = [P, ctypes.c_char_p, I64]
             lib.genred_set_option.restype = I32
+        if hasattr(lib, "genred_last_tiles"):
+            lib.genred_last_tiles.argtypes = [P, ctypes.POINTER(I64), ctypes.POINTER(I64)]
+            lib.genred_last_tiles.restype = I32
         if lib.genred_abi_version() != ABI_VERSION:
             raise RuntimeError("libgenred ABI version mismatch")
         _lib = lib
@@ -144,6 +147,17 @@ def last_plan(device: int | None = None) -> dict:
     p = Plan()
     load().genred_last_plan(context(device), ctypes.byref(p))
     return {k: getattr(p, k) for k, _ in Plan._fields_}
+
+
+def last_tiles(device: int | None = None) -> tuple[int, int]:
+    """(tiles that ran the tile-centred expanded form, all 512-j tiles) of the last call when it
+    took the tile-centred path (plan path 3, R18j); (0, 0) otherwise.  Synchronises."""
+    loc, tot = ctypes.c_int64(0), ctypes.c_int64(0)
+    ctx = context(device)
+    st = load().genred_last_tiles(ctx, ctypes.byref(loc), ctypes.byref(tot))
+    if st != OK:
+        raise GenredError(st, load().genred_last_error(ctx).decode())
+    return int(loc.value), int(tot.value)
 
 
 def launch_count(device: int | None = None) -> int:
@@ -290,7 +304,7 @@ def prepare(formula: str, reduction: str, x, y, b=None, g=None, *, scale: float 
 
 
 def set_option(name: str, value: int, device: int | None = None) -> None:
-    """genred_set_option on the device's context ("small_fused", "fused_merge")."""
+    """genred_set_option on the device's context ("small_fused", "fused_merge", "local_form")."""
     ctx = context(device)
     st = load().genred_set_option(ctx, name.encode(), int(value))
     if st != OK:

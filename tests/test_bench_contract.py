@@ -115,3 +115,8 @@ def test_bench_reports_the_form_the_device_chose():
               "--no-e2e"])
     assert d["config"]["form"] == "direct" and "16/1 MUFU, 128/8 FP32" in d["roofline"]["peak_basis"]
     assert d["cpu_baseline"]["max_r4_err_vs_gpu"] <= 1e-5
+    # N >= 2^18, M >= 2^16: the tile-centred form (R18j), its tiles counted in config.form
+    d = _run(["--config", "5", "--shape", "400000,400000", "--scale", "0.05", "--steps", "3", "--warmup", "3",
+              "--no-e2e"])
+    assert d["config"]["form"].startswith("tile-centred (") and "harmonic mix" in d["roofline"]["peak_basis"]
+    assert d["cpu_baseline"]["max_r4_err_vs_gpu"] <= 1e-5

@@ -452,6 +452,76 @@ def test_gauss_sum_expanded_and_direct_paths(G, case):
     assert_sum_parity(host(a), o, den, what=f"gauss {case}")
 
 
+def _local_case(case):
+    """Inputs of the tile-centred form tests: (x, y, b, sigma, expect) with expect = "all" (every
+    tile centred), "mixed" (some tiles keep the direct layout) or "global" (the global box admits
+    the expanded form: path 2)."""
+    rng = np.random.default_rng(sum(map(ord, case)))
+    if case == "u3_s025":
+        return synth.uniform3(20000, 1), synth.uniform3(30001, 2), synth.signal(30001, 3), 0.25, "all"
+    if case == "u3_s005_mixed":            # 512 points per tile too sparse for sigma = 0.05 here
+        return synth.uniform3(4000, 1), synth.uniform3(400_000, 2), synth.signal(400_000, 3), 0.05, "mixed"
+    if case == "gmm_signed":
+        return synth.gmm3(6000, 1), synth.gmm3(60000, 2), synth.signal(60000, 3, signed=True), 0.05, "mixed"
+    if case == "far_offset":
+        return ((synth.uniform3(8000, 1) + 1000).astype(np.float32),
+                (synth.uniform3(40000, 2) + 1000).astype(np.float32), synth.signal(40000, 3), 0.2, "all")
+    if case == "D2":
+        return (rng.random((3000, 2)).astype(np.float32), rng.random((50000, 2)).astype(np.float32),
+                synth.signal(50000, 4), 0.05, "mixed")
+    if case == "D1":
+        return (rng.random((3000, 1)).astype(np.float32), rng.random((70000, 1)).astype(np.float32),
+                synth.signal(70000, 5), 0.01, "all")
+    if case == "E2_ragged":
+        return synth.uniform3(5001, 6), synth.uniform3(33333, 7), synth.signal(33333, 8, E=2), 0.25, "all"
+    if case == "outliers":                 # a few far points: their tiles keep the direct layout
+        y = synth.uniform3(30000, 9)
+        y[::101] *= 40.0
+        return synth.uniform3(5000, 10), y, synth.signal(30000, 11), 0.25, "mixed"
+    if case == "global_box":               # narrow cloud: the global box wins (path 2)
+        return synth.uniform3(5000, 12), synth.uniform3(20000, 13), synth.signal(20000, 14), 0.8, "global"
+    raise ValueError(case)
+
+
+@pytest.mark.parametrize("case", ["u3_s025", "u3_s005_mixed", "gmm_signed", "far_offset", "D2", "D1",
+                                  "E2_ragged", "outliers", "global_box"])
+def test_gauss_sum_tile_centred_form(G, monkeypatch, case):
+    """Tile-centred expanded form (reading R18j): y in Hilbert order, records centred per 512-j
+    tile, tiles too wide for the radius bound on the direct form, the global box first.  Forced
+    at test sizes (option local_form = 2); every row against the oracle at the plain R4 bar, and
+    bitwise reproducible."""
+    option(G, monkeypatch, "local_form", 2)
+    x, y, b, sigma, expect = _local_case(case)
+    a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=sigma)
+    plan = G.last_plan()
+    loc, tot = G.last_tiles()
+    if expect == "global":
+        assert plan["path"] == 2, plan
+    else:
+        assert plan["path"] == 3 and tot == (len(y) + 511) // 512, (plan, loc, tot)
+        assert (loc == tot) if expect == "all" else (0 < loc < tot), (loc, tot)
+    o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+    assert_sum_parity(host(a), o, den, what=f"tile-centred {case}")
+    a2 = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=sigma)
+    np.testing.assert_array_equal(host(a2), host(a))
+
+
+@pytest.mark.parametrize("split", [1, 3, 40])
+def test_tile_centred_splits_and_ishards(G, monkeypatch, split):
+    """The tile-centred form with forced j-splits (rounded to whole 512-j tiles) against the
+    oracle, and i-shards on 1024-row boundaries bitwise equal to the full call (north star (d))."""
+    option(G, monkeypatch, "local_form", 2)
+    M, N = 6000, 60000
+    x = synth.uniform3(M, 21); y = synth.uniform3(N, 22); b = synth.signal(N, 23, signed=True)
+    full = host(G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=0.1, split_j=split))
+    assert G.last_plan()["path"] == 3
+    o, den = oracle.gauss_sum(x, y, b, sigma=0.1)
+    assert_sum_parity(full, o, den, what=f"tile-centred split {split}")
+    for lo, hi in ((0, 1024), (1024, 3072), (3072, 6000)):
+        part = host(G.eval("gauss", "sum", dev(x[lo:hi]), dev(y), dev(b), scale=0.1, split_j=split))
+        np.testing.assert_array_equal(part, full[lo:hi])
+
+
 @pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
 @pytest.mark.parametrize("M,N,D", [(1, 200_000, 3), (5, 70_001, 2), (37, 150_000, 4), (64, 100_000, 1),
                                    (300, 400_000, 3)])
@@ -1039,7 +1109,10 @@ def test_randomized_hard_inputs(G, seed):
     red = str(rng.choice(["gauss", "gauss_sum_gradx", "lse", "argkmin", "lse_grad"]))
     split = int(rng.choice([0, 0, 3]))
     E = int(rng.choice([1, 1, 2, 3]))
-    tag = f"hard seed {seed} (D={D} M={M} N={N} E={E} off={off} spread={spread} split={split})"
+    lf = int(rng.choice([1, 2]))                               # tile-centred form forced or auto
+    tag = f"hard seed {seed} (D={D} M={M} N={N} E={E} off={off} spread={spread} split={split} lf={lf})"
+    G.set_option("local_form", lf)
+    _RESTORE.append("local_form")
     if red in ("gauss", "gauss_sum_gradx"):
         b = rng.standard_normal((N, E)).astype(np.float32)
         g = rng.standard_normal((M, E)).astype(np.float32) if E > 1 else None

@@ -1,0 +1,85 @@
+"""Tile-centred form of the Gaussian Sum (R18j): parity against the oracle on a few shapes and the
+pair-loop time against the direct form.
+
+  python tools/local_check.py [parity] [time]
+"""
+import os
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import oracle  # noqa: E402
+import synth  # noqa: E402
+from paper_2004_11127_b200 import genred as G  # noqa: E402
+from tests.parity import r4_error  # noqa: E402
+
+
+def dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).cuda()
+
+
+def parity():
+    rng = np.random.default_rng(5)
+    cases = [
+        ("u3 s0.25", synth.uniform3(20000, 1), synth.uniform3(30001, 2), synth.signal(30001, 3), 0.25),
+        ("u3 s0.15 mixed", synth.uniform3(20000, 1), synth.uniform3(30001, 2), synth.signal(30001, 3), 0.15),
+        ("u3 s0.05", synth.uniform3(4000, 1), synth.uniform3(400000, 2), synth.signal(400000, 3), 0.05),
+        ("gmm s0.05", synth.gmm3(6000, 1), synth.gmm3(60000, 2), synth.signal(60000, 3, signed=True), 0.05),
+        ("far 1000", (synth.uniform3(8000, 1) + 1000).astype(np.float32),
+         (synth.uniform3(40000, 2) + 1000).astype(np.float32), synth.signal(40000, 3), 0.2),
+    ]
+    y = rng.random((50000, 2)).astype(np.float32)
+    cases.append(("D2 s0.05", rng.random((3000, 2)).astype(np.float32), y, synth.signal(50000, 4), 0.05))
+    y = rng.random((70000, 1)).astype(np.float32)
+    cases.append(("D1 s0.01", rng.random((3000, 1)).astype(np.float32), y, synth.signal(70000, 5), 0.01))
+    yo = synth.uniform3(30000, 7)
+    yo[::101] *= 40.0                                   # outliers: wide tiles stay direct
+    cases.append(("outliers", synth.uniform3(5000, 8), yo, synth.signal(30000, 9), 0.25))
+    G.set_option("local_form", 2)
+    for name, x, y, b, sig in cases:
+        a = G.eval("gauss", "sum", dev(x), dev(y), dev(b), scale=sig)
+        plan = G.last_plan()
+        lt = G.last_tiles()
+        t0 = time.time()
+        o, den = oracle.gauss_sum(x, y, b, sigma=sig)
+        err = r4_error(a.cpu().numpy(), o, den)
+        print(f"{name:16s} M={len(x):6d} N={len(y):7d} path={plan['path']} split={plan['split_j']} "
+              f"tiles={lt} maxR4={err.max():.3e} meanR4={err.mean():.2e} (oracle {time.time() - t0:.1f}s)",
+              flush=True)
+    G.set_option("local_form", 1)
+
+
+def timing():
+    for (M, N, sig) in [(2_000_000, 2_000_000, 0.05), (1_000_000, 1_000_000, 0.05), (1_000_000, 1_000_000, 0.1)]:
+        x = dev(synth.uniform3(M, 1)); y = dev(synth.uniform3(N, 2)); b = dev(synth.signal(N, 3))
+        for lf in (0, 1):
+            G.set_option("local_form", lf)
+            for _ in range(2):
+                G.eval("gauss", "sum", x, y, b, scale=sig)
+            torch.cuda.synchronize()
+            G.profile(True)
+            t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(3):
+                G.eval("gauss", "sum", x, y, b, scale=sig)
+            t1.record(); torch.cuda.synchronize()
+            ms = G.profile_read()
+            G.profile(False)
+            plan = G.last_plan()
+            lt = G.last_tiles()
+            step = t0.elapsed_time(t1) / 3
+            print(f"M={M} N={N} sigma={sig} local_form={lf} path={plan['path']} tiles={lt} "
+                  f"kernel {min(ms):.2f} ms step {step:.2f} ms pairs/clk/SM {M * N / (min(ms) * 1e-3) / (148 * 1.965e9):.2f}",
+                  flush=True)
+    G.set_option("local_form", 1)
+
+
+if __name__ == "__main__":
+    what = sys.argv[1:] or ["parity", "time"]
+    if "parity" in what:
+        parity()
+    if "time" in what:
+        timing()
