@@ -736,17 +736,49 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             pl.R = Rs;
         }
         const int pk = a->b ? PACK_LSE_H : PACK_LSE_HZ;
-        const int RS = pack_record_stride(pk, D, 1);
+        // Tile-centred form (R18j): as the Gaussian Sum's, with the LSE's own radius bound
+        const bool local = !smm && D <= 3 && pl.R == 4 && N > kDirectMaxN && M > kDirectMaxM &&
+                           N < ((int64_t)1 << 31) &&
+                           (ctx->local_form == 2 || (ctx->local_form == 1 && N >= kLocalMinN && M >= kLocalMinM));
+        if (local) {
+            const int64_t P = kTileJ / 2;
+            pl.pairs_per_split = (pl.pairs_per_split + P - 1) / P * P;
+            pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+        }
+        const int RS = local ? lse_local_record_stride(D, a->b == nullptr) : pack_record_stride(pk, D, 1);
         const int64_t npairs = pl.ntiles * (kTileJ / 2);
         const size_t jbytes = al256((size_t)npairs * RS * 4);
         const size_t pbytes = pl.split > 1 ? al256((size_t)pl.split * M * 2 * 8) : 0;
-        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes);
+        const size_t lbytes = local ? 256 + al256((size_t)pl.ntiles * 16) + 4 * al256((size_t)N * 4) +
+                                      al256(tile_order_temp_bytes(N)) : 0;
+        genred_status s = ensure(ctx, &ctx->scratch, &ctx->scratch_cap, jbytes + pbytes + lbytes);
         if (s != GENRED_OK) return s;
         float *J = (float *)ctx->scratch;
         double *part = pl.split > 1 ? (double *)((char *)ctx->scratch + jbytes) : nullptr;
-        e = launch_pack(pk, a->y, a->b, N, D, 1, 1.0f, kLog2e, npairs, J, st);
+        float4 *centers = nullptr;
+        const float sl = (float)sqrt(kLog2e / a->scale);     // s units of the tile-centred form
+        int kernels = 2;
+        if (local) {
+            char *lb = (char *)ctx->scratch + jbytes + pbytes;
+            uint32_t *geo = (uint32_t *)lb;
+            centers = (float4 *)(lb + 256);
+            char *q = lb + 256 + al256((size_t)pl.ntiles * 16);
+            const size_t nb = al256((size_t)N * 4);
+            e = launch_bbox(a->x, M, a->y, N, D, geo, st);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "bbox kernel");
+            int lk = 0;
+            e = launch_tile_order(a->y, a->b, N, D, 1, sl, geo, (uint32_t *)q, (uint32_t *)(q + nb),
+                                  (uint32_t *)(q + 2 * nb), (uint32_t *)(q + 3 * nb), q + 4 * nb,
+                                  tile_order_temp_bytes(N), pl.ntiles, J, centers, st, &lk, 1, RS, kLog2e,
+                                  kLseLocalR2Max);
+            if (e != cudaSuccess) return cuda_fail(ctx, e, "tile order / pack kernels");
+            kernels += lk;                               // bbox + keys + sort + pack (pack counted in 2)
+        } else {
+            e = launch_pack(pk, a->y, a->b, N, D, 1, 1.0f, kLog2e, npairs, J, st);
+        }
         if (e != cudaSuccess) return cuda_fail(ctx, e, "pack kernel");
         LseLaunch L;
+        L.centers = centers; L.s = sl;
         L.D = D; L.R = pl.R; L.x = a->x; L.J = J; L.M = M; L.split = pl.split;
         L.pairs_per_split = pl.pairs_per_split; L.npv = pl.npv;
         L.negc = (float)(-kLog2e / a->scale);
@@ -758,7 +790,6 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         e = smm ? launch_lse_smm(L, st, &ctas) : launch_lse(L, st, &ctas);
         prof_event(ctx, false, st);
         if (e != cudaSuccess) return cuda_fail(ctx, e, "lse kernel");
-        int kernels = 2;
         if (pl.split > 1) {
             e = launch_lse_finalize(part, pl.split, M, a->out, out_f64, a->lse_state, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "lse finalize kernel");
@@ -766,8 +797,11 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         }
         ctx->launches += kernels;
         ctx->plan.split_j = pl.split; ctx->plan.rows_per_cta = smm ? pl.R : kConsumerWarps * 32 * pl.R;
-        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = 0;
+        ctx->plan.ctas = ctas; ctx->plan.kernels = kernels; ctx->plan.path = local ? 3 : 0;
         ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
+        ctx->centers_dev = centers;
+        ctx->centers_n = local ? pl.ntiles : 0;
+        ctx->geo_dev = nullptr;
         return GENRED_OK;
     }
 

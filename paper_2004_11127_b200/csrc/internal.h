@@ -124,7 +124,8 @@ size_t tile_order_temp_bytes(int64_t N);
 cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, int E, float s,
                               const uint32_t *geo, uint32_t *keys, uint32_t *idx, uint32_t *keys_s,
                               uint32_t *perm, void *temp, size_t temp_bytes, int64_t ntiles, float *J,
-                              float4 *centers, cudaStream_t st, int *kernels);
+                              float4 *centers, cudaStream_t st, int *kernels, int lse = 0, int RS_lse = 0,
+                              double hscale = 0.0, float r2max = 6.0f);
 // Small problems in one launch (sum_small_kernel, sum_body.cuh): E = 1, D <= 4, j-splits of at
 // most kSmallMaxPairs record pairs (the CTA's records live in shared memory); a.J is unused.
 constexpr int64_t kSmallMaxPairs = 512;
@@ -156,8 +157,16 @@ struct LseLaunch {
     double *state;            // split == 1: optional M x 2 state; split > 1: split x M x 2 partials
     const RangeUnit *units = nullptr;   // block-sparse ranges (device), or nullptr
     int64_t n_units = 0;
+    // tile-centred form (lse_kernel.cu, R18j): per-tile table of tile_order.cu, s = sqrt(log2 e / eps)
+    const float4 *centers = nullptr;
+    float s = 0.0f;
 };
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas);
+// Record stride (floats per record pair) of the tile-centred LSE layout (tile_order.cu)
+int lse_local_record_stride(int D, bool hz);
+// Tile radius bound (s units, squared) of the tile-centred LSE: the exponent's fp32 rounding stays
+// below ~3 ulp(4) for the dominant terms (1e-6 absolute bar of R6; R18j)
+constexpr float kLseLocalR2Max = 0.5f;
 // Small-M mode (lse_kernel.cu): CTAs of lse_smm_rows(D) rows whose threads split j; grid =
 // ceil(M / R) * split, split-major, 2 CTAs per SM.
 int lse_smm_rows(int D);

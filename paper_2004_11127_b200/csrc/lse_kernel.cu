@@ -61,6 +61,8 @@ struct LseCfg {
 };
 
 struct LseParams {
+    const float4 *centers = nullptr;   // tile-centred form: per 512-j tile (c_k, r_k^2 or -1)
+    float s = 0.0f;                    // tile-centred form: sqrt(log2(e) / eps)
     const float *x, *J;
     int64_t M;
     int split;
@@ -348,6 +350,270 @@ __global__ void __launch_bounds__(kThreads, lse_min_blocks<D, R>(HZ)) lse_kernel
     }
 }
 
+// ---- tile-centred form (R18j; records by tile_order.cu) ------------------------------
+// y in Hilbert order; a 512-j tile k whose radius (s units, s = sqrt(log2(e)/eps)) is at most
+// kLseLocalR2Max carries y'' = s (y - c_k) and w = fl32(h' - |y''|^2) (+ c = 2^(rest) with h),
+// so that for x'' = s (x - c_k) (from raw x)
+//     v_ij = -|x'' - y''|^2 + h'_j = o_i + (2 x''.y'' + w_j),     o_i = -|x''|^2  (fp64, per tile)
+// and a pair costs FADD (w - m') + D FFMA + MUFU.EX2 + 1 accumulate: 5 FP32 lane-ops against
+// the raw-difference loop's 8, so MUFU becomes the only bound.  Wider tiles keep the direct
+// layout and the raw-difference loop (R6).  Each row keeps its reference M_i in fp64; at a tile
+// start the fp32 reference of the tile's frame is m' = fl32(M_i - o_i) and M_i is moved to
+// m' + o_i exactly (the fp64 sum is rescaled by 2^(M_old - M_new), a few ulps of m'), so every
+// fp32 term 2^(u - m') is relative to M_i.  The lazy rescale (kSumMax) works in the tile frame.
+template <int D, bool HZ>
+struct LseLocCfg {
+    static constexpr int RS = ((2 * D + 2 + (HZ ? 0 : 2)) + 3) / 4 * 4;
+    static constexpr int PAIRS = kTileJ / 2;
+    static constexpr int TILE_FLOATS = PAIRS * RS;
+    static constexpr int SMEM = JRing<kStages>::smem_bytes(TILE_FLOATS);
+};
+int lse_local_record_stride(int D, bool hz) { return ((2 * D + 2 + (hz ? 0 : 2)) + 3) / 4 * 4; }
+
+// Rare path of the tile-centred loop: exact max of the sub-chunk's values in the tile frame, the
+// fp64 sum rescaled, the sub-chunk recomputed (as lse_rescale).  xv: 2 x'' (centred tile) or raw x.
+template <int D, bool HZ, int RS>
+__device__ __noinline__ LseRescale lse_local_rescale(const float *base, const float (&xv)[D], bool loc, float negc,
+                                                     float m_old, double s64, float s32) {
+    auto value = [&](const float *rec, int h) {
+        if (loc) {
+            float u = rec[2 * D + h];
+#pragma unroll
+            for (int d = 0; d < D; ++d) u = fmaf(xv[d], rec[2 * d + h], u);
+            return u;
+        }
+        float q1 = 0.f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) {
+            const float dd = xv[d] + rec[2 * d + h];
+            q1 = fmaf(dd, dd, q1);
+        }
+        return fmaf(q1, negc, HZ ? 0.0f : rec[2 * D + h]);
+    };
+    float vmax = -INFINITY;
+    for (int q = 0; q < kSub; ++q)
+        for (int h = 0; h < 2; ++h) vmax = fmaxf(vmax, value(base + q * RS, h));
+    LseRescale o;
+    o.m = fmaxf(vmax, m_old);
+    o.s64 = (s64 + (double)s32) * exp2((double)m_old - (double)o.m);
+    float c1 = 0.f;
+    for (int q = 0; q < kSub; ++q)
+        for (int h = 0; h < 2; ++h) {
+            const float *rec = base + q * RS;
+            const float cj = HZ ? 1.0f : rec[2 * D + 2 + h];
+            c1 = fmaf(ex2(value(rec, h) - o.m), cj, c1);
+        }
+    o.c1 = c1;
+    return o;
+}
+
+// (1/8 of the exponentials on the FP32 pipe, as the Sum: 14.54 against 14.63 pairs/clk/SM with
+// h = 0 and 14.14 against 14.46 with h at C3's shape -- not used; 3 CTAs/SM the same as 4)
+#ifndef GENRED_LSE_POLY
+#define GENRED_LSE_POLY 0
+#endif
+#ifndef GENRED_LSE_LOC_MINB
+#define GENRED_LSE_LOC_MINB 4
+#endif
+
+template <int D, bool HZ>
+__global__ void __launch_bounds__(kThreads, HZ ? GENRED_LSE_LOC_MINB : 3) lse_local_kernel(const LseParams p) {
+    using Cfg = LseLocCfg<D, HZ>;
+    constexpr int RS = Cfg::RS;
+    constexpr int R = 4, RQ = 2;
+    extern __shared__ __align__(128) unsigned char smem_raw[];
+    const int64_t itile = blockIdx.x / p.split;
+    const int sp = (int)(blockIdx.x % p.split);
+    const int64_t q0 = (int64_t)sp * p.pairs_per_split;             // a multiple of PAIRS
+    const int64_t npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
+    const int64_t row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
+    const int nt = (int)((npc + Cfg::PAIRS - 1) / Cfg::PAIRS);
+    const int last_np = (int)(npc - (int64_t)(nt > 0 ? nt - 1 : 0) * Cfg::PAIRS);
+    JRing<kStages> ring;
+    ring.init(smem_raw, Cfg::TILE_FLOATS, p.J + q0 * RS, nt, kConsumerWarps, (uint32_t)last_np * RS * 4u);
+
+    const int ct = threadIdx.x;
+    const float negc = p.negc;
+    const float2 negc2 = dup2(negc);
+    double Mr[R], s64[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) { Mr[r] = (double)kLseSentinel; s64[r] = 0.0; }
+    float2 X2[RQ][D], NM2[RQ], S32[RQ];
+#pragma unroll
+    for (int q = 0; q < RQ; ++q) S32[q] = make_float2(0.f, 0.f);
+    const int64_t tile0 = q0 / Cfg::PAIRS;
+    for (int k = 0; k < nt; ++k) {
+        const float4 cen = __ldg(p.centers + tile0 + k);
+        const bool loc = cen.w >= 0.0f;
+        const float cc[3] = {cen.x, cen.y, cen.z};
+        // this tile's frame: 2 x'' (or raw x), m' = fl32(M - o), M moved to m' + o
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+            double o = 0.0;
+            float xv[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const float xd = i < p.M ? __ldg(p.x + i * D + d) : 0.0f;
+                if (loc) {
+                    const float h = p.s * (xd - cc[d]);
+                    xv[d] = 2.0f * h;
+                    const double hd = 0.5 * (double)xv[d];           // = h exactly
+                    o = fma(-hd, hd, o);
+                } else {
+                    xv[d] = xd;
+                }
+            }
+            const float mp = (float)(Mr[r] - o);
+            const double Mn = (double)mp + o;
+            if (s64[r] != 0.0) {
+                const double dl = (Mr[r] - Mn) * 0.69314718055994530942;     // ln of 2^(M_old - M_new)
+                s64[r] *= fabs(dl) < 1e-4 ? 1.0 + dl * (1.0 + dl * (0.5 + dl * (1.0 / 6.0))) : exp(dl);
+            }
+            Mr[r] = Mn;
+#pragma unroll
+            for (int d = 0; d < D; ++d) { if (r & 1) X2[r >> 1][d].y = xv[d]; else X2[r >> 1][d].x = xv[d]; }
+            if (r & 1) NM2[r >> 1].y = -mp; else NM2[r >> 1].x = -mp;
+        }
+        const float *tile = ring.acquire(k);
+        const int nsc = (k == nt - 1 ? last_np : Cfg::PAIRS) / kSub;
+        for (int sc = 0; sc < nsc; ++sc) {
+            const float *base = tile + sc * kSub * RS;
+            float2 cs[RQ];
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) cs[q] = make_float2(0.f, 0.f);
+            if (loc) {
+#pragma unroll
+                for (int pq = 0; pq < kSub; ++pq) {
+                    float f[RS];
+#pragma unroll
+                    for (int u = 0; u < RS / 4; ++u) {
+                        const float4 v = lds128(base + pq * RS + 4 * u);
+                        f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int q = 0; q < RQ; ++q) {
+                            float2 t = add2(NM2[q], dup2(f[2 * D + h]));                 // w - m'
+#pragma unroll
+                            for (int d = 0; d < D; ++d) t = fma2(X2[q][d], dup2(f[2 * d + h]), t);   // + 2x''.y''
+                            float2 e;
+                            if (GENRED_LSE_POLY && q == RQ - 1 && h == 0 && (pq & 1) == 0) {
+                                // 1/8 of the exponentials on the FP32 pipe (as the Sum, sum_body.cuh);
+                                // t clamped to [-126, 64]: 2^64 still trips the kSumMax check
+                                const float2 tc = make_float2(fminf(fmaxf(t.x, -126.0f), 64.0f),
+                                                              fminf(fmaxf(t.y, -126.0f), 64.0f));
+                                e = ex2_poly2(tc);
+                            } else {
+                                e = make_float2(ex2(t.x), ex2(t.y));
+                            }
+                            cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
+                        }
+                    }
+                }
+            } else {
+#pragma unroll
+                for (int pq = 0; pq < kSub; ++pq) {
+                    float f[RS];
+#pragma unroll
+                    for (int u = 0; u < RS / 4; ++u) {
+                        const float4 v = lds128(base + pq * RS + 4 * u);
+                        f[4 * u + 0] = v.x; f[4 * u + 1] = v.y; f[4 * u + 2] = v.z; f[4 * u + 3] = v.w;
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h) {
+#pragma unroll
+                        for (int q = 0; q < RQ; ++q) {
+                            float2 dd = add2(X2[q][0], dup2(f[h]));                       // x - y (raw, R6)
+                            float2 q2 = mul2(dd, dd);
+#pragma unroll
+                            for (int d = 1; d < D; ++d) {
+                                dd = add2(X2[q][d], dup2(f[2 * d + h]));
+                                q2 = fma2(dd, dd, q2);
+                            }
+                            const float2 hm = HZ ? NM2[q] : add2(NM2[q], dup2(f[2 * D + h]));
+                            const float2 t = fma2(q2, negc2, hm);
+                            const float2 e = make_float2(ex2(t.x), ex2(t.y));
+                            cs[q] = HZ ? add2(cs[q], e) : fma2(e, dup2(f[2 * D + 2 + h]), cs[q]);
+                        }
+                    }
+                }
+            }
+#pragma unroll
+            for (int q = 0; q < RQ; ++q) {
+                if (!(fmaxf(cs[q].x, cs[q].y) <= kSumMax)) {           // rare: per-row rescale
+#pragma unroll
+                    for (int l = 0; l < 2; ++l) {
+                        const int r = 2 * q + l;
+                        const float c = l ? cs[q].y : cs[q].x;
+                        if (c <= kSumMax) {
+                            if (l) S32[q].y += c; else S32[q].x += c;
+                            continue;
+                        }
+                        float xrow[D];
+#pragma unroll
+                        for (int d = 0; d < D; ++d) xrow[d] = l ? X2[q][d].y : X2[q][d].x;
+                        const float m_old = -(l ? NM2[q].y : NM2[q].x);
+                        const LseRescale rs = lse_local_rescale<D, HZ, RS>(base, xrow, loc, negc, m_old, s64[r],
+                                                                           l ? S32[q].y : S32[q].x);
+                        // M = m' + o with this tile's o = -|x''|^2 (recomputed bitwise as at the
+                        // tile start; 0 for a direct tile)
+                        double o = 0.0;
+                        if (loc) {
+#pragma unroll
+                            for (int d = 0; d < D; ++d) {
+                                const double hd = 0.5 * (double)xrow[d];
+                                o = fma(-hd, hd, o);
+                            }
+                        }
+                        Mr[r] = (double)rs.m + o;
+                        s64[r] = rs.s64;
+                        if (l) { S32[q].y = rs.c1; NM2[q].y = -rs.m; } else { S32[q].x = rs.c1; NM2[q].x = -rs.m; }
+                    }
+                } else {
+                    S32[q] = add2(S32[q], cs[q]);
+                }
+            }
+            if ((sc + 1) % kPromote == 0) {
+#pragma unroll
+                for (int q = 0; q < RQ; ++q) {
+                    s64[2 * q] += (double)S32[q].x;
+                    s64[2 * q + 1] += (double)S32[q].y;
+                    S32[q] = make_float2(0.f, 0.f);
+                }
+            }
+        }
+        ring.release(k);
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {                 // (a partial last tile's tail promotion)
+            s64[2 * q] += (double)S32[q].x;
+            s64[2 * q + 1] += (double)S32[q].y;
+            S32[q] = make_float2(0.f, 0.f);
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= p.M) continue;
+        const double stot = s64[r];
+        if (p.split > 1) {
+            p.state[((int64_t)sp * p.M + i) * 2 + 0] = Mr[r];
+            p.state[((int64_t)sp * p.M + i) * 2 + 1] = stot;
+            continue;
+        }
+        const double a = (stot > 0.0) ? 0.69314718055994530942 * (Mr[r] + log2(stot)) : -INFINITY;
+        if (p.out) {
+            if (p.out_f64) ((double *)p.out)[i] = a;
+            else ((float *)p.out)[i] = (float)a;
+        }
+        if (p.state) {
+            p.state[2 * i + 0] = Mr[r];
+            p.state[2 * i + 1] = stot;
+        }
+    }
+}
+
 // Small-M mode (north star (a), the warp-shuffle finish; see sum_smm.cu): a CTA owns R rows, its
 // 256 threads take the tile's record pairs t, t + 256, ..., each keeping its own streaming
 // (m, s) per row with the same lazy rescale (one pair per check), and the CTA merges the 256
@@ -533,6 +799,26 @@ static cudaError_t run_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
     return cudaGetLastError();
 }
 
+template <int D, bool HZ>
+static cudaError_t run_lse_local(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    using Cfg = LseLocCfg<D, HZ>;
+    auto kern = lse_local_kernel<D, HZ>;
+    {
+        const cudaError_t e = smem_opt_in((const void *)kern, Cfg::SMEM);
+        if (e != cudaSuccess) return e;
+    }
+    LseParams p;
+    p.x = a.x; p.J = a.J; p.M = a.M; p.split = a.split; p.pairs_per_split = a.pairs_per_split;
+    p.npv = a.npv; p.negc = a.negc; p.out = a.out; p.out_f64 = a.out_f64; p.state = a.state;
+    p.units = nullptr; p.centers = a.centers; p.s = a.s;
+    const int64_t rows = (int64_t)kConsumerWarps * 32 * 4;
+    const int64_t grid = ((a.M + rows - 1) / rows) * a.split;
+    *ctas = (int)grid;
+    if (grid == 0) return cudaSuccess;
+    kern<<<(unsigned)grid, kThreads, Cfg::SMEM, st>>>(p);
+    return cudaGetLastError();
+}
+
 template <int D, int R>
 static int occ_lse(bool hz) {
     using Cfg = LseCfg<D, false>;
@@ -564,6 +850,15 @@ static cudaError_t run_lse_r(const LseLaunch &a, cudaStream_t st, int *ctas) {
 }
 
 cudaError_t launch_lse(const LseLaunch &a, cudaStream_t st, int *ctas) {
+    if (a.centers) {                                   // tile-centred form (R = 4, D <= 3)
+        if (a.R != 4) return cudaErrorInvalidValue;
+        switch (a.D) {
+            case 1: return a.h_zero ? run_lse_local<1, true>(a, st, ctas) : run_lse_local<1, false>(a, st, ctas);
+            case 2: return a.h_zero ? run_lse_local<2, true>(a, st, ctas) : run_lse_local<2, false>(a, st, ctas);
+            case 3: return a.h_zero ? run_lse_local<3, true>(a, st, ctas) : run_lse_local<3, false>(a, st, ctas);
+        }
+        return cudaErrorInvalidValue;
+    }
     switch (a.D) {
         case 1: return run_lse_r<1>(a, st, ctas);
         case 2: return run_lse_r<2>(a, st, ctas);

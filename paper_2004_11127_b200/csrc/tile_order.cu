@@ -85,14 +85,20 @@ __global__ void __launch_bounds__(256) hilbert_keys_kernel(const float *__restri
 }
 
 // One CTA per 512-j tile of the curve order: stage the tile's y (and b) through the permutation,
-// reduce its box, decide its layout, build its 256 record pairs (PACK_GAUSS_AUTO layout:
-// [2D coordinates][w pair][2E signal], padded to RS floats).  Padding records (j >= N) are zero
-// (y = 0, w = 0, b = 0) in both layouts.
+// reduce its box, decide its layout, build its 256 record pairs, padded to RS floats:
+//   Sum (lse = 0; the PACK_GAUSS_AUTO layout): [2D coordinates][w pair][2E signal]; padding
+//     records (j >= N) are zero (y = 0, w = 0, b = 0) in both layouts;
+//   LSE (lse = 1, E = 1, b = h or nullptr): [2D coordinates][w pair][c pair], centred:
+//     y'', w = fl32(h' - |y''|^2), c = 2^((h' - |y''|^2) - w) (h' = log2(e) h; the fp32 split of
+//     R6c applied to the whole j term); direct: -y, h'_hi, c = 2^(h' - h'_hi).  Padding: w = -inf
+//     (centred) or -y = -inf (direct), c = 0.
+// A tile is centred when its radius^2 in s units is at most r2max (and finite).
 __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict__ y, const float *__restrict__ b,
                                                          int64_t N, int D, int E, float s,
                                                          const uint32_t *__restrict__ perm, int64_t ntiles, int RS,
                                                          float *__restrict__ J, float4 *__restrict__ centers,
-                                                         const uint32_t *__restrict__ geo_enc) {
+                                                         const uint32_t *__restrict__ geo_enc, int lse,
+                                                         double hscale, float r2max) {
     extern __shared__ float4 plk_smem4[];
     float *sm = reinterpret_cast<float *>(plk_smem4);
     float *ys = sm;                                   // [512][D]
@@ -103,14 +109,15 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     // the global box (as pack_kernel): when it admits the expanded form everywhere, every tile
     // takes the global centre (the pair loop then runs sum_body's expanded form)
-    const Geo geo = geo_decode(geo_enc, D, s);
+    Geo geo = geo_decode(geo_enc, D, s);
+    if (lse) geo.expanded = false;                    // (no global form for the LSE, R18b)
     for (int64_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x) {
         const int64_t j0 = blk * kTileJ;
         const int nj = (int)max((int64_t)0, min((int64_t)kTileJ, N - j0));
         for (int k = t; k < nj; k += 256) {
             const int64_t j = (int64_t)__ldg(perm + j0 + k);
             for (int d = 0; d < D; ++d) ys[k * D + d] = __ldg(y + j * D + d);
-            for (int e = 0; e < E; ++e) bs[k * E + e] = b ? __ldg(b + j * E + e) : 1.0f;
+            for (int e = 0; e < E; ++e) bs[k * E + e] = b ? __ldg(b + j * E + e) : (lse ? 0.0f : 1.0f);
         }
         __syncthreads();
         // tile box
@@ -156,7 +163,7 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
             float m = wr2[0];
             for (int w = 1; w < 8; ++w) m = fmaxf(m, wr2[w]);
             m *= 1.0001f;
-            cen[3] = (geo.expanded || (isfinite(m) && m <= kExpandedR2Max)) ? m : -1.0f;
+            cen[3] = (geo.expanded || (isfinite(m) && m <= r2max)) ? m : -1.0f;
             centers[blk] = make_float4(cen[0], cen[1], cen[2], cen[3]);
         }
         __syncthreads();
@@ -166,6 +173,26 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
         for (int h = 0; h < 2; ++h) {
             const int jj = 2 * t + h;
             const bool valid = jj < nj;
+            if (lse) {
+                const double hp = valid ? hscale * (double)bs[jj] : 0.0;    // h' = log2(e) h
+                double w = 0.0;
+                for (int d = 0; d < D; ++d) {
+                    const float v = valid ? ys[jj * D + d] : 0.0f;
+                    float r;
+                    if (local) {
+                        r = valid ? s * (v - cen[d]) : 0.0f;
+                        w += (double)r * (double)r;
+                    } else {
+                        r = valid ? -v : -INFINITY;
+                    }
+                    rec[2 * d + h] = r;
+                }
+                const double tj = hp - (local ? w : 0.0);                    // the j term, log2 units
+                const float hi = valid ? (float)tj : -INFINITY;
+                rec[2 * D + h] = hi;
+                if (RS >= 2 * D + 4) rec[2 * D + 2 + h] = valid ? (float)exp2(tj - (double)hi) : 0.0f;
+                continue;
+            }
             double w = 0.0;
             for (int d = 0; d < D; ++d) {
                 const float v = valid ? ys[jj * D + d] : 0.0f;
@@ -199,7 +226,8 @@ size_t tile_order_temp_bytes(int64_t N) {
 cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, int E, float s,
                               const uint32_t *geo, uint32_t *keys, uint32_t *idx, uint32_t *keys_s,
                               uint32_t *perm, void *temp, size_t temp_bytes, int64_t ntiles, float *J,
-                              float4 *centers, cudaStream_t st, int *kernels) {
+                              float4 *centers, cudaStream_t st, int *kernels, int lse, int RS_lse,
+                              double hscale, float r2max) {
     int64_t blocks = (N + 255) / 256;
     if (blocks > 148 * 16) blocks = 148 * 16;
     if (blocks < 1) blocks = 1;
@@ -211,7 +239,7 @@ cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, 
     e = cub::DeviceRadixSort::SortPairs(temp, tb, (const uint32_t *)keys, keys_s, (const uint32_t *)idx, perm,
                                         (int)N, 0, end_bit, st);
     if (e != cudaSuccess) return e;
-    const int RS = pack_record_stride(PACK_GAUSS_AUTO, D, E);
+    const int RS = lse ? RS_lse : pack_record_stride(PACK_GAUSS_AUTO, D, E);
     const int smem = (kTileJ * (D + E) + 256 * RS) * 4;
     if (smem > 48 * 1024) {
         e = smem_opt_in((const void *)pack_local_kernel, 96 * 1024);
@@ -219,7 +247,8 @@ cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, 
     }
     int64_t pb = ntiles < 148 * 8 ? ntiles : 148 * 8;
     if (pb < 1) pb = 1;
-    pack_local_kernel<<<(unsigned)pb, 256, smem, st>>>(y, b, N, D, E, s, perm, ntiles, RS, J, centers, geo);
+    pack_local_kernel<<<(unsigned)pb, 256, smem, st>>>(y, b, N, D, E, s, perm, ntiles, RS, J, centers, geo,
+                                                        lse, hscale, r2max);
     // keys + pack + the radix sort's launches (onesweep: histogram, exclusive sum, one pass per
     // 8 key bits -- 4 for the 30- or 32-bit keys; counted from the ncu launch list)
     *kernels = 2 + 2 + 4;

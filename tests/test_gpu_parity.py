@@ -522,6 +522,83 @@ def test_tile_centred_splits_and_ishards(G, monkeypatch, split):
         np.testing.assert_array_equal(part, full[lo:hi])
 
 
+def _lse_local_case(case):
+    rng = np.random.default_rng(sum(map(ord, case)))
+    if case == "u3_hz":
+        return synth.uniform3(4000, 1), synth.uniform3(400_000, 2), None, 0.05, "mixed"
+    if case == "u3_h":
+        return (synth.uniform3(4000, 1), synth.uniform3(400_000, 2),
+                rng.standard_normal(400_000).astype(np.float32), 0.05, "mixed")
+    if case == "u3_h3_ragged":
+        return (synth.uniform3(20000, 3), synth.uniform3(30001, 4), (3 * rng.standard_normal(30001)).astype(np.float32),
+                0.2, "mixed")
+    if case == "gmm":
+        return synth.gmm3(5000, 5), synth.gmm3(100_000, 6), None, 0.01, "mixed"
+    if case == "far_offset":
+        return ((synth.uniform3(5000, 7) + 1000).astype(np.float32),
+                (synth.uniform3(60000, 8) + 1000).astype(np.float32), None, 0.1, "mixed")
+    if case == "D2":
+        return (rng.random((3000, 2)).astype(np.float32), rng.random((100_000, 2)).astype(np.float32), None,
+                0.01, "mixed")
+    if case == "D1_h":
+        return (rng.random((3000, 1)).astype(np.float32), rng.random((70000, 1)).astype(np.float32),
+                rng.standard_normal(70000).astype(np.float32), 1e-4, "all")
+    if case == "dominant_far_h":        # a far point with a large h dominates some rows
+        y = synth.uniform3(50000, 9)
+        h = np.zeros(50000, np.float32)
+        h[::997] = 40.0
+        return synth.uniform3(4000, 10), y, h, 0.02, "any"
+    raise ValueError(case)
+
+
+@pytest.mark.parametrize("case", ["u3_hz", "u3_h", "u3_h3_ragged", "gmm", "far_offset", "D2", "D1_h",
+                                  "dominant_far_h"])
+def test_lse_tile_centred_form(G, monkeypatch, case):
+    """LSE in the tile-centred form (reading R18j; radius bound kLseLocalR2Max): every row
+    against the oracle at the plain 1e-6 absolute bar (fp64 output), bitwise reproducible."""
+    option(G, monkeypatch, "local_form", 2)
+    x, y, h, eps, expect = _lse_local_case(case)
+    hd = dev(h) if h is not None else None
+    a = G.eval("sqdist", "lse", dev(x), dev(y), hd, scale=eps, out_dtype="float64")
+    plan = G.last_plan()
+    loc, tot = G.last_tiles()
+    assert plan["path"] == 3 and tot == (len(y) + 511) // 512, (plan, loc, tot)
+    if expect == "all":
+        assert loc == tot
+    elif expect == "mixed":
+        assert 0 < loc < tot, (loc, tot)
+    o, _ = oracle.lse(x, y, h, eps=eps)
+    assert_lse_parity(host(a), o, what=f"lse tile-centred {case}")
+    a2 = G.eval("sqdist", "lse", dev(x), dev(y), hd, scale=eps, out_dtype="float64")
+    np.testing.assert_array_equal(host(a2), host(a))
+
+
+@pytest.mark.parametrize("split", [1, 3, 40])
+def test_lse_tile_centred_splits_state_and_ishards(G, monkeypatch, split):
+    """Tile-centred LSE with forced j-splits (finalize merge of (M, S) states), the state output
+    combined across emulated j-shards (genred_combine_lse), and i-shards bitwise equal."""
+    option(G, monkeypatch, "local_form", 2)
+    M, N = 6000, 60000
+    x = synth.uniform3(M, 31); y = synth.uniform3(N, 32)
+    h = np.random.default_rng(33).standard_normal(N).astype(np.float32)
+    full = host(G.eval("sqdist", "lse", dev(x), dev(y), dev(h), scale=0.02, out_dtype="float64", split_j=split))
+    assert G.last_plan()["path"] == 3
+    o, _ = oracle.lse(x, y, h, eps=0.02)
+    assert_lse_parity(full, o, what=f"lse tile-centred split {split}")
+    for lo, hi in ((0, 1024), (1024, 3072), (3072, 6000)):
+        part = host(G.eval("sqdist", "lse", dev(x[lo:hi]), dev(y), dev(h), scale=0.02, out_dtype="float64",
+                           split_j=split))
+        np.testing.assert_array_equal(part, full[lo:hi])
+    states = []
+    for lo, hi in ((0, 30000), (30000, 60000)):                 # two j-shards, combined
+        st = torch.empty((M, 2), dtype=torch.float64, device="cuda")
+        G.eval("sqdist", "lse", dev(x), dev(y[lo:hi]), dev(h[lo:hi]), scale=0.02, out_dtype="float64",
+               split_j=split, lse_state=st)
+        states.append(st)
+    comb = G.combine_lse(torch.stack(states), out_dtype="float64")
+    assert_lse_parity(host(comb), o, what=f"lse tile-centred j-shard combine split {split}")
+
+
 @pytest.mark.parametrize("formula", ["gauss", "gauss_gradx", "gauss_sum_gradx", "sqdist"])
 @pytest.mark.parametrize("M,N,D", [(1, 200_000, 3), (5, 70_001, 2), (37, 150_000, 4), (64, 100_000, 1),
                                    (300, 400_000, 3)])

@@ -52,6 +52,60 @@ def parity():
     G.set_option("local_form", 1)
 
 
+def lse_parity():
+    rng = np.random.default_rng(7)
+    cases = [
+        ("lse u3 e0.05", synth.uniform3(4000, 1), synth.uniform3(400000, 2), None, 0.05),
+        ("lse u3 e0.05 h", synth.uniform3(4000, 1), synth.uniform3(400000, 2),
+         rng.standard_normal(400000).astype(np.float32), 0.05),
+        ("lse u3 e0.2 h3", synth.uniform3(20000, 3), synth.uniform3(30001, 4),
+         (3 * rng.standard_normal(30001)).astype(np.float32), 0.2),
+        ("lse gmm e0.01", synth.gmm3(5000, 5), synth.gmm3(100000, 6), None, 0.01),
+        ("lse far e0.1", (synth.uniform3(5000, 7) + 1000).astype(np.float32),
+         (synth.uniform3(60000, 8) + 1000).astype(np.float32), None, 0.1),
+        ("lse D2 e0.01", rng.random((3000, 2)).astype(np.float32), rng.random((100000, 2)).astype(np.float32),
+         None, 0.01),
+        ("lse D1 e1e-4", rng.random((3000, 1)).astype(np.float32), rng.random((70000, 1)).astype(np.float32),
+         rng.standard_normal(70000).astype(np.float32), 1e-4),
+    ]
+    G.set_option("local_form", 2)
+    for name, x, y, h, eps in cases:
+        a = G.eval("sqdist", "lse", dev(x), dev(y), dev(h) if h is not None else None, scale=eps,
+                   out_dtype="float64")
+        plan = G.last_plan()
+        lt = G.last_tiles()
+        o, _ = oracle.lse(x, y, h, eps=eps)
+        err = np.abs(a.cpu().numpy() - o)
+        print(f"{name:16s} M={len(x):6d} N={len(y):7d} path={plan['path']} split={plan['split_j']} "
+              f"tiles={lt} maxabs={err.max():.3e} mean={err.mean():.2e}", flush=True)
+    G.set_option("local_form", 1)
+
+
+def lse_timing():
+    for (M, N, eps, hz) in [(1_000_000, 1_000_000, 0.05, True), (1_000_000, 1_000_000, 0.05, False)]:
+        x = dev(synth.uniform3(M, 1)); y = dev(synth.uniform3(N, 2))
+        h = None if hz else dev(np.random.default_rng(4).standard_normal(N).astype(np.float32))
+        for lf in (0, 1):
+            G.set_option("local_form", lf)
+            for _ in range(2):
+                G.eval("sqdist", "lse", x, y, h, scale=eps, out_dtype="float64")
+            torch.cuda.synchronize()
+            G.profile(True)
+            t0 = torch.cuda.Event(enable_timing=True); t1 = torch.cuda.Event(enable_timing=True)
+            t0.record()
+            for _ in range(3):
+                G.eval("sqdist", "lse", x, y, h, scale=eps, out_dtype="float64")
+            t1.record(); torch.cuda.synchronize()
+            ms = G.profile_read()
+            G.profile(False)
+            plan = G.last_plan()
+            lt = G.last_tiles()
+            print(f"LSE M={M} N={N} eps={eps} h={'0' if hz else 'N(0,1)'} local_form={lf} path={plan['path']} "
+                  f"tiles={lt} split={plan['split_j']} kernel {min(ms):.2f} ms step {t0.elapsed_time(t1) / 3:.2f} ms "
+                  f"pairs/clk/SM {M * N / (min(ms) * 1e-3) / (148 * 1.965e9):.2f}", flush=True)
+    G.set_option("local_form", 1)
+
+
 def timing():
     for (M, N, sig) in [(2_000_000, 2_000_000, 0.05), (1_000_000, 1_000_000, 0.05), (1_000_000, 1_000_000, 0.1)]:
         x = dev(synth.uniform3(M, 1)); y = dev(synth.uniform3(N, 2)); b = dev(synth.signal(N, 3))
@@ -83,3 +137,7 @@ if __name__ == "__main__":
         parity()
     if "time" in what:
         timing()
+    if "lse" in what:
+        lse_parity()
+    if "lsetime" in what:
+        lse_timing()
