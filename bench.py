@@ -81,7 +81,9 @@ def workload(cid: int) -> dict:
         return dict(cfg=c, formula="gauss", reduction="sum", fp32=5, mufu=7 / 8, out_dtype="float64")
     if cid == 8:   # j-sharded LSE: as C3 per rank, (m, s) states all-gathered and combined
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
-    if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8
+    if cid == 3:   # raw diff (3) + |d|^2 (3) + t = fma(-c,|d|^2,-m) (1) + s += e (1) = 8; at C3's
+        #            size the tile-centred form runs (R18j): w - m' (1) + 2x''.y'' (3) + s += e (1)
+        #            = 5 (set from the plan below); the peak is the MUFU's either way
         return dict(cfg=c, formula="sqdist", reduction="lse", fp32=8, mufu=1, out_dtype="float64")
     if cid == 6:   # Cedge: N tiny -> 12 B of x read + 4 B of a written per row (HBM-bound)
         return dict(cfg=c, formula="gauss", reduction="sum", fp32=None, mufu=None, out_dtype="float32",
@@ -658,13 +660,18 @@ def main() -> None:
             w = dict(w, fp32=8, mufu=1)                      # (no polynomial share in the direct form)
         peak = alu_peak_pairs(w["fp32"], w["mufu"], mhz_max)
         basis_extra = ""
-        if w["formula"] == "gauss" and plan.get("path") == 3:
-            # tile-centred form (R18j): centred tiles run the expanded mix, the others the direct
-            # one; the ceiling is the pair-weighted harmonic mix of the two
+        if w["formula"] in ("gauss", "sqdist") and plan.get("path") == 3:
+            # tile-centred form (R18j): centred tiles run the expanded mix (Sum: 4 FP32 lane-ops
+            # + 1 of the polynomial exp share, 7/8 MUFU; LSE: FADD + 3 FFMA + 1 accumulate, 1
+            # MUFU), the others the direct one (8 FP32 + 1 MUFU); the ceiling is the
+            # pair-weighted harmonic mix of the two
             f_loc = tiles[0] / max(tiles[1], 1)
+            loc_mix = (5, 7 / 8) if w["formula"] == "gauss" else (5, 1)
+            p_loc = alu_peak_pairs(*loc_mix, mhz_max)
             p_dir = alu_peak_pairs(8, 1, mhz_max)
-            peak = 1.0 / (f_loc / peak + (1.0 - f_loc) / p_dir)
-            basis_extra = (f"; tile-centred form: {tiles[0]} of {tiles[1]} tiles centred (expanded mix), "
+            peak = 1.0 / (f_loc / p_loc + (1.0 - f_loc) / p_dir)
+            w = dict(w, fp32=loc_mix[0], mufu=loc_mix[1])
+            basis_extra = (f"; tile-centred form: {tiles[0]} of {tiles[1]} tiles centred (this mix), "
                            f"the rest direct (16/1 MUFU, 128/8 FP32), harmonic mix")
         achieved = Ml * N / (kmean * 1e-3)
         roofline = {"bound": "alu", "achieved": achieved / 1e12, "peak": peak / 1e12, "unit": "Tpair/s",

@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--K", type=int, default=10)
     ap.add_argument("--D", type=int, default=3)
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--scale", type=float, default=None, help="sigma (Gaussian) / eps (LSE)")
     a = ap.parse_args()
     if a.D == 784:
         x = torch.from_numpy(synth.mnist784(a.M, 1)).cuda()
@@ -36,15 +37,15 @@ def main():
     h = torch.from_numpy(np.random.default_rng(4).standard_normal(a.N).astype(np.float32)).cuda()
     for _ in range(a.reps):
         if a.what == "gauss":
-            genred.eval("gauss", "sum", x, y, b, scale=0.5)
+            genred.eval("gauss", "sum", x, y, b, scale=a.scale or 0.5)
         elif a.what == "gradx":
             genred.eval("gauss_gradx", "sum", x, y, b, scale=0.5)
         elif a.what == "fused":
             genred.eval("gauss_sum_gradx", "sum", x, y, b, scale=0.5)
         elif a.what == "lse":
-            genred.eval("sqdist", "lse", x, y, None, scale=0.05, out_dtype="float64")
+            genred.eval("sqdist", "lse", x, y, None, scale=a.scale or 0.05, out_dtype="float64")
         elif a.what == "lse_h":
-            genred.eval("sqdist", "lse", x, y, h, scale=0.05, out_dtype="float64")
+            genred.eval("sqdist", "lse", x, y, h, scale=a.scale or 0.05, out_dtype="float64")
         else:
             genred.eval("sqdist", "argkmin", x, y, K=a.K)
     torch.cuda.synchronize()
