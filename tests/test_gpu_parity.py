@@ -567,8 +567,14 @@ def test_lse_tile_centred_form(G, monkeypatch, case):
         assert loc == tot
     elif expect == "mixed":
         assert 0 < loc < tot, (loc, tot)
-    o, _ = oracle.lse(x, y, h, eps=eps)
-    assert_lse_parity(host(a), o, what=f"lse tile-centred {case}")
+    if case == "dominant_far_h":
+        # rows whose dominant term is a far point lifted by h = 40: exponents ~190 in magnitude,
+        # rounded in fp32 by any form -- the R6b conditioning floor (as the other hard-input tests)
+        o, _, cond = oracle.lse(x, y, h, eps=eps, cond=True)
+        assert_lse_parity(host(a), o, rel=True, cond=cond, D=3, what=f"lse tile-centred {case}")
+    else:
+        o, _ = oracle.lse(x, y, h, eps=eps)
+        assert_lse_parity(host(a), o, what=f"lse tile-centred {case}")
     a2 = G.eval("sqdist", "lse", dev(x), dev(y), hd, scale=eps, out_dtype="float64")
     np.testing.assert_array_equal(host(a2), host(a))
 
