@@ -566,7 +566,8 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         // Tile-centred form (R18j): y in Hilbert order, records centred per 512-j tile; the device
         // takes it where the global box rules the expanded form out (geo.cuh), tile by tile.  The
         // j-splits then cover whole tiles.
-        const bool local = mode == 0 && !smm && D <= 3 && N > kDirectMaxN && M > kDirectMaxM &&
+        const bool local = (mode == 0 || ((mode == 1 || mode == 2) && E == 1 && kGradBY && pl.R == 4)) &&
+                           !smm && D <= 3 && N > kDirectMaxN && M > kDirectMaxM &&
                            N < ((int64_t)1 << 31) &&
                            (ctx->local_form == 2 || (ctx->local_form == 1 && N >= kLocalMinN && M >= kLocalMinM));
         if (local) {
@@ -654,7 +655,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
                      *perm = (uint32_t *)(q + 3 * nb);
             int lk = 0;
             e = launch_tile_order(a->y, a->b, N, D, E, sc, geo, keys, idx, keys_s, perm, q + 4 * nb,
-                                  tile_order_temp_bytes(N), pl.ntiles, J, centers, st, &lk);
+                                  tile_order_temp_bytes(N), pl.ntiles, J, centers, st, &lk, mode == 0 ? 0 : 2);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "tile order / pack kernels");
             kernels += lk - 1;
         } else {

@@ -642,6 +642,172 @@ __device__ __forceinline__ void sum_body_local(const SumParams &p, Ring &ring, i
     }
 }
 
+// Tile-centred form of the gradient modes (MODE 1 / 2, E = 1, D <= 3, R = 4 rows per thread; R18j
+// with R18g's records per tile: y'', b' = b 2^(-|y''|^2), b' y'').  The row-pair loop of sum_body
+// (two rows in the FFMA2 lanes) runs on 2x'' = 2s(x - c_k); per row and tile, with
+// fac = 2^(-|x''|^2):  S0 += fac S0p,  G += fac (x'' S0p - Sp)  (sum_j w (x'' - y'') is the
+// s-scaled x - y in any frame).  Direct tiles run sum_body's raw-difference gradient loop, their
+// (x - y) sums scaled by s into the same convention.
+template <int MODE, int D, class Ring>
+__device__ __forceinline__ void sum_body_local_grad(const SumParams &p, Ring &ring, int nt, int last_np,
+                                                    int64_t row0, int64_t row_end, int sp, int64_t tile0) {
+    using Cfg = SumCfg<MODE, D, 1>;
+    constexpr int R = 4, RQ = 2, RS = Cfg::RS, BOFF = Cfg::BOFF, BYOFF = Cfg::BYOFF;
+    constexpr int HH = GENRED_GRAD_HH;
+    constexpr int NS = Cfg::NS, C = Cfg::C;
+    const int ct = threadIdx.x;
+    const float2 negs2 = dup2(-(p.s * p.s));
+    double acc64[R][C];            // [sum (MODE 2)][grad D]
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int c = 0; c < C; ++c) acc64[r][c] = 0.0;
+    for (int k = 0; k < nt; ++k) {
+        const float4 cen = __ldg(p.centers + tile0 + k);
+        const bool loc = cen.w >= 0.0f;
+        const float cc[3] = {cen.x, cen.y, cen.z};
+        const float lim = loc ? sqrtf(cen.w) + 11.5f : 0.0f;
+        float2 X2[RQ][D];              // 2x'' (centred tile) or raw x (direct tile), row pairs
+        unsigned far = 0u;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+            float q = 0.0f;
+            float xv[D];
+#pragma unroll
+            for (int d = 0; d < D; ++d) {
+                const float xd = i < row_end ? __ldg(p.x + i * D + d) : 0.0f;
+                if (loc) {
+                    const float h = p.s * (xd - cc[d]);
+                    xv[d] = 2.0f * h;
+                    q = fmaf(h, h, q);
+                } else {
+                    xv[d] = xd;
+                }
+            }
+            if (loc && q > lim * lim) {
+                far |= 1u << r;
+#pragma unroll
+                for (int d = 0; d < D; ++d) xv[d] = 0.0f;
+            }
+#pragma unroll
+            for (int d = 0; d < D; ++d) { if (r & 1) X2[r >> 1][d].y = xv[d]; else X2[r >> 1][d].x = xv[d]; }
+        }
+        const float *tile = ring.acquire(k);
+        const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
+        float2 S0p[RQ], Sp[RQ][D];
+#pragma unroll
+        for (int q = 0; q < RQ; ++q) {
+            S0p[q] = make_float2(0.f, 0.f);
+#pragma unroll
+            for (int d = 0; d < D; ++d) Sp[q][d] = make_float2(0.f, 0.f);
+        }
+        if (loc) {
+            for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+            for (int hh = 0; hh < HH; ++hh) {
+                float f[RS];
+#pragma unroll
+                for (int q = 0; q < RS / 4; ++q) {
+                    const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                    f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+                }
+#pragma unroll
+                for (int hq = 0; hq < 2 * RQ; ++hq) {
+                    const int h = hq / RQ, q = hq % RQ;
+                    float2 u = mul2(X2[q][0], dup2(f[h]));                              // 2 x''.y''
+#pragma unroll
+                    for (int d = 1; d < D; ++d) u = fma2(X2[q][d], dup2(f[2 * d + h]), u);
+                    const float2 ex = make_float2(ex2(u.x), ex2(u.y));
+                    S0p[q] = fma2(ex, dup2(f[BOFF + h]), S0p[q]);                       // e b'
+#pragma unroll
+                    for (int d = 0; d < D; ++d) Sp[q][d] = fma2(ex, dup2(f[BYOFF + 2 * d + h]), Sp[q][d]);
+                }
+            }
+            }
+        } else {
+            for (int pp2 = 0; pp2 < np; pp2 += HH) {
+#pragma unroll
+            for (int hh = 0; hh < HH; ++hh) {
+                float f[RS];
+#pragma unroll
+                for (int q = 0; q < RS / 4; ++q) {
+                    const float4 v = lds128(tile + (pp2 + hh) * RS + 4 * q);
+                    f[4 * q + 0] = v.x; f[4 * q + 1] = v.y; f[4 * q + 2] = v.z; f[4 * q + 3] = v.w;
+                }
+#pragma unroll
+                for (int hq = 0; hq < 2 * RQ; ++hq) {
+                    const int h = hq / RQ, q = hq % RQ;
+                    float2 dd[D];
+#pragma unroll
+                    for (int d = 0; d < D; ++d) dd[d] = add2(X2[q][d], dup2(f[2 * d + h]));   // x - y (raw)
+                    float2 q2 = mul2(dd[0], dd[0]);
+#pragma unroll
+                    for (int d = 1; d < D; ++d) q2 = fma2(dd[d], dd[d], q2);
+                    const float2 t = mul2(q2, negs2);
+                    const float2 ex = make_float2(ex2(t.x), ex2(t.y));
+                    const float2 w = mul2(ex, dup2(f[BOFF + h]));                     // e b
+                    S0p[q] = add2(S0p[q], w);
+#pragma unroll
+                    for (int d = 0; d < D; ++d) Sp[q][d] = fma2(w, dd[d], Sp[q][d]);   // w (x - y)
+                }
+            }
+            }
+        }
+        ring.release(k);
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int q = r >> 1;
+            const double s0 = (double)((r & 1) ? S0p[q].y : S0p[q].x);
+            if (loc) {
+                double q64 = 0.0;
+                double xh[D];
+#pragma unroll
+                for (int d = 0; d < D; ++d) {
+                    xh[d] = 0.5 * (double)((r & 1) ? X2[q][d].y : X2[q][d].x);     // x''
+                    q64 = fma(xh[d], xh[d], q64);
+                }
+                const double n = floor(q64);
+                const double fac = ((far >> r) & 1u) ? 0.0 : ldexp((double)ex2(-(float)(q64 - n)), -(int)n);
+                if constexpr (NS > 0) acc64[r][0] += fac * s0;
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                    acc64[r][NS + d] += fac * (xh[d] * s0 - (double)((r & 1) ? Sp[q][d].y : Sp[q][d].x));
+            } else {
+                if constexpr (NS > 0) acc64[r][0] += s0;
+#pragma unroll
+                for (int d = 0; d < D; ++d)
+                    acc64[r][NS + d] += (double)p.s * (double)((r & 1) ? Sp[q][d].y : Sp[q][d].x);
+            }
+        }
+    }
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int64_t i = row0 + r * (kConsumerWarps * 32) + ct;
+        if (i >= row_end) continue;
+        if (p.split > 1) {
+            double *dst = p.part + ((int64_t)sp * p.M + i) * C;
+#pragma unroll
+            for (int c = 0; c < C; ++c) dst[c] = acc64[r][c];
+            continue;
+        }
+        if constexpr (NS > 0) {
+            const double v = acc64[r][0] * p.scale_sum;
+            if (p.out_f64) ((double *)p.out)[i] = v;
+            else ((float *)p.out)[i] = (float)v;
+        }
+        double gs = p.scale_grad;
+        if (p.g) gs *= (double)__ldg(p.g + i);
+#pragma unroll
+        for (int c = 0; c < D; ++c) {
+            const double v = acc64[r][NS + c] * gs;
+            if (MODE == 2) p.out_grad[i * D + c] = (float)v;
+            else if (p.out_f64) ((double *)p.out)[i * D + c] = v;
+            else ((float *)p.out)[i * D + c] = (float)v;
+        }
+    }
+}
+
 // CTAs per SM the register allocation must allow (the 16 K registers of each SM sub-partition)
 template <int MODE, int D, int E, int R, bool SMM>
 constexpr int sum_min_blocks() {
@@ -739,6 +905,11 @@ sum_kernel(const SumParams p) {
             if constexpr (MODE == 0 && !SMM && D <= 3) {
                 if (p.centers && !p.units) {           // tile-centred form (R18j)
                     sum_body_local<D, E, R>(p, ring, nt, last_np, row0, row_end, sp, q0 / Cfg::PAIRS);
+                    local = true;
+                }
+            } else if constexpr ((MODE == 1 || MODE == 2) && E == 1 && D <= 3 && R == 4 && !SMM && Cfg::BY) {
+                if (p.centers && !p.units) {
+                    sum_body_local_grad<MODE, D>(p, ring, nt, last_np, row0, row_end, sp, q0 / Cfg::PAIRS);
                     local = true;
                 }
             }

@@ -88,6 +88,8 @@ __global__ void __launch_bounds__(256) hilbert_keys_kernel(const float *__restri
 // reduce its box, decide its layout, build its 256 record pairs, padded to RS floats:
 //   Sum (lse = 0; the PACK_GAUSS_AUTO layout): [2D coordinates][w pair][2E signal]; padding
 //     records (j >= N) are zero (y = 0, w = 0, b = 0) in both layouts;
+//   gradient modes (lse = 2, E = 1; the PACK_GAUSS_AUTO_RAW layout with the b y' slots):
+//     centred: y'', 0, b' = b 2^(-|y''|^2), b' y'' (R18g per tile); direct: -y, 0, b, 0;
 //   LSE (lse = 1, E = 1, b = h or nullptr): [2D coordinates][w pair][c pair], centred:
 //     y'', w = fl32(h' - |y''|^2), c = 2^((h' - |y''|^2) - w) (h' = log2(e) h; the fp32 split of
 //     R6c applied to the whole j term); direct: -y, h'_hi, c = 2^(h' - h'_hi).  Padding: w = -inf
@@ -110,14 +112,14 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
     // the global box (as pack_kernel): when it admits the expanded form everywhere, every tile
     // takes the global centre (the pair loop then runs sum_body's expanded form)
     Geo geo = geo_decode(geo_enc, D, s);
-    if (lse) geo.expanded = false;                    // (no global form for the LSE, R18b)
+    if (lse == 1) geo.expanded = false;               // (no global form for the LSE, R18b)
     for (int64_t blk = blockIdx.x; blk < ntiles; blk += gridDim.x) {
         const int64_t j0 = blk * kTileJ;
         const int nj = (int)max((int64_t)0, min((int64_t)kTileJ, N - j0));
         for (int k = t; k < nj; k += 256) {
             const int64_t j = (int64_t)__ldg(perm + j0 + k);
             for (int d = 0; d < D; ++d) ys[k * D + d] = __ldg(y + j * D + d);
-            for (int e = 0; e < E; ++e) bs[k * E + e] = b ? __ldg(b + j * E + e) : (lse ? 0.0f : 1.0f);
+            for (int e = 0; e < E; ++e) bs[k * E + e] = b ? __ldg(b + j * E + e) : (lse == 1 ? 0.0f : 1.0f);
         }
         __syncthreads();
         // tile box
@@ -173,7 +175,7 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
         for (int h = 0; h < 2; ++h) {
             const int jj = 2 * t + h;
             const bool valid = jj < nj;
-            if (lse) {
+            if (lse == 1) {
                 const double hp = valid ? hscale * (double)bs[jj] : 0.0;    // h' = log2(e) h
                 double w = 0.0;
                 for (int d = 0; d < D; ++d) {
@@ -207,6 +209,16 @@ __global__ void __launch_bounds__(256) pack_local_kernel(const float *__restrict
             }
             rec[2 * D + h] = local ? (float)(-w) : 0.0f;
             for (int e = 0; e < E; ++e) rec[2 * D + 2 + 2 * e + h] = valid ? bs[jj * E + e] : 0.0f;
+            if (lse == 2) {                                  // gradient records (E = 1, R18g)
+                rec[2 * D + h] = 0.0f;
+                if (local) {
+                    const float bp = (float)((valid ? (double)bs[jj] : 0.0) * exp2(-w));
+                    rec[2 * D + 2 + h] = bp;
+                    for (int d = 0; d < D; ++d) rec[2 * D + 4 + 2 * d + h] = bp * rec[2 * d + h];
+                } else {
+                    for (int d = 0; d < D; ++d) rec[2 * D + 4 + 2 * d + h] = 0.0f;
+                }
+            }
         }
         __syncthreads();
         float4 *dst = reinterpret_cast<float4 *>(J + blk * 256 * RS);
@@ -239,7 +251,7 @@ cudaError_t launch_tile_order(const float *y, const float *b, int64_t N, int D, 
     e = cub::DeviceRadixSort::SortPairs(temp, tb, (const uint32_t *)keys, keys_s, (const uint32_t *)idx, perm,
                                         (int)N, 0, end_bit, st);
     if (e != cudaSuccess) return e;
-    const int RS = lse ? RS_lse : pack_record_stride(PACK_GAUSS_AUTO, D, E);
+    const int RS = lse == 1 ? RS_lse : pack_record_stride(lse == 2 ? PACK_GAUSS_AUTO_RAW : PACK_GAUSS_AUTO, D, E);
     const int smem = (kTileJ * (D + E) + 256 * RS) * 4;
     if (smem > 48 * 1024) {
         e = smem_opt_in((const void *)pack_local_kernel, 96 * 1024);

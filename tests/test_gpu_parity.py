@@ -506,6 +506,33 @@ def test_gauss_sum_tile_centred_form(G, monkeypatch, case):
     np.testing.assert_array_equal(host(a2), host(a))
 
 
+@pytest.mark.parametrize("formula", ["gauss_gradx", "gauss_sum_gradx"])
+@pytest.mark.parametrize("case", ["u3_s025", "u3_s005_mixed", "gmm_signed", "far_offset", "outliers", "global_box"])
+def test_gradient_tile_centred_form(G, monkeypatch, formula, case):
+    """The gradient modes in the tile-centred form (R18j with R18g's records per tile): the
+    x-gradient (with a cotangent) and the fused Sum + gradient against the oracle at the plain
+    R4 bar, every row."""
+    option(G, monkeypatch, "local_form", 2)
+    x, y, b, sigma, expect = _local_case(case)
+    g = synth.cotangent(len(x), 77)
+    if formula == "gauss_gradx":
+        gx = G.eval(formula, "sum", dev(x), dev(y), dev(b), dev(g), scale=sigma)
+        s = None
+    else:
+        s, gx = G.eval(formula, "sum", dev(x), dev(y), dev(b), scale=sigma)
+    plan = G.last_plan()
+    loc, tot = G.last_tiles()
+    if expect == "global":
+        assert plan["path"] == 2, plan
+    else:
+        assert plan["path"] == 3 and ((loc == tot) if expect == "all" else (0 < loc < tot)), (plan, loc, tot)
+    og, deng = oracle.gauss_gradx(x, y, b, g if s is None else None, sigma=sigma)
+    assert_sum_parity(host(gx), og, deng, what=f"tile-centred {formula} {case} grad")
+    if s is not None:
+        o, den = oracle.gauss_sum(x, y, b, sigma=sigma)
+        assert_sum_parity(host(s), o, den, what=f"tile-centred {formula} {case} sum")
+
+
 @pytest.mark.parametrize("split", [1, 3, 40])
 def test_tile_centred_splits_and_ishards(G, monkeypatch, split):
     """The tile-centred form with forced j-splits (rounded to whole 512-j tiles) against the
