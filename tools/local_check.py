@@ -106,6 +106,26 @@ def lse_timing():
     G.set_option("local_form", 1)
 
 
+def grad_timing():
+    for formula in ("gauss_sum_gradx", "gauss_gradx"):
+        M = N = 1_000_000
+        x = dev(synth.uniform3(M, 1)); y = dev(synth.uniform3(N, 2)); b = dev(synth.signal(N, 3))
+        for lf in (0, 1):
+            G.set_option("local_form", lf)
+            for _ in range(2):
+                G.eval(formula, "sum", x, y, b, scale=0.05)
+            torch.cuda.synchronize()
+            G.profile(True)
+            for _ in range(3):
+                G.eval(formula, "sum", x, y, b, scale=0.05)
+            ms = G.profile_read()
+            G.profile(False)
+            plan = G.last_plan()
+            print(f"{formula} M=N=1e6 sigma=0.05 local_form={lf} path={plan['path']} tiles={G.last_tiles()} "
+                  f"kernel {min(ms):.2f} ms pairs/clk/SM {M * N / (min(ms) * 1e-3) / (148 * 1.965e9):.2f}", flush=True)
+    G.set_option("local_form", 1)
+
+
 def timing():
     for (M, N, sig) in [(2_000_000, 2_000_000, 0.05), (1_000_000, 1_000_000, 0.05), (1_000_000, 1_000_000, 0.1)]:
         x = dev(synth.uniform3(M, 1)); y = dev(synth.uniform3(N, 2)); b = dev(synth.signal(N, 3))
@@ -141,3 +161,5 @@ if __name__ == "__main__":
         lse_parity()
     if "lsetime" in what:
         lse_timing()
+    if "gradtime" in what:
+        grad_timing()
