@@ -41,6 +41,7 @@ struct genred_ctx {
     bool small_fused = true;                                   // genred_set_option("small_fused")
     bool fused_merge = true;                                   // genred_set_option("fused_merge")
     int local_form = 1;                                        // genred_set_option("local_form")
+    bool split_major = true;                                   // genred_set_option("split_major")
     const float4 *centers_dev = nullptr;                       // last tile-centred call: per-tile
     int64_t centers_n = 0;                                     //   (centre, r^2 or -1)
     bool profiling = false;
@@ -172,6 +173,7 @@ constexpr int64_t kSmmMaxM = 64;             // small-M mode for M at or below
 constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
 // Tile-centred form of the Gaussian Sum (R18j, tile_order.cu), option local_form = 1: for N and M
 // at or above these (the sort's cost, ~N, against the pair loop's M N)
+constexpr size_t kL2SplitBytes = (size_t)48 << 20;   // j-records per split in the split-major order
 constexpr int64_t kLocalMinN = 1 << 18;
 constexpr int64_t kLocalMinM = 1 << 16;
 
@@ -570,6 +572,17 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
                            !smm && D <= 3 && N > kDirectMaxN && M > kDirectMaxM &&
                            N < ((int64_t)1 << 31) &&
                            (ctx->local_form == 2 || (ctx->local_form == 1 && N >= kLocalMinN && M >= kLocalMinM));
+        // Large j-record sets (C5: 240 MB, twice the L2): at least enough j-splits for one split's
+        // records to fit kL2SplitBytes, and the CTAs ordered split by split, so the resident
+        // CTAs share one split's records in L2 instead of re-streaming them from DRAM per wave.
+        const bool split_major = ctx->split_major && !smm && (size_t)npairs * RS * 4 > kL2SplitBytes;
+        if (split_major && a->split_j <= 0) {
+            const int64_t smin = (int64_t)(((size_t)npairs * RS * 4 + kL2SplitBytes - 1) / kL2SplitBytes);
+            if (pl.split < smin) {
+                pl.pairs_per_split = ((pl.npv + smin - 1) / smin + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+                pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
+            }
+        }
         if (local) {
             const int64_t P = kTileJ / 2;
             pl.pairs_per_split = (pl.pairs_per_split + P - 1) / P * P;
@@ -684,6 +697,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         L.scale_sum = 1.0; L.scale_grad = scale_grad; L.out = a->out; L.out_f64 = out_f64;
         L.out_grad = a->out_grad; L.part = part; L.geo = geo; L.units = nullptr; L.n_units = 0;
         L.centers = centers;
+        L.split_major = split_major ? 1 : 0;
         // Few partials per row tile: the last CTA of each row tile merges them (no finalize
         // launch); the merge tail is bounded at 16 K fp64 reads for that CTA.  Only up to 32
         // splits: above that the finalize kernel sums lane-strided (sum_finalize_warp_kernel),
@@ -950,6 +964,7 @@ genred_status genred_create(int32_t cuda_device, genred_ctx **out) {
     if (const char *v = getenv("GENRED_SMALL_FUSED")) ctx->small_fused = atoi(v) != 0;
     if (const char *v = getenv("GENRED_FUSED_MERGE")) ctx->fused_merge = atoi(v) != 0;
     if (const char *v = getenv("GENRED_LOCAL_FORM")) ctx->local_form = atoi(v);
+    if (const char *v = getenv("GENRED_SPLIT_MAJOR")) ctx->split_major = atoi(v) != 0;
     cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, cuda_device);
     cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, cuda_device);
     cudaSetDevice(prev);
@@ -1129,6 +1144,7 @@ genred_status genred_set_option(genred_ctx *ctx, const char *name, int64_t value
     const std::string n(name);
     if (n == "small_fused") { ctx->small_fused = value != 0; return GENRED_OK; }
     if (n == "fused_merge") { ctx->fused_merge = value != 0; return GENRED_OK; }
+    if (n == "split_major") { ctx->split_major = value != 0; return GENRED_OK; }
     if (n == "local_form") {
         if (value < 0 || value > 2) return fail(ctx, GENRED_E_INVALID, "local_form is 0, 1 or 2");
         ctx->local_form = (int)value;

@@ -115,6 +115,7 @@ struct SumLaunch {
     // MODE 0, tile-centred form (tile_order.cu, R18j): per 512-j tile (centre, radius^2 or -1 =
     // direct layout); pairs_per_split is then a multiple of kTileJ / 2
     const float4 *centers = nullptr;
+    int split_major = 0;      // row-tile CTAs ordered split by split (L2 residency of a split's records)
 };
 cudaError_t launch_sum(const SumLaunch &a, cudaStream_t st, int *ctas);
 // Tile-centred form (tile_order.cu): Hilbert keys of y over its box (geo), a radix sort of

@@ -96,6 +96,8 @@ struct SumParams {
     double *part_smem = nullptr;   // sum_small_kernel with a cluster merge: this CTA's partials go
                                    // to its own shared memory, [local row][C], not to `part`
     const float4 *centers = nullptr;   // MODE 0 tile-centred form: per 512-j tile (c_k, r_k^2 or -1)
+    int split_major = 0;      // row tiles: work unit w -> (split w / itiles, row tile w % itiles)
+    int64_t itiles = 0;       // row tiles (split_major)
 };
 
 // (Round 1, at 3 CTAs/SM: moving 1/8 (1/4) of the exps to the FP32 pipe measured 14.74 (13.73)
@@ -884,8 +886,16 @@ sum_kernel(const SumParams p) {
         q0 = (int64_t)sp * p.pairs_per_split;
         npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);
     } else {
-        const int64_t itile = w / p.split;
-        sp = (int)(w % p.split);
+        // split-major (large j-record sets): the CTAs resident at any time stream the same j-split,
+        // whose records then stay in L2 (one DRAM read per split, not one per wave)
+        int64_t itile;
+        if (p.split_major) {
+            itile = w % p.itiles;
+            sp = (int)(w / p.itiles);
+        } else {
+            itile = w / p.split;
+            sp = (int)(w % p.split);
+        }
         q0 = (int64_t)sp * p.pairs_per_split;
         npc = max(min(q0 + p.pairs_per_split, p.npv) - q0, (int64_t)0);   // empty: zero partial
         row0 = itile * (int64_t)(kConsumerWarps * 32 * R);
@@ -920,7 +930,8 @@ sum_kernel(const SumParams p) {
         Geo geo{};
         sum_body<MODE, D, E, R, false, SMM>(p, ring, nt, last_np, row0, row_end, sp, geo);
     }
-    if (!SMM && p.tile_done && !p.units) sum_tile_merge<MODE, D, E, R>(p, w / p.split, row0, row_end);
+    if (!SMM && p.tile_done && !p.units)
+        sum_tile_merge<MODE, D, E, R>(p, p.split_major ? w % p.itiles : w / p.split, row0, row_end);
     }
 }
 

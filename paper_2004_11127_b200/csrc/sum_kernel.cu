@@ -55,6 +55,8 @@ static cudaError_t run_sum(const SumLaunch &a, cudaStream_t st, int *ctas) {
     p.scale_sum = a.scale_sum; p.scale_grad = a.scale_grad; p.out = a.out; p.out_f64 = a.out_f64;
     p.out_grad = a.out_grad; p.part = a.part; p.geo = a.geo; p.units = a.units;
     p.centers = a.centers;
+    p.split_major = a.split_major;
+    p.itiles = (a.M + (int64_t)kConsumerWarps * 32 * R - 1) / ((int64_t)kConsumerWarps * 32 * R);
     p.tile_done = a.split > 1 ? a.tile_done : nullptr;
     const int64_t rows = (int64_t)kConsumerWarps * 32 * R;
     const int64_t itiles = (a.M + rows - 1) / rows;
