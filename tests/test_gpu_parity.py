@@ -1008,6 +1008,39 @@ def test_gauss_cg_cuda_graph_matches_eager(G):
     assert ig["rel_residual"] == ie["rel_residual"]
 
 
+@pytest.mark.parametrize("formula,red", [("gauss", "sum"), ("sqdist", "lse")])
+def test_tile_centred_call_captured_in_cuda_graph(G, monkeypatch, formula, red):
+    """A tile-centred call (key, sort, pack and pair-loop launches, R18j) captured in a CUDA graph
+    after one eager call of the same shape, replayed on new inputs: bitwise the eager results."""
+    option(G, monkeypatch, "local_form", 2)
+    M, N = 5000, 40000
+    x1, y1 = synth.uniform3(M, 61), synth.uniform3(N, 62)
+    x2, y2 = synth.uniform3(M, 63), synth.uniform3(N, 64)
+    b1, b2 = synth.signal(N, 65), synth.signal(N, 66)
+    xd, yd, bd = dev(x1), dev(y1), dev(b1)
+    kw = dict(scale=0.1) if red == "sum" else dict(scale=0.02, out_dtype="float64")
+    bb = bd if red == "sum" else None
+    out = torch.empty((M, 1), dtype=torch.float32, device="cuda") if red == "sum" else \
+        torch.empty((M,), dtype=torch.float64, device="cuda")
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        G.eval(formula, red, xd, yd, bb, out=out, **kw)            # warm-up: scratch sized
+    torch.cuda.synchronize()
+    assert G.last_plan()["path"] == 3
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph, stream=s):
+        G.eval(formula, red, xd, yd, bb, out=out, **kw)
+    res = []
+    for xx, yy, bbv in ((x1, y1, b1), (x2, y2, b2)):
+        xd.copy_(dev(xx)); yd.copy_(dev(yy)); bd.copy_(dev(bbv))
+        graph.replay()
+        torch.cuda.synchronize()
+        res.append(host(out).copy())
+        ref = G.eval(formula, red, dev(xx), dev(yy), dev(bbv) if red == "sum" else None, **kw)
+        np.testing.assert_array_equal(res[-1], host(ref))
+    assert not np.array_equal(res[0], res[1])
+
+
 def test_kmeans_assignment_and_monotone_objective(G):
     from paper_2004_11127_b200.solvers import kmeans
     x = synth.gmm3(20000, 131)
