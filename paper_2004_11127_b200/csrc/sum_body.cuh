@@ -24,6 +24,10 @@ namespace genred {
 #ifndef GENRED_GRAD_MINB
 #define GENRED_GRAD_MINB 3
 #endif
+// (Round 2: the row-pair loop's 4 accumulating FFMA2s -- a broadcast scalar and two register
+// pairs, 95.8 lane-FMA/clk/SM in tools/hwprobe2.cu, the wall C2 sits at -- split into scalar
+// fma.rn.f32 pairs measured 11.18 against 13.78 pairs/clk/SM: issue-bound,
+// profiles/r02_grad_scalar_acc.txt.)
 // Row-pair packing of the expanded gradient modes (E = 1, records carrying b' and b' y'): the
 // packed FFMA2 lanes hold two ROWS and the j-record value is a broadcast scalar operand, instead
 // of two j's against a per-row broadcast.  Every FFMA2 then reads one fresh scalar + two register
