@@ -579,7 +579,24 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
         if (split_major && a->split_j <= 0) {
             const int64_t smin = (int64_t)(((size_t)npairs * RS * 4 + kL2SplitBytes - 1) / kL2SplitBytes);
             if (pl.split < smin) {
-                pl.pairs_per_split = ((pl.npv + smin - 1) / smin + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+                // the best wave efficiency over [smin, 2 smin] (ties: fewer splits), as the
+                // planner's wave rule: e.g. an 8-way i-shard of C5 (1221 row tiles, 592 slots)
+                // goes from 0.94 at 5 splits to 0.98 at 10
+                const int64_t slots = (int64_t)ctx->num_sms * occupancy(ctx, 0, mode, D, E, pl.R);
+                const int64_t P = local ? kTileJ / 2 : kSplitGrain;
+                double e_best = -1.0;
+                int64_t pps_best = 0;
+                for (int64_t S2 = smin; S2 <= 2 * smin; ++S2) {
+                    const int64_t pps = ((pl.npv + S2 - 1) / S2 + P - 1) / P * P;
+                    const int64_t Se = (pl.npv + pps - 1) / pps;
+                    if (Se < smin) continue;
+                    const int64_t U = pl.itiles * Se, waves = (U + slots - 1) / slots;
+                    const double e2 = (double)U / (double)(waves * slots);
+                    if (e2 > e_best + 1e-9) { e_best = e2; pps_best = pps; }
+                }
+                if (pps_best == 0)
+                    pps_best = ((pl.npv + smin - 1) / smin + kSplitGrain - 1) / kSplitGrain * kSplitGrain;
+                pl.pairs_per_split = pps_best;
                 pl.split = (int)((pl.npv + pl.pairs_per_split - 1) / pl.pairs_per_split);
             }
         }
