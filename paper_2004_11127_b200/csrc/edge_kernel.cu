@@ -7,9 +7,9 @@
 // copy, x loads, store) once per CTA; here instead:
 //   * persistent CTAs (a few per SM) keep the N packed j-records in shared memory for the whole
 //     launch and walk row tiles c, c + grid, ...;
-//   * each 1024-row x tile (contiguous, 1024 * D * 4 bytes) arrives by one cp.async.bulk into a
-//     4-stage shared-memory ring completing on mbarriers, so up to 4 tiles per CTA are in flight
-//     (the bytes in flight per SM, not the thread count, set the achieved HBM bandwidth);
+//   * each 4096-row x tile (contiguous, 4096 * D * 4 bytes) arrives by one cp.async.bulk into a
+//     2-stage shared-memory ring completing on mbarriers (2 CTAs per SM: 192 KB in flight per SM
+//     at D = 3; the bytes in flight per SM, not the thread count, set the achieved HBM bandwidth);
 //   * a thread evaluates its rows from shared memory in the direct form (no bounding-box pass
 //     over x, which would be a second full read) and stores a with coalesced writes.
 // The j-records are the PACK_GAUSS_AUTO direct records (raw -y_j pairs, w slot, b_j pairs;
@@ -24,14 +24,18 @@
 namespace genred {
 namespace edge {
 
+// Round 2: 4096-row tiles in a 2-stage ring (16 rows per thread) measured 0.970 / 0.743 / 0.247
+// of HBM at N = 1 / 8 / 32 against 0.949 / 0.720 / 0.246 for 1024-row tiles in 4 stages (2048 x
+// 3: 0.965 / 0.729; 1024 x 6: 0.688 at N = 8; 512 x 8: 0.604; 4096 x 3: 0.638;
+// profiles/r02_edge_tiles.txt): fewer, larger bulk copies and half the per-tile barriers.
 #ifndef GENRED_EDGE_ROWS
-#define GENRED_EDGE_ROWS 1024
+#define GENRED_EDGE_ROWS 4096
 #endif
 constexpr int kRowsPerTile = GENRED_EDGE_ROWS;
 constexpr int kThreads = 256;
 constexpr int kRows = kRowsPerTile / kThreads;      // rows per thread per tile
 #ifndef GENRED_EDGE_STAGES
-#define GENRED_EDGE_STAGES 4
+#define GENRED_EDGE_STAGES 2
 #endif
 constexpr int kStages = GENRED_EDGE_STAGES;
 constexpr int kMaxPairs = 32;                       // N <= 64
@@ -41,7 +45,7 @@ __global__ void __launch_bounds__(kThreads)
 sum_edge_kernel(const float *__restrict__ x, const float *__restrict__ J, int npairs, int RS,
                 int64_t M, float s, double scale, void *out, int out_f64) {
     extern __shared__ __align__(128) unsigned char smem_raw[];
-    float *xt = reinterpret_cast<float *>(smem_raw);                         // [kStages][1024*D]
+    float *xt = reinterpret_cast<float *>(smem_raw);                         // [kStages][kRowsPerTile*D]
     float *jr = xt + kStages * kRowsPerTile * D;                             // [npairs][RS]
     uint64_t *full = reinterpret_cast<uint64_t *>(jr + kMaxPairs * 12 + 4);
     const int64_t ntiles = (M + kRowsPerTile - 1) / kRowsPerTile;
@@ -150,6 +154,7 @@ static cudaError_t run(const float *x, const float *J, int npairs, int RS, int64
 }  // namespace edge
 
 int sum_edge_max_n() { return 2 * edge::kMaxPairs; }
+int sum_edge_tile_rows() { return edge::kRowsPerTile; }
 
 cudaError_t launch_sum_edge(const float *x, const float *J, int64_t N, int D, int RS, int64_t M, float s,
                             double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas) {

@@ -701,7 +701,7 @@ genred_status eval_device(genred_ctx *ctx, const genred_args *a, cudaStream_t st
             prof_event(ctx, false, st);
             if (e != cudaSuccess) return cuda_fail(ctx, e, "edge sum kernel");
             ctx->launches += kernels;
-            ctx->plan.split_j = 1; ctx->plan.rows_per_cta = 1024; ctx->plan.ctas = ctas;
+            ctx->plan.split_j = 1; ctx->plan.rows_per_cta = sum_edge_tile_rows(); ctx->plan.ctas = ctas;
             ctx->plan.kernels = kernels; ctx->plan.path = 0; ctx->plan.tile_j = (int32_t)N;
             ctx->plan.scratch_bytes = (int64_t)ctx->scratch_need;
             ctx->geo_dev = nullptr;

@@ -239,6 +239,7 @@ cudaError_t launch_knn_tc(const KnnTcLaunch &a, cudaStream_t st, KnnTcInfo *info
 // Gaussian Sum at the HBM-bound edge (edge_kernel.cu): N <= sum_edge_max_n(), D <= 4, E = 1,
 // x 16-byte aligned; J = the PACK_GAUSS_AUTO direct records (geo = nullptr).
 int sum_edge_max_n();
+int sum_edge_tile_rows();   // x rows per bulk-copied tile of the edge kernel
 cudaError_t launch_sum_edge(const float *x, const float *J, int64_t N, int D, int RS, int64_t M, float s,
                             double scale, void *out, int out_f64, int num_sms, cudaStream_t st, int *ctas);
 
