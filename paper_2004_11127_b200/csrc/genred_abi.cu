@@ -29,6 +29,8 @@ struct genred_ctx {
     size_t scratch_need = 0;                                   // bytes the last call used
     void *stage = nullptr;
     size_t stage_cap = 0;
+    void *hstage = nullptr;                                    // pinned host gather buffer (small
+    size_t hstage_cap = 0;                                     //   GENRED_MEM_HOST calls)
     genred_plan plan{};
     int64_t launches = 0;
     std::map<std::tuple<int, int, int, int, int>, int> occ;   // (kind, a, b, c, R) -> CTAs/SM
@@ -173,7 +175,8 @@ constexpr int64_t kSmmMaxM = 64;             // small-M mode for M at or below
 constexpr int64_t kMinSmmPairs = 512;        // small-M mode: shortest j-split (1024 j)
 // Tile-centred form of the Gaussian Sum (R18j, tile_order.cu), option local_form = 1: for N and M
 // at or above these (the sort's cost, ~N, against the pair loop's M N)
-constexpr size_t kL2SplitBytes = (size_t)48 << 20;   // j-records per split in the split-major order
+constexpr size_t kL2SplitBytes = (size_t)48 << 20;
+constexpr size_t kHostGatherMax = (size_t)1 << 20;   // GENRED_MEM_HOST inputs gathered into one copy   // j-records per split in the split-major order
 constexpr int64_t kLocalMinN = 1 << 18;
 constexpr int64_t kLocalMinM = 1 << 16;
 
@@ -1000,6 +1003,7 @@ void genred_destroy(genred_ctx *ctx) {
     cudaSetDevice(ctx->device);
     if (ctx->scratch) cudaFree(ctx->scratch);
     if (ctx->stage) cudaFree(ctx->stage);
+    if (ctx->hstage) cudaFreeHost(ctx->hstage);
     if (ctx->tile_done) cudaFree(ctx->tile_done);
     for (cudaEvent_t e : ctx->ev) cudaEventDestroy(e);
     cudaSetDevice(prev);
@@ -1048,7 +1052,31 @@ genred_status genred_eval(genred_ctx *ctx, const genred_args *args, void *stream
                                    (const void **)&d.g, (const void **)&d.row_shift,
                                    (const void **)&d.col_shift};
             const int slot[6] = {0, 1, 2, 3, 8, 9};
-            for (int k = 0; k < 6 && s == GENRED_OK; ++k) {
+            // Small inputs (C1-like: launch-latency bound) are gathered on the host into a pinned
+            // buffer with the device layout and sent by ONE copy; large ones go one copy each.
+            size_t in_bytes = 0, in_end = 0;
+            for (int k = 0; k < 6; ++k)
+                if (src[k] && sz[slot[k]] > 0) { in_bytes += sz[slot[k]]; in_end = off[slot[k]] + sz[slot[k]]; }
+            bool gathered = false;
+            if (in_bytes > 0 && in_bytes <= kHostGatherMax) {
+                if (ctx->hstage_cap < in_end) {
+                    if (ctx->hstage) { cudaFreeHost(ctx->hstage); ctx->hstage = nullptr; ctx->hstage_cap = 0; }
+                    const size_t cap = std::max<size_t>(in_end, (size_t)1 << 20);
+                    if (cudaMallocHost(&ctx->hstage, cap) == cudaSuccess) ctx->hstage_cap = cap;
+                    else { cudaGetLastError(); ctx->hstage = nullptr; }
+                }
+                if (ctx->hstage) {
+                    for (int k = 0; k < 6; ++k) {
+                        if (!src[k] || sz[slot[k]] == 0) continue;
+                        *dst[k] = base + off[slot[k]];
+                        memcpy((char *)ctx->hstage + off[slot[k]], src[k], sz[slot[k]]);
+                    }
+                    cudaError_t e = cudaMemcpyAsync(base, ctx->hstage, in_end, cudaMemcpyHostToDevice, st);
+                    if (e != cudaSuccess) s = cuda_fail(ctx, e, "H2D copy");
+                    gathered = true;
+                }
+            }
+            for (int k = 0; k < 6 && s == GENRED_OK && !gathered; ++k) {
                 if (!src[k] || sz[slot[k]] == 0) continue;
                 *dst[k] = base + off[slot[k]];
                 cudaError_t e = cudaMemcpyAsync(base + off[slot[k]], src[k], sz[slot[k]], cudaMemcpyHostToDevice, st);
