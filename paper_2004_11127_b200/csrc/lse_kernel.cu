@@ -409,6 +409,9 @@ __device__ __noinline__ LseRescale lse_local_rescale(const float *base, const fl
 
 // (1/8 of the exponentials on the FP32 pipe, as the Sum: 14.54 against 14.63 pairs/clk/SM with
 // h = 0 and 14.14 against 14.46 with h at C3's shape -- not used; 3 CTAs/SM the same as 4)
+#ifndef GENRED_CEN_PREFETCH
+#define GENRED_CEN_PREFETCH 1
+#endif
 #ifndef GENRED_LSE_POLY
 #define GENRED_LSE_POLY 0
 #endif
@@ -442,8 +445,16 @@ __global__ void __launch_bounds__(kThreads, HZ ? GENRED_LSE_LOC_MINB : 3) lse_lo
 #pragma unroll
     for (int q = 0; q < RQ; ++q) S32[q] = make_float2(0.f, 0.f);
     const int64_t tile0 = q0 / Cfg::PAIRS;
+#if GENRED_CEN_PREFETCH
+    float4 cen_next = nt > 0 ? __ldg(p.centers + tile0) : make_float4(0.f, 0.f, 0.f, -1.f);
+#endif
     for (int k = 0; k < nt; ++k) {
+#if GENRED_CEN_PREFETCH
+        const float4 cen = cen_next;                 // loaded one tile ahead
+        if (k + 1 < nt) cen_next = __ldg(p.centers + tile0 + k + 1);
+#else
         const float4 cen = __ldg(p.centers + tile0 + k);
+#endif
         const bool loc = cen.w >= 0.0f;
         const float cc[3] = {cen.x, cen.y, cen.z};
         // this tile's frame: 2 x'' (or raw x), m' = fl32(M - o), M moved to m' + o

@@ -46,6 +46,11 @@ namespace genred {
 #ifndef GENRED_SUM_MINB
 #define GENRED_SUM_MINB 4
 #endif
+// Tile-centred loops: each tile's table entry (c_k, r_k^2) loaded one tile ahead (fused gradient
+// at sigma = 0.05: 13.15 -> 13.61 pairs/clk/SM; Sum and LSE unchanged)
+#ifndef GENRED_CEN_PREFETCH
+#define GENRED_CEN_PREFETCH 1
+#endif
 #ifndef GENRED_GRAD_HH
 #define GENRED_GRAD_HH 16
 #endif
@@ -528,8 +533,16 @@ __device__ __forceinline__ void sum_body_local(const SumParams &p, Ring &ring, i
 #pragma unroll
         for (int e = 0; e < E; ++e) acc64[r][e] = 0.0;
     }
+#if GENRED_CEN_PREFETCH
+    float4 cen_next = nt > 0 ? __ldg(p.centers + tile0) : make_float4(0.f, 0.f, 0.f, -1.f);
+#endif
     for (int k = 0; k < nt; ++k) {
+#if GENRED_CEN_PREFETCH
+        const float4 cen = cen_next;                 // loaded one tile ahead
+        if (k + 1 < nt) cen_next = __ldg(p.centers + tile0 + k + 1);
+#else
         const float4 cen = __ldg(p.centers + tile0 + k);
+#endif
         const float *tile = ring.acquire(k);
         const int np = k == nt - 1 ? last_np : Cfg::PAIRS;
         float2 acc[R][E];
@@ -668,8 +681,16 @@ __device__ __forceinline__ void sum_body_local_grad(const SumParams &p, Ring &ri
     for (int r = 0; r < R; ++r)
 #pragma unroll
         for (int c = 0; c < C; ++c) acc64[r][c] = 0.0;
+#if GENRED_CEN_PREFETCH
+    float4 cen_next = nt > 0 ? __ldg(p.centers + tile0) : make_float4(0.f, 0.f, 0.f, -1.f);
+#endif
     for (int k = 0; k < nt; ++k) {
+#if GENRED_CEN_PREFETCH
+        const float4 cen = cen_next;                 // loaded one tile ahead
+        if (k + 1 < nt) cen_next = __ldg(p.centers + tile0 + k + 1);
+#else
         const float4 cen = __ldg(p.centers + tile0 + k);
+#endif
         const bool loc = cen.w >= 0.0f;
         const float cc[3] = {cen.x, cen.y, cen.z};
         const float lim = loc ? sqrtf(cen.w) + 11.5f : 0.0f;
